@@ -1,0 +1,160 @@
+/*
+ * libhopgnn — C ABI of the B200 (sm_100a) HopGNN micrograph training step.
+ *
+ * Drop-in boundary: the reference's operator layer is the `gnnsim.kernels`
+ * module (reference pkg/src/gnnsim/kernels.py:31-34), which its callers bind
+ * per call from Python.  The first block below replaces those entry points
+ * one for one (same argument meaning; device pointers instead of numpy
+ * arrays).  The rest is the batched hot path the reference runs as per-root
+ * Python loops (sampler.py:84-106, model.py:183-329, engine.py:413-448).
+ *
+ * Conventions:
+ *   - every function returns hg_status (0 = ok); hg_last_error() describes
+ *     the last failure of the calling thread;
+ *   - all array arguments are caller-owned DEVICE pointers unless the name
+ *     ends in _host; nothing is allocated inside except where a *_ws
+ *     workspace size query says so;
+ *   - every function takes a cudaStream_t (as void*) and is asynchronous;
+ *     kernels that detect a data-dependent error (root out of range,
+ *     capacity overflow) set *err_flag (device int) instead of trapping;
+ *   - no C++ exception crosses the ABI; no torch types in signatures.
+ */
+#ifndef HOPGNN_H_
+#define HOPGNN_H_
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HG_OK = 0,
+  HG_ERANGE = 1,      /* maps to ValueError (sampler.py:86-87, model.py:223-224) */
+  HG_ECONFIG = 2,     /* maps to ConfigError (errors.py:4)                       */
+  HG_EINVARIANT = 3,  /* maps to InvariantViolation (errors.py:8)                */
+  HG_ECUDA = 4,       /* CUDA runtime failure                                    */
+  HG_ENCCL = 5,       /* NCCL failure                                            */
+  HG_ECAPACITY = 6    /* caller buffer too small                                 */
+} hg_status;
+
+#define HG_MAX_LAYERS 6
+
+const char* hg_last_error(void);
+int hg_version(void);
+int hg_device_sync(void* stream); /* cudaStreamSynchronize + error-flag check */
+
+/* ------------------------------------------------------------------------
+ * 1. Reference kernel boundary (gnnsim.kernels, kernels.py:31-34)
+ * --------------------------------------------------------------------- */
+
+/* replaces kernels.sample_frontier (_kernels_nb.py:55-90 / _kernels_np.py:55-84).
+ * offsets int64[n+1], targets int32[m], frontier int64[f].  Outputs
+ * counts_out int64[f] and flat_out int64[flat_cap]; *flat_len_host receives
+ * sum(counts) (this call synchronises `stream` to report it). */
+int hg_sample_frontier(const int64_t* offsets, const int32_t* targets, int64_t n_vertices,
+                       const int64_t* frontier, int64_t n_frontier, int32_t fanout,
+                       uint64_t state, int64_t* counts_out, int64_t* flat_out,
+                       int64_t flat_cap, int64_t* flat_len_host, void* stream);
+
+/* replaces kernels.feature_rows (_kernels_nb.py:109-122): out f32[n, dim]. */
+int hg_feature_rows(const int64_t* ids, int64_t n, int32_t dim, uint64_t state, float* out,
+                    void* stream);
+
+/* ------------------------------------------------------------------------
+ * 2. Counter RNG products (rng.py, engine.py:268-287, model.py:69-109)
+ * --------------------------------------------------------------------- */
+
+/* Feature table init: row v of a shard = feature_rows(v) (featstore.py:161-184).
+ * Writes rows for ids [first, first+count) into out with row stride `ld`
+ * elements (ld >= dim, padding columns zeroed).  dtype 0 = f32, 1 = bf16 (RNE). */
+int hg_feature_table(int64_t first, int64_t count, int32_t dim, int32_t ld, uint64_t state,
+                     int32_t dtype, void* out, void* stream);
+
+/* Epoch permutation: stable argsort of chain(state, v) for v < n
+ * (engine.py:273-275).  perm_out int64[n].  ws_bytes query when ws == NULL. */
+int hg_epoch_permutation(int64_t n, uint64_t state, int64_t* perm_out, void* ws,
+                         size_t* ws_bytes, void* stream);
+
+/* Glorot init (model.py:87-90): out f64 or f32 [rows*cols] row-major. */
+int hg_glorot(int32_t rows, int32_t cols, uint64_t state, int32_t dtype, void* out,
+              void* stream);
+
+/* ------------------------------------------------------------------------
+ * 3. Synthetic graph generator (oracle/graphgen.py twin)
+ * --------------------------------------------------------------------- */
+typedef struct {
+  int64_t n;
+  int32_t n_blocks;
+  int32_t n_levels;
+  uint64_t key;           /* row key base: slot draws use mix64(key ^ v) */
+  uint64_t deg_key;       /* chain(key, 0xDE): row-length draw           */
+  uint32_t thr_in;        /* in-block acceptance threshold on hi32 (0..2^32-1) */
+  int32_t in_always;      /* 1 when p_in >= 1 or n_blocks == 1 */
+  int64_t block_start[65];
+  uint64_t a[64], c[64], a_inv[64];
+  uint64_t cum[64];
+  int64_t lvl_size[64], deg_lo[64], deg_span[64];
+} hg_graph_tables;
+
+/* Pass 1: raw row lengths (pre-dedup) -> raw_deg int64[n]. */
+int hg_graph_raw_degrees(const hg_graph_tables* t, int64_t* raw_deg, void* stream);
+/* Pass 2: slots of rows [v0, v1) into raw_targets at raw_off[v]-raw_off[v0]. */
+int hg_graph_fill(const hg_graph_tables* t, int64_t v0, int64_t v1, const int64_t* raw_off,
+                  int32_t* raw_targets, void* stream);
+/* Pass 3: per-row sort + unique + self-loop drop in place; row_len int64[v1-v0]. */
+int hg_graph_canonicalize(int64_t v0, int64_t v1, const int64_t* raw_off, int32_t* raw_targets,
+                          int64_t* row_len, void* ws, size_t* ws_bytes, void* stream);
+/* Pass 4: compact canonical rows into targets at offsets[v]. */
+int hg_graph_compact(int64_t v0, int64_t v1, const int64_t* raw_off, const int32_t* raw_targets,
+                     const int64_t* offsets, int32_t* targets, void* stream);
+/* inclusive/exclusive scans used by the host orchestration */
+int hg_exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, void* ws,
+                          size_t* ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * 4. Micrograph batch: sampling + dedup/relabel + need-chain plan
+ *    (sampler.py:84-106, model.py:183-198)
+ * --------------------------------------------------------------------- */
+typedef struct {
+  int32_t n_layers;                    /* L */
+  int32_t fanout[HG_MAX_LAYERS];       /* fanout[h-1] for hop h (hop 1 = root's neighbours) */
+  int32_t cap_lay[HG_MAX_LAYERS + 1];  /* per-root capacity of layers[k] */
+  int32_t cap_need[HG_MAX_LAYERS + 1]; /* per-root capacity of need[k] */
+  int32_t cand_cap;                    /* per-task candidate buffer (threshold select) */
+  int32_t sort_cap;                    /* power-of-two smem sort buffer */
+  int32_t smem_bytes;                  /* dynamic smem of the build kernel */
+  int32_t ws_root_ints;                /* padded per-root workspace (int32 words) */
+} hg_mg_layout;
+
+typedef struct {
+  /* compact outputs, global row numbering; index k = layer 0..L */
+  int32_t* need_ids[HG_MAX_LAYERS + 1];  /* vertex ids of need[k] rows                */
+  int32_t* need_off[HG_MAX_LAYERS + 1];  /* [R+1] first row of each root in need[k]    */
+  int8_t* in_layer[HG_MAX_LAYERS + 1];   /* 1 iff the need[k] row is in layers[k]      */
+  int32_t* self_pos[HG_MAX_LAYERS + 1];  /* k>=1: row of the same vertex in need[k-1]  */
+  int32_t* nbr_off[HG_MAX_LAYERS + 1];   /* k>=1: [N_k+1] CSR of sampled pairs by dst  */
+  int32_t* nbr_idx[HG_MAX_LAYERS + 1];   /* k>=1: need[k-1] row of each pair's source  */
+  int32_t* pair_off[HG_MAX_LAYERS + 1];  /* k>=1: [R+1] first pair of each root         */
+  int32_t* totals;                       /* [2L+2]: N_0..N_L, P_1..P_L, err             */
+} hg_mg_batch;
+
+/* Fill capacities / smem / workspace for a fanout list; returns HG_ECONFIG if
+ * the per-root tile does not fit in shared memory. */
+int hg_mg_plan_layout(int32_t n_layers, const int32_t* fanout, hg_mg_layout* out);
+
+/* Sample + build micrographs for n_roots roots.  Root i uses stream key
+ * mix64(iter_state[i / roots_per_state] ^ roots[i]) where iter_state holds
+ * chain(sampler_seed, epoch, iteration) (sampler.py:52-54), or, when
+ * roots_per_state == 0, iter_state[i] itself (caller-made keys); ws must hold
+ * n_roots * layout.ws_root_ints int32 words.  err_flag: device int. */
+int hg_mg_build(const int64_t* offsets, const int32_t* targets, int64_t n_vertices,
+                const int64_t* roots, int32_t n_roots, const uint64_t* iter_state,
+                int32_t roots_per_state, const hg_mg_layout* layout, int32_t* ws,
+                hg_mg_batch* out, int* err_flag, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HOPGNN_H_ */

@@ -1,0 +1,119 @@
+"""ctypes binding of libhopgnn.so (include/hopgnn.h).
+
+The product path has no fallback: if the shared library is missing or does
+not load, every entry point raises ``RuntimeError`` (the CUDA extension is
+the only implementation).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .errors import ConfigError, InvariantViolation
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libhopgnn.so")
+MAX_LAYERS = 6
+
+_lib = None
+
+
+class MgLayout(C.Structure):
+    _fields_ = [("n_layers", C.c_int32),
+                ("fanout", C.c_int32 * MAX_LAYERS),
+                ("cap_lay", C.c_int32 * (MAX_LAYERS + 1)),
+                ("cap_need", C.c_int32 * (MAX_LAYERS + 1)),
+                ("cand_cap", C.c_int32),
+                ("sort_cap", C.c_int32),
+                ("smem_bytes", C.c_int32),
+                ("ws_root_ints", C.c_int32)]
+
+
+_P7 = C.c_void_p * (MAX_LAYERS + 1)
+
+
+class MgBatch(C.Structure):
+    _fields_ = [("need_ids", _P7), ("need_off", _P7), ("in_layer", _P7), ("self_pos", _P7),
+                ("nbr_off", _P7), ("nbr_idx", _P7), ("pair_off", _P7), ("totals", C.c_void_p)]
+
+
+class GraphTables(C.Structure):
+    _fields_ = [("n", C.c_int64), ("n_blocks", C.c_int32), ("n_levels", C.c_int32),
+                ("key", C.c_uint64), ("deg_key", C.c_uint64), ("thr_in", C.c_uint32), ("in_always", C.c_int32),
+                ("block_start", C.c_int64 * 65), ("a", C.c_uint64 * 64),
+                ("c", C.c_uint64 * 64), ("a_inv", C.c_uint64 * 64), ("cum", C.c_uint64 * 64),
+                ("lvl_size", C.c_int64 * 64), ("deg_lo", C.c_int64 * 64),
+                ("deg_span", C.c_int64 * 64)]
+
+
+V, I32, I64, U64, SZ = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_size_t
+PSZ = C.POINTER(C.c_size_t)
+PI64 = C.POINTER(C.c_int64)
+
+# name -> argtypes (every function returns int status)
+SIGNATURES = {
+    "hg_version": [],
+    "hg_device_sync": [V],
+    "hg_sample_frontier": [V, V, I64, V, I64, I32, U64, V, V, I64, PI64, V],
+    "hg_feature_rows": [V, I64, I32, U64, V, V],
+    "hg_feature_table": [I64, I64, I32, I32, U64, I32, V, V],
+    "hg_epoch_permutation": [I64, U64, V, V, PSZ, V],
+    "hg_glorot": [I32, I32, U64, I32, V, V],
+    "hg_graph_raw_degrees": [C.POINTER(GraphTables), V, V],
+    "hg_graph_fill": [C.POINTER(GraphTables), I64, I64, V, V, V],
+    "hg_graph_canonicalize": [I64, I64, V, V, V, V, PSZ, V],
+    "hg_graph_compact": [I64, I64, V, V, V, V, V],
+    "hg_exclusive_scan_i64": [V, V, I64, V, PSZ, V],
+    "hg_mg_plan_layout": [I32, C.POINTER(I32), C.POINTER(MgLayout)],
+    "hg_mg_build": [V, V, I64, V, I32, V, I32, C.POINTER(MgLayout), V, C.POINTER(MgBatch),
+                    V, V],
+}
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"libhopgnn.so not built ({LIB_PATH}); run `python -m paper_2409_00657_b200.build`"
+                " — there is no CPU fallback")
+        h = C.CDLL(LIB_PATH)
+        for name, args in SIGNATURES.items():
+            fn = getattr(h, name)
+            fn.argtypes = args
+            fn.restype = C.c_int
+        h.hg_last_error.argtypes = []
+        h.hg_last_error.restype = C.c_char_p
+        _lib = h
+    return _lib
+
+
+def check(status: int, what: str = "") -> None:
+    """Map hg_status to the reference's exception types (errors.py:4-12)."""
+    if status == 0:
+        return
+    msg = lib().hg_last_error().decode(errors="replace")
+    if what:
+        msg = f"{what}: {msg}"
+    if status == 1:
+        raise ValueError(msg)
+    if status == 2:
+        raise ConfigError(msg)
+    if status == 3:
+        raise InvariantViolation(msg)
+    raise RuntimeError(f"hopgnn status {status}: {msg}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args), name)
+
+
+def flag_status(code: int, what: str) -> None:
+    """Raise for a device-side error flag read back by the caller."""
+    if code == 0:
+        return
+    if code == 1:
+        raise ValueError(f"{what}: index out of range (device flag)")
+    if code == 3:
+        raise InvariantViolation(f"{what}: device invariant violated")
+    raise RuntimeError(f"{what}: device error flag {code}")

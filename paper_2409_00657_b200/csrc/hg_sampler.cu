@@ -1,0 +1,594 @@
+// Bit-exact k-hop micrograph sampling, dedup/relabel and need-chain plan.
+//
+// Reference semantics:
+//   * draw rule  -- _kernels_nb.py:55-86: deg <= fanout keeps all neighbours
+//     in CSR order; otherwise slot j gets key (mix64(mix64(state^v)^j) & HI32)|j
+//     and the `fanout` smallest keys win, emitted in ascending slot order;
+//   * hop loop   -- sampler.py:92-105 (hop h = L-k uses fanout[h-1] and
+//     state chain(key, h); layers sorted-unique; pairs = searchsorted);
+//   * plan       -- model.py:183-198 (need[k] = union(layers[k], need[k+1]),
+//     self_pos / dpos / spos / deg).
+//
+// B200 design: one CTA (8 warps) owns one root's micrograph in shared memory.
+// Per frontier vertex the draw is a *threshold select*: one hashing pass keeps
+// only slots whose hash is below a threshold sized for ~fanout+4*sqrt(fanout)+8
+// expected survivors (ballot compaction into smem), then the exact `fanout`
+// smallest survivors are ranked in smem.  Cost is one mix64 per slot, no sort
+// of the hub's adjacency.  Vertices with degree <= 1024 are handled by one
+// warp; larger hubs by the whole CTA.  A rare under/overflow of the survivor
+// buffer bisects the threshold and retries, so the result is always exact.
+#include <climits>
+#include <cstdio>
+
+#include <cub/device/device_scan.cuh>
+
+#include "hg_common.cuh"
+
+namespace hg {
+
+constexpr int kBuildThreads = 256;
+constexpr int kBuildWarps = kBuildThreads / 32;
+constexpr int kBigTask = 1024;
+
+struct MgCarve {
+  int L;
+  int fanout[HG_MAX_LAYERS];
+  int mean[HG_MAX_LAYERS];
+  int cap_lay[HG_MAX_LAYERS + 1];
+  int cap_need[HG_MAX_LAYERS + 1];
+  // shared-memory int offsets
+  int sm_lay[HG_MAX_LAYERS + 1], sm_need[HG_MAX_LAYERS + 1];
+  int sm_flat[HG_MAX_LAYERS + 1], sm_cnt[HG_MAX_LAYERS + 1], sm_off[HG_MAX_LAYERS + 1],
+      sm_deg[HG_MAX_LAYERS + 1];
+  int sm_sort, sm_scan, sm_misc, sm_ints;
+  int cand_cap, sort_cap;
+  int cand_byte_off;  // byte offset of the candidate buffers (8-aligned)
+  int smem_bytes;
+  // per-root workspace int offsets
+  int ws_need[HG_MAX_LAYERS + 1], ws_inl[HG_MAX_LAYERS + 1];
+  int ws_self[HG_MAX_LAYERS + 1], ws_rowoff[HG_MAX_LAYERS + 1], ws_nbr[HG_MAX_LAYERS + 1];
+  int ws_cnt, ws_root_ints;
+};
+
+static int pow2ceil(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+static int isqrt_ceil(int x) {
+  int r = 0;
+  while (r * r < x) ++r;
+  return r;
+}
+
+int select_mean(int fanout) { return fanout + 4 * isqrt_ceil(fanout) + 8; }
+
+int make_carve(int L, const int32_t* fanout, MgCarve* c) {
+  if (L < 1 || L > HG_MAX_LAYERS) return hg_fail(HG_ECONFIG, "n_layers must be 1..%d", HG_MAX_LAYERS);
+  *c = MgCarve{};
+  c->L = L;
+  int max_mean = 0;
+  for (int h = 0; h < L; ++h) {
+    if (fanout[h] < 1) return hg_fail(HG_ECONFIG, "fanout must be >= 1");
+    c->fanout[h] = fanout[h];
+    c->mean[h] = select_mean(fanout[h]);
+    max_mean = c->mean[h] > max_mean ? c->mean[h] : max_mean;
+  }
+  c->cap_lay[L] = 1;
+  for (int k = L - 1; k >= 0; --k) {
+    long long v = (long long)c->cap_lay[k + 1] * c->fanout[L - k - 1];
+    if (v > (1 << 16)) return hg_fail(HG_ECONFIG, "micrograph layer capacity %lld too large", v);
+    c->cap_lay[k] = (int)v;
+  }
+  c->cap_need[L] = 1;
+  for (int k = L - 1; k >= 0; --k) c->cap_need[k] = c->cap_lay[k] + c->cap_need[k + 1];
+  c->cand_cap = pow2ceil(2 * max_mean < 64 ? 64 : 2 * max_mean);
+  int mx = 1;
+  for (int k = 0; k <= L; ++k) mx = c->cap_need[k] > mx ? c->cap_need[k] : mx;
+  c->sort_cap = pow2ceil(mx);
+  int o = 0;
+  for (int k = 0; k <= L; ++k) { c->sm_lay[k] = o; o += c->cap_lay[k]; }
+  for (int k = 0; k <= L; ++k) { c->sm_need[k] = o; o += c->cap_need[k]; }
+  for (int h = 1; h <= L; ++h) {
+    int k = L - h;
+    c->sm_flat[h] = o; o += c->cap_lay[k];
+    c->sm_cnt[h] = o; o += c->cap_lay[k + 1];
+    c->sm_off[h] = o; o += c->cap_lay[k + 1] + 1;
+    c->sm_deg[h] = o; o += c->cap_lay[k + 1];
+  }
+  c->sm_sort = o; o += c->sort_cap;
+  c->sm_scan = o; o += 40;
+  c->sm_misc = o; o += 8 + 2 * kBuildWarps + 2 * kBuildWarps;  // counters + T slots
+  c->sm_ints = o;
+  c->cand_byte_off = ((o * 4 + 15) / 16) * 16;
+  c->smem_bytes = c->cand_byte_off + (kBuildWarps + 1) * c->cand_cap * 8;
+  if (c->smem_bytes > 227 * 1024)
+    return hg_fail(HG_ECONFIG, "micrograph tile needs %d B shared memory (> 227 KB)", c->smem_bytes);
+  int w = 0;
+  for (int k = 0; k <= L; ++k) {
+    c->ws_need[k] = w; w += c->cap_need[k];
+    c->ws_inl[k] = w; w += c->cap_need[k];
+  }
+  for (int k = 1; k <= L; ++k) {
+    c->ws_self[k] = w; w += c->cap_need[k];
+    c->ws_rowoff[k] = w; w += c->cap_need[k] + 1;
+    c->ws_nbr[k] = w; w += c->cap_lay[k - 1];
+  }
+  c->ws_cnt = w; w += 2 * L + 2;
+  c->ws_root_ints = w;
+  return HG_OK;
+}
+
+// ---------------------------------------------------------------- team select
+
+struct WarpTeam {
+  __device__ static int rank() { return lane_id(); }
+  __device__ static int size() { return 32; }
+  __device__ static int warp_in_team() { return 0; }
+  __device__ static void sync() { __syncwarp(); }
+};
+struct BlockTeam {
+  __device__ static int rank() { return threadIdx.x; }
+  __device__ static int size() { return blockDim.x; }
+  __device__ static int warp_in_team() { return warp_id(); }
+  __device__ static void sync() { __syncthreads(); }
+};
+
+// Exact "fanout smallest keyed slots" of one frontier vertex, written to out
+// in ascending slot order.  cand: team candidate buffer (cap entries);
+// ctr / tsh: team-private shared scratch.  Requires d > fo.
+template <class Team>
+__device__ void team_select(const int32_t* __restrict__ targets, int64_t lo, int d, int fo,
+                            int mean, uint64_t hv, int32_t* out, uint64_t* cand, int cap,
+                            int* ctr, uint64_t* tsh, int* err) {
+  const int lane = lane_id();
+  uint64_t gh = (uint64_t)mean >= (uint64_t)d ? (1ull << 32)
+                                              : (((uint64_t)mean << 32) / (uint64_t)d);
+  uint64_t lo_b = 0, hi_b = 1ull << 33;
+  int m = 0;
+  for (int attempt = 0;; ++attempt) {
+    if (Team::rank() == 0) *ctr = 0;
+    Team::sync();
+    for (int base = Team::warp_in_team() * 32; base < d; base += Team::size()) {
+      const int j = base + lane;
+      bool take = false;
+      uint64_t key = 0;
+      if (j < d) {
+        const uint64_t h = mix64(hv ^ (uint64_t)j);
+        take = (h >> 32) < gh;
+        key = (h & kHi32) | (uint64_t)j;
+      }
+      const unsigned mask = __ballot_sync(0xffffffffu, take);
+      int off = 0;
+      if (lane == 0 && mask) off = atomicAdd(ctr, __popc(mask));
+      off = __shfl_sync(0xffffffffu, off, 0);
+      const int pos = off + __popc(mask & ((1u << lane) - 1u));
+      if (take && pos < cap) cand[pos] = key;
+    }
+    Team::sync();
+    const int cnt = *ctr;
+    Team::sync();
+    if (cnt >= fo && cnt <= cap) { m = cnt; break; }
+    if (attempt > 80) {  // cannot happen for distinct keys; keep shapes valid
+      raise_flag(err, HG_EINVARIANT);
+      for (int i = Team::rank(); i < fo; i += Team::size()) out[i] = targets[lo + i];
+      Team::sync();
+      return;
+    }
+    if (cnt < fo) lo_b = gh; else hi_b = gh;
+    if (hi_b == (1ull << 33)) {
+      gh = gh * 2 + 1;
+      if (gh > (1ull << 32)) gh = 1ull << 32;
+    } else {
+      gh = (lo_b + hi_b) >> 1;
+    }
+  }
+  // T = fanout-th smallest candidate key
+  for (int i = Team::rank(); i < m; i += Team::size()) {
+    const uint64_t ki = cand[i];
+    int rank = 0;
+    for (int c = 0; c < m; ++c) rank += cand[c] < ki;
+    if (rank == fo - 1) *tsh = ki;
+  }
+  Team::sync();
+  const uint64_t T = *tsh;
+  for (int i = Team::rank(); i < m; i += Team::size()) {
+    const uint64_t ki = cand[i];
+    if (ki <= T) {
+      const uint32_t slot = (uint32_t)ki;
+      int pos = 0;
+      for (int c = 0; c < m; ++c) {
+        const uint64_t kc = cand[c];
+        pos += (kc <= T) && ((uint32_t)kc < slot);
+      }
+      out[pos] = targets[lo + slot];
+    }
+  }
+  Team::sync();
+}
+
+// ---------------------------------------------------------------- block sort
+
+// Sort buf[0..n) ascending (bitonic over the next power of two, INT_MAX pad)
+// then write the distinct values to out; returns the distinct count.
+__device__ int block_sort_unique(int* buf, int n, int* out, int* scan) {
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int i = n + threadIdx.x; i < P; i += blockDim.x) buf[i] = INT_MAX;
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < (P >> 1); i += blockDim.x) {
+        const int a = 2 * i - (i & (stride - 1));
+        const int b = a + stride;
+        const bool up = (a & size) == 0;
+        const int x = buf[a], y = buf[b];
+        if ((x > y) == up) { buf[a] = y; buf[b] = x; }
+      }
+      __syncthreads();
+    }
+  }
+  const int per = (P + blockDim.x - 1) / blockDim.x;
+  const int s = threadIdx.x * per;
+  const int e = min(s + per, P);
+  int keep = 0;
+  for (int i = s; i < e; ++i) {
+    const int v = buf[i];
+    keep += (v != INT_MAX) && (i == 0 || buf[i - 1] != v);
+  }
+  int total;
+  int pos = block_exclusive_scan(keep, scan, &total);
+  for (int i = s; i < e; ++i) {
+    const int v = buf[i];
+    if ((v != INT_MAX) && (i == 0 || buf[i - 1] != v)) out[pos++] = v;
+  }
+  __syncthreads();
+  return total;
+}
+
+// exclusive scan of in[0..n) into out[0..n], out[n] = total (n small)
+__device__ int block_scan_small(const int* in, int* out, int n, int* scan) {
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int s = threadIdx.x * per;
+  const int e = min(s + per, n);
+  int sum = 0;
+  for (int i = s; i < e; ++i) sum += in[i];
+  int total;
+  int pos = block_exclusive_scan(sum, scan, &total);
+  for (int i = s; i < e; ++i) { out[i] = pos; pos += in[i]; }
+  if (threadIdx.x == 0) out[n] = total;
+  __syncthreads();
+  return total;
+}
+
+__device__ __forceinline__ bool contains(const int* a, int n, int x) {
+  const int p = lower_bound(a, n, x);
+  return p < n && a[p] == x;
+}
+
+// ---------------------------------------------------------------- build kernel
+
+__global__ void __launch_bounds__(kBuildThreads)
+k_mg_build(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targets,
+           int64_t n_vertices, const int64_t* __restrict__ roots, int n_roots,
+           const uint64_t* __restrict__ iter_state, int roots_per_state, MgCarve c,
+           int32_t* __restrict__ ws, int* err) {
+  extern __shared__ __align__(16) int sm[];
+  const int r = blockIdx.x;
+  if (r >= n_roots) return;
+  const int L = c.L;
+  int* scan = sm + c.sm_scan;
+  __shared__ int warp_ctr[kBuildWarps + 1];
+  __shared__ uint64_t tslots[kBuildWarps + 1];
+  uint64_t* cand_base = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(sm) + c.cand_byte_off);
+
+  int64_t root = roots[r];
+  if (root < 0 || root >= n_vertices) {
+    raise_flag(err, HG_ERANGE);
+    root = 0;
+  }
+  // roots_per_state == 0: iter_state already holds one final stream key per root
+  const uint64_t key = roots_per_state > 0
+                           ? mix64(iter_state[r / roots_per_state] ^ (uint64_t)root)
+                           : iter_state[r];
+  __shared__ int nlay[HG_MAX_LAYERS + 1], nneed[HG_MAX_LAYERS + 1], ntot[HG_MAX_LAYERS + 1];
+  if (threadIdx.x == 0) {
+    sm[c.sm_lay[L]] = (int)root;
+    nlay[L] = 1;
+  }
+  __syncthreads();
+
+  for (int h = 1; h <= L; ++h) {
+    const int k = L - h;
+    const int F = nlay[k + 1];
+    const int fo = c.fanout[h - 1];
+    const int mean = c.mean[h - 1];
+    const int* front = sm + c.sm_lay[k + 1];
+    int* cnt = sm + c.sm_cnt[h];
+    int* off = sm + c.sm_off[h];
+    int* degs = sm + c.sm_deg[h];
+    int* flat = sm + c.sm_flat[h];
+    const uint64_t state = mix64(mix64(key) ^ (uint64_t)h);  // chain(key, hop)
+    for (int i = threadIdx.x; i < F; i += blockDim.x) {
+      const int v = front[i];
+      const int64_t d = offsets[v + 1] - offsets[v];
+      degs[i] = (int)d;
+      cnt[i] = d <= fo ? (int)d : fo;
+    }
+    __syncthreads();
+    const int T = block_scan_small(cnt, off, F, scan);
+    // small tasks: one warp each
+    for (int i = warp_id(); i < F; i += kBuildWarps) {
+      const int d = degs[i];
+      if (d > kBigTask) continue;
+      const int v = front[i];
+      const int64_t lo = offsets[v];
+      int32_t* out = flat + off[i];
+      if (d <= fo) {
+        for (int j = lane_id(); j < d; j += 32) out[j] = targets[lo + j];
+      } else {
+        team_select<WarpTeam>(targets, lo, d, fo, mean, mix64(state ^ (uint64_t)v), out,
+                              cand_base + (size_t)warp_id() * c.cand_cap, c.cand_cap,
+                              warp_ctr + warp_id(), tslots + warp_id(), err);
+      }
+    }
+    __syncthreads();
+    // hubs: the whole CTA
+    for (int i = 0; i < F; ++i) {
+      const int d = degs[i];
+      if (d <= kBigTask) continue;
+      const int v = front[i];
+      team_select<BlockTeam>(targets, offsets[v], d, fo, mean, mix64(state ^ (uint64_t)v),
+                             flat + off[i], cand_base + (size_t)kBuildWarps * c.cand_cap,
+                             c.cand_cap, warp_ctr + kBuildWarps, tslots + kBuildWarps, err);
+    }
+    __syncthreads();
+    int* sb = sm + c.sm_sort;
+    for (int i = threadIdx.x; i < T; i += blockDim.x) sb[i] = flat[i];
+    __syncthreads();
+    const int u = block_sort_unique(sb, T, sm + c.sm_lay[k], scan);
+    if (threadIdx.x == 0) { nlay[k] = u; ntot[h] = T; }
+    __syncthreads();
+  }
+
+  // need-chain sets: need[L] = [root], need[k] = union(layers[k], need[k+1])
+  if (threadIdx.x == 0) { sm[c.sm_need[L]] = sm[c.sm_lay[L]]; nneed[L] = 1; }
+  __syncthreads();
+  for (int k = L - 1; k >= 0; --k) {
+    int* sb = sm + c.sm_sort;
+    const int a = nlay[k], b = nneed[k + 1];
+    for (int i = threadIdx.x; i < a; i += blockDim.x) sb[i] = sm[c.sm_lay[k] + i];
+    for (int i = threadIdx.x; i < b; i += blockDim.x) sb[a + i] = sm[c.sm_need[k + 1] + i];
+    __syncthreads();
+    const int u = block_sort_unique(sb, a + b, sm + c.sm_need[k], scan);
+    if (threadIdx.x == 0) nneed[k] = u;
+    __syncthreads();
+  }
+
+  // padded per-root outputs
+  int32_t* w = ws + (size_t)r * c.ws_root_ints;
+  for (int k = 0; k <= L; ++k) {
+    const int* need = sm + c.sm_need[k];
+    const int* lay = sm + c.sm_lay[k];
+    for (int a = threadIdx.x; a < nneed[k]; a += blockDim.x) {
+      const int uv = need[a];
+      w[c.ws_need[k] + a] = uv;
+      w[c.ws_inl[k] + a] = contains(lay, nlay[k], uv) ? 1 : 0;
+    }
+  }
+  for (int k = 1; k <= L; ++k) {
+    const int hp = L - k + 1;  // hop whose frontier is layers[k]
+    const int* need = sm + c.sm_need[k];
+    const int* prev = sm + c.sm_need[k - 1];
+    const int* lay = sm + c.sm_lay[k];
+    const int* off = sm + c.sm_off[hp];
+    const int* flat = sm + c.sm_flat[hp];
+    const int nk = nneed[k], np = nneed[k - 1], nl = nlay[k];
+    for (int a = threadIdx.x; a < nk; a += blockDim.x) {
+      const int uv = need[a];
+      w[c.ws_self[k] + a] = lower_bound(prev, np, uv);
+      w[c.ws_rowoff[k] + a] = off[lower_bound(lay, nl, uv)];
+    }
+    if (threadIdx.x == 0) w[c.ws_rowoff[k] + nk] = ntot[hp];
+    for (int t = threadIdx.x; t < ntot[hp]; t += blockDim.x)
+      w[c.ws_nbr[k] + t] = lower_bound(prev, np, flat[t]);
+  }
+  if (threadIdx.x == 0) {
+    for (int k = 0; k <= L; ++k) w[c.ws_cnt + k] = nneed[k];
+    for (int k = 1; k <= L; ++k) w[c.ws_cnt + L + k] = ntot[L - k + 1];
+  }
+}
+
+// Exclusive scans of the per-root counts (one CTA).  cols 0..L: need sizes,
+// cols L+1..2L: pair counts of layers 1..L.
+__global__ void __launch_bounds__(1024)
+k_mg_scan(const int32_t* __restrict__ ws, int n_roots, MgCarve c, hg_mg_batch out) {
+  __shared__ int scan[40];
+  const int L = c.L;
+  for (int col = 0; col <= 2 * L; ++col) {
+    int32_t* dst = col <= L ? out.need_off[col] : out.pair_off[col - L];
+    const int per = (n_roots + blockDim.x - 1) / blockDim.x;
+    const int s = threadIdx.x * per;
+    const int e = min(s + per, n_roots);
+    int sum = 0;
+    for (int i = s; i < e; ++i) sum += ws[(size_t)i * c.ws_root_ints + c.ws_cnt + col];
+    int total;
+    int pos = block_exclusive_scan(sum, scan, &total);
+    for (int i = s; i < e; ++i) {
+      dst[i] = pos;
+      pos += ws[(size_t)i * c.ws_root_ints + c.ws_cnt + col];
+    }
+    if (threadIdx.x == 0) {
+      dst[n_roots] = total;
+      out.totals[col] = total;
+      if (col > L) out.nbr_off[col - L][out.totals[col - L]] = total;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(128)
+k_mg_finalize(const int32_t* __restrict__ ws, int n_roots, MgCarve c, hg_mg_batch out) {
+  const int r = blockIdx.x;
+  if (r >= n_roots) return;
+  const int L = c.L;
+  const int32_t* w = ws + (size_t)r * c.ws_root_ints;
+  for (int k = 0; k <= L; ++k) {
+    const int base = out.need_off[k][r];
+    const int nk = w[c.ws_cnt + k];
+    for (int a = threadIdx.x; a < nk; a += blockDim.x) {
+      out.need_ids[k][base + a] = w[c.ws_need[k] + a];
+      out.in_layer[k][base + a] = (int8_t)w[c.ws_inl[k] + a];
+    }
+    if (k == 0) continue;
+    const int pbase = out.pair_off[k][r];
+    const int prev_base = out.need_off[k - 1][r];
+    for (int a = threadIdx.x; a < nk; a += blockDim.x) {
+      out.self_pos[k][base + a] = prev_base + w[c.ws_self[k] + a];
+      out.nbr_off[k][base + a] = pbase + w[c.ws_rowoff[k] + a];
+    }
+    const int pk = w[c.ws_cnt + L + k];
+    for (int t = threadIdx.x; t < pk; t += blockDim.x)
+      out.nbr_idx[k][pbase + t] = prev_base + w[c.ws_nbr[k] + t];
+  }
+}
+
+// ---------------------------------------------------------------- drop-in frontier
+
+__global__ void k_frontier_counts(const int64_t* __restrict__ offsets, int64_t n_vertices,
+                                  const int64_t* __restrict__ frontier, int64_t f, int fo,
+                                  int64_t* counts, int* err) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= f) return;
+  int64_t v = frontier[i];
+  if (v < 0 || v >= n_vertices) { raise_flag(err, HG_ERANGE); counts[i] = 0; return; }
+  const int64_t d = offsets[v + 1] - offsets[v];
+  counts[i] = d <= fo ? d : fo;
+}
+
+__global__ void __launch_bounds__(256)
+k_frontier_fill(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targets,
+                int64_t n_vertices, const int64_t* __restrict__ frontier, int64_t f, int fo,
+                int mean, uint64_t state, const int64_t* __restrict__ pos,
+                int64_t* __restrict__ flat, int cand_cap, int* err) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  uint64_t* cand = reinterpret_cast<uint64_t*>(smraw) + (size_t)warp_id() * cand_cap;
+  int32_t* obuf = reinterpret_cast<int32_t*>(reinterpret_cast<uint64_t*>(smraw) +
+                                             (size_t)(blockDim.x / 32) * cand_cap) +
+                  (size_t)warp_id() * fo;
+  __shared__ int ctr[8];
+  __shared__ uint64_t tsh[8];
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x / 32) + warp_id();
+  if (i >= f) return;
+  const int64_t v = frontier[i];
+  if (v < 0 || v >= n_vertices) return;
+  const int64_t lo = offsets[v];
+  const int d = (int)(offsets[v + 1] - lo);
+  int64_t* out = flat + pos[i];
+  if (d <= fo) {
+    for (int j = lane_id(); j < d; j += 32) out[j] = targets[lo + j];
+    return;
+  }
+  team_select<WarpTeam>(targets, lo, d, fo, mean, mix64(state ^ (uint64_t)v), obuf, cand,
+                        cand_cap, ctr + warp_id(), tsh + warp_id(), err);
+  for (int j = lane_id(); j < fo; j += 32) out[j] = obuf[j];
+}
+
+}  // namespace hg
+
+using namespace hg;
+
+extern "C" int hg_mg_plan_layout(int32_t n_layers, const int32_t* fanout, hg_mg_layout* out) {
+  MgCarve c;
+  int st = make_carve(n_layers, fanout, &c);
+  if (st) return st;
+  *out = hg_mg_layout{};
+  out->n_layers = n_layers;
+  for (int h = 0; h < n_layers; ++h) out->fanout[h] = fanout[h];
+  for (int k = 0; k <= n_layers; ++k) {
+    out->cap_lay[k] = c.cap_lay[k];
+    out->cap_need[k] = c.cap_need[k];
+  }
+  out->cand_cap = c.cand_cap;
+  out->sort_cap = c.sort_cap;
+  out->smem_bytes = c.smem_bytes;
+  out->ws_root_ints = c.ws_root_ints;
+  return HG_OK;
+}
+
+extern "C" int hg_mg_build(const int64_t* offsets, const int32_t* targets, int64_t n_vertices,
+                           const int64_t* roots, int32_t n_roots, const uint64_t* iter_state,
+                           int32_t roots_per_state, const hg_mg_layout* layout, int32_t* ws,
+                           hg_mg_batch* out, int* err_flag, void* stream) {
+  if (n_roots < 0 || roots_per_state < 0) return hg_fail(HG_ERANGE, "bad root count");
+  MgCarve c;
+  int st = make_carve(layout->n_layers, layout->fanout, &c);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n_roots == 0) return HG_OK;
+  HG_CUDA_TRY(cudaFuncSetAttribute(k_mg_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   c.smem_bytes));
+  k_mg_build<<<n_roots, kBuildThreads, c.smem_bytes, s>>>(offsets, targets, n_vertices, roots,
+                                                          n_roots, iter_state, roots_per_state,
+                                                          c, ws, err_flag);
+  HG_CUDA_TRY(cudaGetLastError());
+  k_mg_scan<<<1, 1024, 0, s>>>(ws, n_roots, c, *out);
+  HG_CUDA_TRY(cudaGetLastError());
+  k_mg_finalize<<<n_roots, 128, 0, s>>>(ws, n_roots, c, *out);
+  HG_CUDA_TRY(cudaGetLastError());
+  return HG_OK;
+}
+
+extern "C" int hg_sample_frontier(const int64_t* offsets, const int32_t* targets,
+                                  int64_t n_vertices, const int64_t* frontier, int64_t n_frontier,
+                                  int32_t fanout, uint64_t state, int64_t* counts_out,
+                                  int64_t* flat_out, int64_t flat_cap, int64_t* flat_len_host,
+                                  void* stream) {
+  if (fanout < 1) return hg_fail(HG_ECONFIG, "fanout must be >= 1");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n_frontier == 0) { *flat_len_host = 0; return HG_OK; }
+  int* err = nullptr;
+  int64_t* pos = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  HG_CUDA_TRY(cudaMallocAsync((void**)&err, sizeof(int), s));
+  HG_CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(int), s));
+  HG_CUDA_TRY(cudaMallocAsync((void**)&pos, (n_frontier + 1) * sizeof(int64_t), s));
+  k_frontier_counts<<<(unsigned)((n_frontier + 255) / 256), 256, 0, s>>>(
+      offsets, n_vertices, frontier, n_frontier, fanout, counts_out, err);
+  HG_CUDA_TRY(cudaGetLastError());
+  HG_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts_out, pos, n_frontier, s));
+  HG_CUDA_TRY(cudaMallocAsync(&tmp, tmp_bytes, s));
+  HG_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts_out, pos, n_frontier, s));
+  int64_t last_pos = 0, last_cnt = 0;
+  HG_CUDA_TRY(cudaMemcpyAsync(&last_pos, pos + n_frontier - 1, 8, cudaMemcpyDeviceToHost, s));
+  HG_CUDA_TRY(cudaMemcpyAsync(&last_cnt, counts_out + n_frontier - 1, 8, cudaMemcpyDeviceToHost, s));
+  int herr = 0;
+  HG_CUDA_TRY(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, s));
+  HG_CUDA_TRY(cudaStreamSynchronize(s));
+  const int64_t total = last_pos + last_cnt;
+  *flat_len_host = total;
+  int rc = HG_OK;
+  if (herr) rc = hg_fail(herr, "frontier vertex out of range");
+  else if (total > flat_cap) rc = hg_fail(HG_ECAPACITY, "flat_out holds %lld < %lld", (long long)flat_cap, (long long)total);
+  if (rc == HG_OK) {
+    const int mean = select_mean(fanout);
+    int cap = pow2ceil(2 * mean < 64 ? 64 : 2 * mean);
+    const int warps = 8;
+    size_t smem = (size_t)warps * cap * 8 + (size_t)warps * fanout * 4;
+    if (smem > 200 * 1024) rc = hg_fail(HG_ECONFIG, "fanout %d too large", fanout);
+    else {
+      HG_CUDA_TRY(cudaFuncSetAttribute(k_frontier_fill, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+      k_frontier_fill<<<(unsigned)((n_frontier + warps - 1) / warps), warps * 32, smem, s>>>(
+          offsets, targets, n_vertices, frontier, n_frontier, fanout, mean, state, pos, flat_out,
+          cap, err);
+      HG_CUDA_TRY(cudaGetLastError());
+    }
+  }
+  HG_CUDA_TRY(cudaFreeAsync(tmp, s));
+  HG_CUDA_TRY(cudaFreeAsync(pos, s));
+  HG_CUDA_TRY(cudaFreeAsync(err, s));
+  return rc;
+}
