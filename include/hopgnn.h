@@ -154,6 +154,55 @@ int hg_mg_build(const int64_t* offsets, const int32_t* targets, int64_t n_vertic
                 int32_t roots_per_state, const hg_mg_layout* layout, int32_t* ws,
                 hg_mg_batch* out, int* err_flag, void* stream);
 
+
+/* ------------------------------------------------------------------------
+ * 5. Forward / backward of a micrograph batch (model.py:213-287) and the
+ *    synchronous update (model.py:299-324)
+ * --------------------------------------------------------------------- */
+typedef struct {
+  int32_t n_layers;                      /* L                                          */
+  int32_t arch;                          /* 0 = gcn, 1 = sage-mean                     */
+  int32_t act_dtype;                     /* 0 = f32, 1 = bf16 activations / operands   */
+  int32_t feat_dim;                      /* D (reference width)                        */
+  int32_t feat_ld;                       /* Dp >= D: padded row stride (multiple of 8) */
+  int32_t hidden;                        /* H (multiple of 8)                          */
+  int32_t n_classes;                     /* C                                          */
+  int32_t max_roots;
+  int32_t max_rows[HG_MAX_LAYERS + 1];   /* capacity of need[k] rows                   */
+  int32_t in_dim[HG_MAX_LAYERS + 1];     /* k>=1: GEMM K of layer k (padded)           */
+  int32_t split_k;                       /* CTAs along the row reduction of dW         */
+  int32_t use_tc;                        /* 1: tcgen05 GEMMs where act_dtype == bf16   */
+  const void* features;                  /* [rows x feat_ld], act dtype                */
+  const int32_t* feat_row;               /* vertex -> feature row; NULL = identity     */
+  const int64_t* roots;                  /* [n_roots]                                  */
+  uint64_t label_state;                  /* chain(label_seed, 0x1A) (model.py:99-100)  */
+  hg_mg_batch mg;                        /* from hg_mg_build                           */
+  float* W[HG_MAX_LAYERS + 1];           /* k>=1: [in_dim[k] x H] f32 master            */
+  float* b[HG_MAX_LAYERS + 1];           /* k>=1: [H]                                  */
+  float* Wc;                             /* [H x C]                                    */
+  void* Wlp[HG_MAX_LAYERS + 1];          /* bf16 shadows of W (act_dtype == 1)         */
+  void* Wclp;
+  float* gW[HG_MAX_LAYERS + 1];          /* gradient accumulators (summed, unscaled)   */
+  float* gb[HG_MAX_LAYERS + 1];
+  float* gWc;
+  void* agg[HG_MAX_LAYERS + 1];          /* [max_rows[k] x in_dim[k]] act dtype        */
+  void* h[HG_MAX_LAYERS + 1];            /* [max_rows[k] x H] act dtype                */
+  float* dh[HG_MAX_LAYERS + 1];          /* [max_rows[k] x H] f32                       */
+  float* dagg;                           /* [max_k>=2 max_rows[k] x in_dim[k]] f32      */
+  float* logits;                         /* [max_roots x C] (dlogits after backward)   */
+  float* loss;                           /* [max_roots] per-root softmax-CE            */
+  void* lowp_scratch;                    /* bf16 [max_rows[1] x H] (tcgen05 dW path)    */
+} hg_step_desc;
+
+/* Forward + backward of the batch in d->mg for n_roots roots; gradients are
+ * ADDED into gW/gb/gWc (the reference GradAccumulator, model.py:144-164). */
+int hg_train_step(const hg_step_desc* d, int32_t n_roots, void* stream);
+/* Forward only: fills logits (and agg/h).  Used by parity tests. */
+int hg_forward(const hg_step_desc* d, int32_t n_roots, void* stream);
+/* theta -= lr * (g * inv_batch); g = 0; refresh bf16 shadow (model.py:315-324). */
+int hg_sgd_update(float* params, float* grads, void* shadow_bf16, int64_t n, float lr,
+                  float inv_batch, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

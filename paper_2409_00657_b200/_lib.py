@@ -46,6 +46,25 @@ class GraphTables(C.Structure):
                 ("deg_span", C.c_int64 * 64)]
 
 
+_P7V = C.c_void_p * 7
+
+
+class StepDesc(C.Structure):
+    """hg_step_desc (include/hopgnn.h section 5)."""
+
+    _fields_ = [("n_layers", C.c_int32), ("arch", C.c_int32), ("act_dtype", C.c_int32),
+                ("feat_dim", C.c_int32), ("feat_ld", C.c_int32), ("hidden", C.c_int32),
+                ("n_classes", C.c_int32), ("max_roots", C.c_int32),
+                ("max_rows", C.c_int32 * 7), ("in_dim", C.c_int32 * 7),
+                ("split_k", C.c_int32), ("use_tc", C.c_int32),
+                ("features", C.c_void_p), ("feat_row", C.c_void_p), ("roots", C.c_void_p),
+                ("label_state", C.c_uint64), ("mg", MgBatch),
+                ("W", _P7V), ("b", _P7V), ("Wc", C.c_void_p), ("Wlp", _P7V), ("Wclp", C.c_void_p),
+                ("gW", _P7V), ("gb", _P7V), ("gWc", C.c_void_p),
+                ("agg", _P7V), ("h", _P7V), ("dh", _P7V), ("dagg", C.c_void_p),
+                ("logits", C.c_void_p), ("loss", C.c_void_p), ("lowp_scratch", C.c_void_p)]
+
+
 V, I32, I64, U64, SZ = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_size_t
 PSZ = C.POINTER(C.c_size_t)
 PI64 = C.POINTER(C.c_int64)
@@ -67,6 +86,9 @@ SIGNATURES = {
     "hg_mg_plan_layout": [I32, C.POINTER(I32), C.POINTER(MgLayout)],
     "hg_mg_build": [V, V, I64, V, I32, V, I32, C.POINTER(MgLayout), V, C.POINTER(MgBatch),
                     V, V],
+    "hg_train_step": [C.POINTER(StepDesc), I32, V],
+    "hg_forward": [C.POINTER(StepDesc), I32, V],
+    "hg_sgd_update": [V, V, V, I64, C.c_float, C.c_float, V],
 }
 
 

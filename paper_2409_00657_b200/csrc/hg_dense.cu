@@ -1,0 +1,497 @@
+// Forward / backward of a batch of micrographs (the GNN math of model.py).
+//
+// Reference: forward model.py:213-247, loss_and_backward model.py:250-287,
+// sync_and_update model.py:299-324.  The reference runs one micrograph at a
+// time in float64; here a whole cell of roots is one segmented computation:
+// every layer is ONE gather+aggregate over the need[k] rows of all roots and
+// ONE dense GEMM, because micrographs share nothing but the parameters
+// (SURVEY §0.4).  Row numbering is the global one produced by hg_mg_build.
+//
+// Kernels:
+//   k_aggregate    gather rows (features for layer 1, h_{k-1} above) and
+//                  build agg_k = [self, mean(nbrs)] (SAGE) or mean(nbrs+self)
+//                  (GCN); 16-byte vector loads, several rows per warp
+//   gemm (SIMT)    fp32-accumulate tiled GEMM with fused epilogues (bias+ReLU,
+//                  ReLU-mask, split-K atomic accumulation for dW)
+//   k_softmax_ce   root logits -> loss, dlogits (labels hashed on the fly)
+//   k_scatter      transpose of the aggregation for dh_{k-1}
+//   k_mask_colsum  dz = dh * (h > 0) and bias gradient
+//   k_sgd          fused update + gradient reset + bf16 shadow refresh
+#include <cuda_bf16.h>
+
+#include "hg_common.cuh"
+
+namespace hg {
+
+using bf16 = __nv_bfloat16;
+
+template <typename T> __device__ __forceinline__ float to_f(T x);
+template <> __device__ __forceinline__ float to_f<float>(float x) { return x; }
+template <> __device__ __forceinline__ float to_f<bf16>(bf16 x) { return __bfloat162float(x); }
+template <typename T> __device__ __forceinline__ T from_f(float x);
+template <> __device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <> __device__ __forceinline__ bf16 from_f<bf16>(float x) { return __float2bfloat16_rn(x); }
+
+// 16-byte vector of T
+template <typename T> struct Vec { static constexpr int N = 16 / sizeof(T); };
+
+template <typename T>
+__device__ __forceinline__ void load_vec(const T* p, float* v) {
+  const uint4 raw = __ldg(reinterpret_cast<const uint4*>(p));
+  if constexpr (sizeof(T) == 4) {
+    v[0] = __uint_as_float(raw.x); v[1] = __uint_as_float(raw.y);
+    v[2] = __uint_as_float(raw.z); v[3] = __uint_as_float(raw.w);
+  } else {
+    const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void store_vec(T* p, const float* v) {
+  uint4 raw;
+  if constexpr (sizeof(T) == 4) {
+    raw.x = __float_as_uint(v[0]); raw.y = __float_as_uint(v[1]);
+    raw.z = __float_as_uint(v[2]); raw.w = __float_as_uint(v[3]);
+  } else {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const __nv_bfloat162 t = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+      w[i] = *reinterpret_cast<const uint32_t*>(&t);
+    }
+    raw = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  *reinterpret_cast<uint4*>(p) = raw;
+}
+
+// ------------------------------------------------------------------ aggregate
+//
+// One group of G = W/VEC lanes (<= 32) per destination row.  For layer 1 the
+// source row of need[0] entry i is feat_row[need_ids0[i]] (vertex ids), for
+// deeper layers the row index itself.
+template <typename T, bool SAGE>
+__global__ void __launch_bounds__(256)
+k_aggregate(const T* __restrict__ src, int src_ld, const int32_t* __restrict__ need_ids0,
+            const int32_t* __restrict__ feat_row, const int32_t* __restrict__ self_pos,
+            const int32_t* __restrict__ nbr_off, const int32_t* __restrict__ nbr_idx,
+            const int32_t* __restrict__ n_rows_dev, int W, T* __restrict__ out, int out_ld) {
+  constexpr int VEC = Vec<T>::N;
+  const int nvec = W / VEC;                        // vectors per row
+  const int G = nvec >= 32 ? 32 : (nvec >= 16 ? 16 : (nvec >= 8 ? 8 : (nvec >= 4 ? 4 : (nvec >= 2 ? 2 : 1))));
+  const int groups_per_block = blockDim.x / G;
+  const int grp = threadIdx.x / G, gl = threadIdx.x % G;
+  const int n_rows = *n_rows_dev;
+  for (int a = blockIdx.x * groups_per_block + grp; a < n_rows; a += gridDim.x * groups_per_block) {
+    int sp = self_pos[a];
+    if (need_ids0) sp = feat_row ? feat_row[need_ids0[sp]] : need_ids0[sp];
+    const int j0 = nbr_off[a], j1 = nbr_off[a + 1];
+    const int deg = j1 - j0;
+    for (int cv = gl; cv < nvec; cv += G) {
+      const int col = cv * VEC;
+      float self[VEC], acc[VEC];
+      load_vec(src + (int64_t)sp * src_ld + col, self);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
+      int j = j0;
+      for (; j + 4 <= j1; j += 4) {
+        int r[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          r[u] = nbr_idx[j + u];
+          if (need_ids0) r[u] = feat_row ? feat_row[need_ids0[r[u]]] : need_ids0[r[u]];
+        }
+        float x[4][VEC];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) load_vec(src + (int64_t)r[u] * src_ld + col, x[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) acc[i] += x[u][i];
+      }
+      for (; j < j1; ++j) {
+        int r = nbr_idx[j];
+        if (need_ids0) r = feat_row ? feat_row[need_ids0[r]] : need_ids0[r];
+        float x[VEC];
+        load_vec(src + (int64_t)r * src_ld + col, x);
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) acc[i] += x[i];
+      }
+      T* o = out + (int64_t)a * out_ld;
+      if constexpr (SAGE) {
+        float nb[VEC];
+        const float inv = deg > 0 ? 1.0f / (float)deg : 0.f;
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) nb[i] = deg > 0 ? acc[i] * inv : self[i];
+        store_vec(o + col, self);
+        store_vec(o + W + col, nb);
+      } else {
+        const float inv = 1.0f / (float)(deg + 1);
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) acc[i] = (acc[i] + self[i]) * inv;
+        store_vec(o + col, acc);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ SIMT GEMM
+//
+// C[m,n] = sum_k A(m,k) B(k,n); A(m,k) = AT ? A[k*lda+m] : A[m*lda+k],
+// B(k,n) = BT ? B[n*ldb+k] : B[k*ldb+n].  M or K may be device-resident
+// (row counts of the batch).  fp32 accumulation.
+enum Epi { EPI_STORE = 0, EPI_BIAS_RELU = 1, EPI_MASK = 2, EPI_ATOMIC = 3 };
+
+constexpr int BM = 64, BN = 64, BK = 16;
+
+template <typename TA, bool AT, bool BT, int EPI, typename TC, typename TM>
+__global__ void __launch_bounds__(256)
+k_gemm(const TA* __restrict__ A, int lda, const float* __restrict__ B, int ldb, TC* C, int ldc,
+       const int32_t* M_dev, int M_host, int N, const int32_t* K_dev, int K_host,
+       const float* __restrict__ bias, const TM* __restrict__ mask, int ldm) {
+  __shared__ float As[BK][BM + 4];
+  __shared__ float Bs[BK][BN + 4];
+  const int M = M_dev ? *M_dev : M_host;
+  const int K = K_dev ? *K_dev : K_host;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (m0 >= M) return;
+  // split along K (gridDim.z)
+  const int kchunk = ((K + gridDim.z - 1) / gridDim.z + BK - 1) / BK * BK;
+  const int kb = blockIdx.z * kchunk;
+  const int ke = min(K, kb + kchunk);
+  if (kb >= ke) return;
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  float acc[4][4] = {};
+  for (int k0 = kb; k0 < ke; k0 += BK) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = tid + i * 256;
+      int r, kk;
+      if (AT) { kk = e / BM; r = e % BM; } else { r = e / BK; kk = e % BK; }
+      const int gm = m0 + r, gk = k0 + kk;
+      float v = 0.f;
+      if (gm < M && gk < ke) v = to_f(AT ? A[(int64_t)gk * lda + gm] : A[(int64_t)gm * lda + gk]);
+      As[kk][r] = v;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int e = tid + i * 256;
+      int c, kk;
+      if (BT) { c = e / BK; kk = e % BK; } else { kk = e / BN; c = e % BN; }
+      const int gn = n0 + c, gk = k0 + kk;
+      float v = 0.f;
+      if (gn < N && gk < ke) v = BT ? B[(int64_t)gn * ldb + gk] : B[(int64_t)gk * ldb + gn];
+      Bs[kk][c] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gm = m0 + ty * 4 + i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gn = n0 + tx * 4 + j;
+      if (gn >= N) continue;
+      float v = acc[i][j];
+      if constexpr (EPI == EPI_BIAS_RELU) {
+        v = fmaxf(v + bias[gn], 0.f);
+        C[(int64_t)gm * ldc + gn] = from_f<TC>(v);
+      } else if constexpr (EPI == EPI_MASK) {
+        v = to_f(mask[(int64_t)gm * ldm + gn]) > 0.f ? v : 0.f;
+        C[(int64_t)gm * ldc + gn] = from_f<TC>(v);
+      } else if constexpr (EPI == EPI_ATOMIC) {
+        atomicAdd(reinterpret_cast<float*>(C) + (int64_t)gm * ldc + gn, v);
+      } else {
+        C[(int64_t)gm * ldc + gn] = from_f<TC>(v);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ loss
+
+// warp per root: softmax-CE on the root logits (model.py:253-259); logits are
+// overwritten with dlogits = softmax - onehot(label).
+__global__ void k_softmax_ce(float* __restrict__ logits, int C, const int64_t* __restrict__ roots,
+                             int n_roots, uint64_t label_state, float* __restrict__ loss) {
+  const int r = blockIdx.x * (blockDim.x / 32) + warp_id();
+  if (r >= n_roots) return;
+  const int lane = lane_id();
+  float* x = logits + (int64_t)r * C;
+  float mx = -INFINITY;
+  for (int c = lane; c < C; c += 32) mx = fmaxf(mx, x[c]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float s = 0.f;
+  for (int c = lane; c < C; c += 32) s += expf(x[c] - mx);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const int label = (int)(mix64(label_state ^ (uint64_t)roots[r]) % (uint64_t)C);
+  const float xl = x[label];
+  __syncwarp();
+  const float inv = 1.0f / s;
+  for (int c = lane; c < C; c += 32) x[c] = expf(x[c] - mx) * inv - (c == label ? 1.f : 0.f);
+  if (lane == 0) loss[r] = logf(s) - (xl - mx);
+}
+
+// ------------------------------------------------------------------ backward
+
+// Transpose of k_aggregate (model.py:266-285): warp per destination row.
+template <bool SAGE>
+__global__ void __launch_bounds__(256)
+k_scatter(const float* __restrict__ dagg, int ld, const int32_t* __restrict__ self_pos,
+          const int32_t* __restrict__ nbr_off, const int32_t* __restrict__ nbr_idx,
+          const int32_t* __restrict__ n_rows_dev, int W, float* __restrict__ dh) {
+  const int n_rows = *n_rows_dev;
+  const int a = blockIdx.x * (blockDim.x / 32) + warp_id();
+  if (a >= n_rows) return;
+  const int lane = lane_id();
+  const int s = self_pos[a];
+  const int j0 = nbr_off[a], j1 = nbr_off[a + 1];
+  const int deg = j1 - j0;
+  const float* g = dagg + (int64_t)a * ld;
+  if constexpr (SAGE) {
+    const float inv = deg > 0 ? 1.0f / (float)deg : 0.f;
+    for (int c = lane; c < W; c += 32) {
+      const float gs = g[c], gn = g[W + c];
+      atomicAdd(dh + (int64_t)s * W + c, deg > 0 ? gs : gs + gn);
+      if (deg > 0) {
+        const float v = gn * inv;
+        for (int j = j0; j < j1; ++j) atomicAdd(dh + (int64_t)nbr_idx[j] * W + c, v);
+      }
+    }
+  } else {
+    const float inv = 1.0f / (float)(deg + 1);
+    for (int c = lane; c < W; c += 32) {
+      const float v = g[c] * inv;
+      atomicAdd(dh + (int64_t)s * W + c, v);
+      for (int j = j0; j < j1; ++j) atomicAdd(dh + (int64_t)nbr_idx[j] * W + c, v);
+    }
+  }
+}
+
+// dz = dh * (h > 0) in place; gb[c] += sum_rows dz[., c]
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_mask_colsum(float* __restrict__ dh, const T* __restrict__ h, const int32_t* __restrict__ n_rows_dev,
+              int H, float* __restrict__ gb) {
+  const int n_rows = *n_rows_dev;
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int r0 = blockIdx.y * 8 + (threadIdx.x >> 5);
+  float s = 0.f;
+  if (c < H) {
+    for (int r = r0; r < n_rows; r += gridDim.y * 8) {
+      const int64_t i = (int64_t)r * H + c;
+      float v = dh[i];
+      v = to_f(h[i]) > 0.f ? v : 0.f;
+      dh[i] = v;
+      s += v;
+    }
+  }
+  __shared__ float red[8][33];
+  red[threadIdx.x >> 5][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (threadIdx.x < 32 && c < H) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
+    atomicAdd(gb + c, t);
+  }
+}
+
+// column sums of an already-masked matrix (bias grad of the top layer)
+__global__ void __launch_bounds__(256)
+k_colsum(const float* __restrict__ x, const int32_t* __restrict__ n_rows_dev, int n_rows_host,
+         int H, float* __restrict__ gb) {
+  const int n_rows = n_rows_dev ? *n_rows_dev : n_rows_host;
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int r0 = blockIdx.y * 8 + (threadIdx.x >> 5);
+  float s = 0.f;
+  if (c < H)
+    for (int r = r0; r < n_rows; r += gridDim.y * 8) s += x[(int64_t)r * H + c];
+  __shared__ float red[8][33];
+  red[threadIdx.x >> 5][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (threadIdx.x < 32 && c < H) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
+    atomicAdd(gb + c, t);
+  }
+}
+
+__global__ void k_zero_rows(float* __restrict__ x, const int32_t* __restrict__ n_rows_dev, int W) {
+  const int64_t total = (int64_t)(*n_rows_dev) * W;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i < total;
+       i += (int64_t)gridDim.x * blockDim.x * 4) {
+    if (i + 4 <= total) *reinterpret_cast<float4*>(x + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+    else for (int64_t j = i; j < total; ++j) x[j] = 0.f;
+  }
+}
+
+__global__ void k_sgd(float* __restrict__ p, float* __restrict__ g, bf16* __restrict__ shadow,
+                      int64_t n, float lr, float inv_batch) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float step = g[i] * inv_batch;
+    const float v = p[i] - lr * step;
+    p[i] = v;
+    g[i] = 0.f;
+    if (shadow) shadow[i] = __float2bfloat16_rn(v);
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (!g_num_sms) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <typename TA, bool AT, bool BT, int EPI, typename TC, typename TM>
+static void gemm(cudaStream_t s, const TA* A, int lda, const float* B, int ldb, TC* C, int ldc,
+                 const int32_t* M_dev, int M_cap, int N, const int32_t* K_dev, int K_cap,
+                 const float* bias, const TM* mask, int ldm, int split) {
+  dim3 grid((N + BN - 1) / BN, (M_cap + BM - 1) / BM, split);
+  k_gemm<TA, AT, BT, EPI, TC, TM><<<grid, 256, 0, s>>>(A, lda, B, ldb, C, ldc, M_dev, M_cap, N,
+                                                       K_dev, K_cap, bias, mask, ldm);
+}
+
+template <typename T>
+static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool backward) {
+  const int L = d->n_layers;
+  const bool sage = d->arch == 1;
+  const int H = d->hidden, C = d->n_classes;
+  const int32_t* tot = d->mg.totals;  // N_0..N_L on device
+  const int nb = num_sms() * 4;
+  // ---- forward
+  for (int k = 1; k <= L; ++k) {
+    const int Wd = k == 1 ? d->feat_ld : H;
+    const T* src = k == 1 ? (const T*)d->features : (const T*)d->h[k - 1];
+    const int32_t* ids0 = k == 1 ? d->mg.need_ids[0] : nullptr;
+    if (sage)
+      k_aggregate<T, true><<<nb, 256, 0, s>>>(src, Wd, ids0, d->feat_row, d->mg.self_pos[k],
+                                              d->mg.nbr_off[k], d->mg.nbr_idx[k], tot + k, Wd,
+                                              (T*)d->agg[k], d->in_dim[k]);
+    else
+      k_aggregate<T, false><<<nb, 256, 0, s>>>(src, Wd, ids0, d->feat_row, d->mg.self_pos[k],
+                                               d->mg.nbr_off[k], d->mg.nbr_idx[k], tot + k, Wd,
+                                               (T*)d->agg[k], d->in_dim[k]);
+    gemm<T, false, false, EPI_BIAS_RELU, T, T>(s, (const T*)d->agg[k], d->in_dim[k], d->W[k], H,
+                                               (T*)d->h[k], H, tot + k, d->max_rows[k], H,
+                                               nullptr, d->in_dim[k], d->b[k], nullptr, 0, 1);
+  }
+  // logits = h_L[roots] @ Wc (need[L] rows are the roots, in order)
+  gemm<T, false, false, EPI_STORE, float, T>(s, (const T*)d->h[L], H, d->Wc, C, d->logits, C,
+                                             nullptr, n_roots, C, nullptr, H, nullptr, nullptr, 0,
+                                             1);
+  k_softmax_ce<<<(n_roots + 7) / 8, 256, 0, s>>>(d->logits, C, d->roots, n_roots,
+                                                 d->label_state, d->loss);
+  if (!backward) return HG_OK;
+  // ---- backward (model.py:262-285)
+  const int split_r = n_roots >= 4096 ? 8 : 1;
+  // gWc += h_L^T dlogits
+  gemm<T, true, false, EPI_ATOMIC, float, T>(s, (const T*)d->h[L], H, d->logits, C, d->gWc, C,
+                                             nullptr, H, C, nullptr, n_roots, nullptr, nullptr, 0,
+                                             split_r);
+  // dz_L = (dlogits Wc^T) * (h_L > 0)
+  gemm<float, false, true, EPI_MASK, float, T>(s, d->logits, C, d->Wc, C, d->dh[L], H, nullptr,
+                                               n_roots, H, nullptr, C, nullptr, (const T*)d->h[L],
+                                               H, 1);
+  {
+    dim3 g((H + 31) / 32, 16);
+    k_colsum<<<g, 256, 0, s>>>(d->dh[L], nullptr, n_roots, H, d->gb[L]);
+  }
+  for (int k = L; k >= 1; --k) {
+    // gW_k += agg_k^T dz_k   (reduction over the N_k rows, split across CTAs)
+    gemm<T, true, false, EPI_ATOMIC, float, T>(s, (const T*)d->agg[k], d->in_dim[k], d->dh[k], H,
+                                               d->gW[k], H, nullptr, d->in_dim[k], H, tot + k,
+                                               d->max_rows[k], nullptr, nullptr, 0,
+                                               k == L ? split_r : d->split_k);
+    if (k == 1) break;  // layer-1 dX is unused (features are not trainable)
+    // dagg_k = dz_k W_k^T
+    gemm<float, false, true, EPI_STORE, float, T>(s, d->dh[k], H, d->W[k], H, d->dagg,
+                                                  d->in_dim[k], tot + k, d->max_rows[k],
+                                                  d->in_dim[k], nullptr, H, nullptr, nullptr, 0, 1);
+    k_zero_rows<<<nb, 256, 0, s>>>(d->dh[k - 1], tot + (k - 1), H);
+    const int grid = (d->max_rows[k] + 7) / 8;
+    if (sage)
+      k_scatter<true><<<grid, 256, 0, s>>>(d->dagg, d->in_dim[k], d->mg.self_pos[k],
+                                           d->mg.nbr_off[k], d->mg.nbr_idx[k], tot + k, H,
+                                           d->dh[k - 1]);
+    else
+      k_scatter<false><<<grid, 256, 0, s>>>(d->dagg, d->in_dim[k], d->mg.self_pos[k],
+                                            d->mg.nbr_off[k], d->mg.nbr_idx[k], tot + k, H,
+                                            d->dh[k - 1]);
+    dim3 g((H + 31) / 32, 64);
+    k_mask_colsum<T><<<g, 256, 0, s>>>(d->dh[k - 1], (const T*)d->h[k - 1], tot + (k - 1), H,
+                                       d->gb[k - 1]);
+  }
+  return HG_OK;
+}
+
+static int validate(const hg_step_desc* d, int n_roots) {
+  if (d->n_layers < 1 || d->n_layers > HG_MAX_LAYERS) return hg_fail(HG_ECONFIG, "bad n_layers");
+  if (n_roots < 1 || n_roots > d->max_roots) return hg_fail(HG_ERANGE, "bad n_roots %d", n_roots);
+  if (d->feat_ld % 8 || d->hidden % 8) return hg_fail(HG_ECONFIG, "feat_ld and hidden must be multiples of 8");
+  if (d->act_dtype != 0 && d->act_dtype != 1) return hg_fail(HG_ECONFIG, "bad act_dtype");
+  return HG_OK;
+}
+
+}  // namespace hg
+
+using namespace hg;
+
+extern "C" int hg_train_step(const hg_step_desc* d, int32_t n_roots, void* stream) {
+  int st = validate(d, n_roots);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  st = d->act_dtype == 0 ? run_step<float>(d, n_roots, s, true) : run_step<bf16>(d, n_roots, s, true);
+  if (st) return st;
+  HG_CUDA_TRY(cudaGetLastError());
+  return HG_OK;
+}
+
+extern "C" int hg_forward(const hg_step_desc* d, int32_t n_roots, void* stream) {
+  int st = validate(d, n_roots);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  st = d->act_dtype == 0 ? run_step<float>(d, n_roots, s, false) : run_step<bf16>(d, n_roots, s, false);
+  if (st) return st;
+  HG_CUDA_TRY(cudaGetLastError());
+  return HG_OK;
+}
+
+extern "C" int hg_sgd_update(float* params, float* grads, void* shadow_bf16, int64_t n, float lr,
+                             float inv_batch, void* stream) {
+  if (n <= 0) return HG_OK;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  k_sgd<<<grid, 256, 0, (cudaStream_t)stream>>>(params, grads, (bf16*)shadow_bf16, n, lr, inv_batch);
+  HG_CUDA_TRY(cudaGetLastError());
+  return HG_OK;
+}

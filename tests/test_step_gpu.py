@@ -1,0 +1,142 @@
+"""Numeric parity of the CUDA training step with the float64 oracle.
+
+Tolerances (north_star): fp32 path -- losses, gradients and updated weights
+within 1e-3 relative (max-abs error <= 1e-3 * max|ref| per tensor, and
+norm-relative error <= 1e-3).  bf16 path (features and activations in
+bf16, fp32 accumulation) -- stated separately: 1e-2 on the same metrics
+against an oracle that rounds to bf16 at the same storage points.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import kernels as OK
+from oracle import model as OM
+from oracle.graphgen import GraphSpec as OSpec, build_csr, build_tables
+from oracle.rng import chain
+from oracle.sampler import sample_micrograph as o_sample, stream_key
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: 1e-3, torch.bfloat16: 1e-2}
+
+CASES = [("sage-mean", (15, 10), 24, 16, 7),
+         ("gcn", (10, 10, 10), 20, 16, 5),
+         ("sage-mean", (10, 10, 5, 5), 16, 8, 4),
+         ("sage-mean", (10, 5), 100, 32, 47),
+         ("gcn", (4,), 8, 8, 3)]
+
+
+def close(got, want, tol, what):
+    got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
+    scale = max(np.abs(want).max(), 1e-30)
+    err = np.abs(got - want).max() / scale
+    nrel = np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30)
+    assert err <= tol and nrel <= tol, f"{what}: max-rel {err:.3e} norm-rel {nrel:.3e} > {tol}"
+
+
+@pytest.fixture(scope="module")
+def world():
+    kw = dict(n=3000, avg_deg=12.0, beta=0.7, p_in=0.9, n_blocks=4, d_cap=600, seed=11)
+    off, tgt = build_csr(build_tables(OSpec(**kw)))
+    from paper_2409_00657_b200.graph import Graph
+    return off, tgt, Graph.from_host(off, tgt)
+
+
+def _bf(a):
+    return torch.from_numpy(np.asarray(a, np.float32)).to(torch.bfloat16).double().numpy()
+
+
+def forward_bf16(m, x_rows, P):
+    """OM.forward with the bf16 storage points of the device path emulated:
+    features, every aggregate and every activation h_k are rounded to bf16."""
+    need, steps = OM.build_plan(m)
+    x = _bf(x_rows)
+    h = [x[np.searchsorted(m.vertices, need[0])]]
+    aggs, zs = [], []
+    for k, (self_pos, dpos, spos, deg) in enumerate(steps, start=1):
+        prev = h[-1]
+        s = np.zeros((len(need[k]), prev.shape[1]))
+        np.add.at(s, dpos, prev[spos])
+        own = prev[self_pos]
+        if P.arch == OM.GCN:
+            agg = (s + own) / (deg + 1.0)[:, None]
+        else:
+            has = (deg > 0)[:, None]
+            agg = np.concatenate([own, np.where(has, s / np.maximum(deg, 1.0)[:, None], own)], 1)
+        agg = _bf(agg)
+        z = agg @ P.W[k - 1] + P.b[k - 1]
+        aggs.append(agg)
+        zs.append(z)
+        h.append(_bf(np.maximum(z, 0.0)))
+    return dict(need=need, steps=steps, h=h, aggs=aggs, zs=zs, logits=h[-1][0] @ P.Wc)
+
+
+def oracle_cell(off, tgt, roots, fo, sseed, it_key, P, D, fstate, lseed, C, bf16_feats=False):
+    """Oracle gradients; with bf16_feats the oracle rounds features, aggregates and
+    activations to bf16 where the device stores them (arithmetic stays float64)."""
+    G = P.zeros()
+    losses = []
+    for r in roots.tolist():
+        m = o_sample(off, tgt, r, fo, stream_key(sseed, *it_key, r), draw=OK.sample_frontier_nb)
+        x = OK.feature_rows(m.vertices, D, fstate)
+        st = forward_bf16(m, x, P) if bf16_feats else OM.forward(m, x, P)
+        lab = int(OM.labels([r], C, lseed)[0])
+        loss, g = OM.loss_and_grads(st, lab, P)
+        OM.add_into(G, g)
+        losses.append(loss)
+    return np.array(losses), G
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16], ids=["f32", "bf16"])
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}-{'x'.join(map(str, c[1]))}-D{c[2]}")
+def test_step_matches_oracle(world, case, dtype):
+    from paper_2409_00657_b200.featstore import FeatureTable, feature_state
+    from paper_2409_00657_b200.model import LabelOracle, init_model
+    from paper_2409_00657_b200.trainer import CellRunner
+    arch, fo, D, H, C = case
+    off, tgt, G = world
+    seed = 7
+    sseed, mseed, lseed = chain(seed, 0x06), chain(seed, 0x07), chain(seed, 0x04)
+    rng = np.random.default_rng(1)
+    roots = rng.choice(len(off) - 1, 96, replace=False).astype(np.int64)
+    model = init_model(arch, D, H, len(fo), C, mseed)
+    table = FeatureTable.generated(len(off) - 1, D, seed, dtype=dtype)
+    run = CellRunner(G, table, model, fo, 128, LabelOracle(C, lseed))
+    st = np.uint64(chain(sseed, 0, 3)).view(np.int64)
+    run.stage_roots(roots, [st], len(roots))
+    run.launch()
+    torch.cuda.synchronize()
+    run.check()
+    P = OM.init_params(arch, D, H, len(fo), C, mseed)
+    want_loss, want_g = oracle_cell(off, tgt, roots, fo, sseed, (0, 3), P, D,
+                                    feature_state(seed), lseed, C, dtype == torch.bfloat16)
+    tol = TOL[dtype]
+    close(run.losses(), want_loss, tol, "loss")
+    for i, (a, b) in enumerate(zip(model.grads(), want_g.arrays())):
+        close(a, b, tol, f"grad[{i}]")
+    # synchronous update (model.py:315-324)
+    model.sgd(0.1, len(roots))
+    OM.sgd_step(P, want_g, len(roots), 0.1)
+    for i, (a, b) in enumerate(zip(model.params(), P.arrays())):
+        close(a, b, tol, f"param[{i}]")
+    assert float(model.grad.abs().max()) == 0.0
+
+
+def test_forward_only_and_repeat_determinism(world):
+    from paper_2409_00657_b200.featstore import FeatureTable
+    from paper_2409_00657_b200.model import LabelOracle, init_model
+    from paper_2409_00657_b200.trainer import CellRunner
+    off, tgt, G = world
+    model = init_model("sage-mean", 24, 16, 2, 7, 3)
+    table = FeatureTable.generated(len(off) - 1, 24, 3, dtype=torch.float32)
+    run = CellRunner(G, table, model, (15, 10), 64, LabelOracle(7, 5))
+    roots = np.arange(0, 3000, 50, dtype=np.int64)
+    st = np.uint64(chain(1, 0, 0)).view(np.int64)
+    run.stage_roots(roots, [st], len(roots))
+    run.launch(backward=False)
+    a = run.losses().copy()
+    run.launch(backward=False)
+    b = run.losses().copy()
+    assert np.array_equal(a, b)
+    assert float(model.grad.abs().max()) == 0.0
