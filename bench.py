@@ -1,0 +1,304 @@
+#!/usr/bin/env python
+"""Benchmark of the HopGNN micrograph training step on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--config papers|products|small]
+                    [--impl ours|reference]
+
+One JSON line on stdout (rank 0).  A *step* is one training iteration: every
+model trains B=1024 roots (sample micrographs -> gather/aggregate -> GEMMs ->
+softmax-CE -> backward -> synchronous SGD).  ``value`` is whole-job seeds/s
+(roots trained per second) with inputs resident in HBM, timed with CUDA
+events over exactly K steps (max over ranks for N>1); ``e2e`` is the same
+metric through the public ``Trainer.train_step`` API with the step's roots
+copied from pinned host memory and the step loss read back.
+
+Workload (BASELINE.json configs[3]): GraphSAGE 2-layer, fanout [15,10],
+hidden 256, 172 classes, bf16 activations, on a synthetic papers100M-shaped
+graph (111M vertices, ~1.6B CSR entries, 128-d features) generated on the
+GPU (oracle/graphgen.py describes the generator).  The graph (6.4 GB CSR) and
+feature table (28 GB) exceed L2 (126 MB), so no L2 flush is needed between
+steps.
+
+``--impl reference`` times the reference algorithm's CPU port (oracle/,
+restated from gnnsim and pinned to its golden vectors) on all host cores on a
+bounded root sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+CONFIGS = {
+    # BASELINE.json configs[3] (north_star target shape)
+    "papers": dict(workload="cfg4: GraphSAGE-2 fanout[15,10] hidden256 bf16, synthetic "
+                            "ogbn-papers100M-shaped graph (111M V, ~1.6B E, 128-d feats)",
+                   n=111_000_000, avg_deg=15.6, beta=0.6, p_in=0.95, n_blocks=8, d_cap=1 << 15,
+                   arch="sage-mean", fanout=(15, 10), dim=128, hidden=256, classes=172,
+                   batch=1024, seed=0),
+    # BASELINE.json configs[1]
+    "products": dict(workload="cfg2: GraphSAGE-2 fanout[15,10] hidden256 bf16, synthetic "
+                              "ogbn-products-shaped graph (2.4M V, ~62M E, 100-d feats)",
+                     n=2_400_000, avg_deg=27.0, beta=0.6, p_in=0.9, n_blocks=8, d_cap=1 << 14,
+                     arch="sage-mean", fanout=(15, 10), dim=100, hidden=256, classes=47,
+                     batch=1024, seed=0),
+    "small": dict(workload="smoke: GraphSAGE-2 fanout[10,5] on a 100K-vertex power-law graph",
+                  n=100_000, avg_deg=18.5, beta=0.8, p_in=0.9, n_blocks=8, d_cap=1 << 14,
+                  arch="sage-mean", fanout=(10, 5), dim=128, hidden=128, classes=16,
+                  batch=1024, seed=0),
+}
+
+
+def peaks():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"hg_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                p = [x.strip() for x in line.split(",")]
+                if len(p) >= 9:
+                    rows.append(p)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = sorted(float(r[1]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def cpu_baseline(cfg, budget_s=15.0):
+    """Single-core oracle port on a bounded sample (rank 0, N=1)."""
+    from oracle.cpu_bench import run_single
+    from oracle.graphgen import GraphSpec as OSpec
+    spec = OSpec(n=cfg["n"], avg_deg=cfg["avg_deg"], beta=cfg["beta"], p_in=cfg["p_in"],
+                 n_blocks=cfg["n_blocks"], d_cap=cfg["d_cap"], seed=cfg["seed"])
+    kw = dict(arch=cfg["arch"], fanout=cfg["fanout"], dim=cfg["dim"], hidden=cfg["hidden"],
+              classes=cfg["classes"])
+    rate, done = run_single(spec, kw, cfg["seed"], 32, 64, budget_s=budget_s)
+    return {"value": round(rate, 2), "unit": "seeds/s", "cores": 1, "kind": "port",
+            "sample": f"{done} roots (32-root steps, keyed sample of the epoch) through the "
+                      "oracle port: numpy/numba sampling on lazily materialised rows + float64 "
+                      "SAGE forward/backward + SGD, one core"}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle.cpu_bench import run_pool
+    from oracle.graphgen import GraphSpec as OSpec
+    spec = OSpec(n=cfg["n"], avg_deg=cfg["avg_deg"], beta=cfg["beta"], p_in=cfg["p_in"],
+                 n_blocks=cfg["n_blocks"], d_cap=cfg["d_cap"], seed=cfg["seed"])
+    kw = dict(arch=cfg["arch"], fanout=cfg["fanout"], dim=cfg["dim"], hidden=cfg["hidden"],
+              classes=cfg["classes"])
+    procs = os.cpu_count() or 1
+    per_step = 16 * procs
+    rate, procs, times = run_pool(spec, kw, cfg["seed"], per_step, args.steps, args.warmup, procs)
+    ms = 1000.0 * sum(times) / len(times)
+    line = {"impl": "reference", "metric": "seeds_per_sec", "value": round(rate, 2),
+            "unit": "seeds/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "roots_per_step": per_step,
+                       "fanout": list(cfg["fanout"]), "hidden": cfg["hidden"]},
+            "cpu_baseline": {"value": round(rate, 2), "unit": "seeds/s", "cores": procs,
+                             "kind": "port",
+                             "sample": f"{per_step} keyed-sample roots per step split over "
+                                       f"{procs} processes (oracle port of the reference path)"},
+            "e2e": {"value": round(rate, 2), "unit": "seeds/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "epoch_time_s_extrapolated": round(cfg["n"] / rate, 1)}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def gather_bytes(sizes_per_step, cfg, e_f=2, e_a=2):
+    """Algorithmic bytes of the layer-1 gather+aggregate:
+    |V|*D*e_f + n1*w1*e_a + 4*(p0 + n1), from the actual batch sizes."""
+    D = cfg["dim"]
+    w1 = 2 * D if cfg["arch"] == "sage-mean" else D
+    tot = 0
+    for n0, n1, p0 in sizes_per_step:
+        tot += n0 * D * e_f + n1 * w1 * e_a + 4 * (p0 + n1)
+    return tot
+
+
+def run_ours(args, cfg):
+    import numpy as np
+    import torch
+    from paper_2409_00657_b200 import _lib
+    from paper_2409_00657_b200.engine import Trainer
+    from paper_2409_00657_b200.featstore import FeatureTable
+    from paper_2409_00657_b200.graph import GraphSpec, generate
+    from paper_2409_00657_b200.model import init_model
+    from paper_2409_00657_b200.rng import chain
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1 or args.gpus > 1:
+        from paper_2409_00657_b200.dist_bench import run_distributed
+        return run_distributed(args, cfg)
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    t0 = time.time()
+    spec = GraphSpec(n=cfg["n"], avg_deg=cfg["avg_deg"], beta=cfg["beta"], p_in=cfg["p_in"],
+                     n_blocks=cfg["n_blocks"], d_cap=cfg["d_cap"], seed=cfg["seed"])
+    g = generate(spec, dev)
+    table = FeatureTable.generated(g.n_vertices, cfg["dim"], cfg["seed"], torch.bfloat16, dev)
+    model = init_model(cfg["arch"], cfg["dim"], cfg["hidden"], len(cfg["fanout"]),
+                       cfg["classes"], chain(cfg["seed"], 0x07), dev)
+    B = cfg["batch"]
+    tr = Trainer(g, table, model, cfg["fanout"], B, cfg["seed"])
+    iters = tr.begin_epoch(0)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+    K, W = args.steps, args.warmup
+    if W + 2 * K > iters:
+        raise SystemExit("epoch too short for the requested steps")
+    for i in range(W):
+        tr.step(i)
+    torch.cuda.synchronize()
+    tr.check()
+    L = len(cfg["fanout"])
+    totals = torch.zeros((K, 2 * L + 2), dtype=torch.int32, device=dev)
+    tot_src = tr.runner.builder.tensors["totals"]
+    _lib.prof_enable(True)
+    _lib.launch_count(reset=True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(0) as clk:
+        ev0.record()
+        for i in range(K):
+            tr.step(W + i)
+            totals[i].copy_(tot_src, non_blocking=True)
+        ev1.record()
+        torch.cuda.synchronize()
+    launches = _lib.launch_count()
+    ms = ev0.elapsed_time(ev1)
+    agg_ms, agg_n = _lib.prof_read(_lib.PROF_AGG1)
+    sites = {name: _lib.prof_read(s) for name, s in (("build", _lib.PROF_BUILD),
+                                                      ("agg1", _lib.PROF_AGG1),
+                                                      ("gemm1", _lib.PROF_GEMM1),
+                                                      ("dw1", _lib.PROF_DW1),
+                                                      ("step", _lib.PROF_STEP),
+                                                      ("sgd", _lib.PROF_SGD))}
+    _lib.prof_enable(False)
+    tr.check()
+    tot = totals.cpu().numpy()
+    sizes = [(int(r[0]), int(r[1]), int(r[L + 1])) for r in tot]
+    value = K * B / (ms / 1000.0)
+    # end-to-end through the public API: pinned host roots in, loss out, every step
+    perm_host = tr.perm[(W + K) * B:(W + 2 * K) * B].cpu().pin_memory()
+    torch.cuda.synchronize()
+    e0 = time.perf_counter()
+    for i in range(K):
+        tr.train_step(perm_host[i * B:(i + 1) * B], W + K + i)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - e0
+    e2e = K * B / e2e_s
+    hbm, tflops, peak_kind = peaks()
+    bytes_per_launch = gather_bytes(sizes, cfg) / K
+    agg_avg_s = agg_ms / max(agg_n, 1) / 1000.0
+    achieved = bytes_per_launch / agg_avg_s / 1e9
+    traffic = None
+    tp = os.path.join(HERE, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(args.config)
+        except Exception:
+            traffic = None
+    line = {
+        "metric": "seeds_per_sec", "value": round(value, 1), "unit": "seeds/s",
+        "n_gpus": 1, "steps": K, "warmup": W, "ms_per_step": round(ms / K, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (GPU-generated graph, keyed features/labels/weights)",
+        "config": {"workload": cfg["workload"], "global_batch": B, "fanout": list(cfg["fanout"]),
+                   "hidden": cfg["hidden"], "n_vertices": g.n_vertices, "n_edges": g.n_targets,
+                   "parallelism": "single GPU (S=1: micrograph == model-centric)",
+                   "l2": "inputs larger than L2 (CSR 6.4 GB, features 28 GB)"},
+        "epoch_time_s_extrapolated": round(g.n_vertices / value, 2),
+        "e2e": {"value": round(e2e, 1), "unit": "seeds/s", "h2d_bytes_per_step": 8 * B,
+                "d2h_bytes_per_step": 4},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": "k_aggregate (layer-1 gather + segment-mean)",
+                     "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4), "traffic": traffic,
+                     "peak_source": peak_kind,
+                     "bytes_per_launch": int(bytes_per_launch),
+                     "avg_launch_us": round(agg_avg_s * 1e6, 2)},
+        "kernel_ms_per_step": {k: round(v[0] / max(v[1], 1), 4) for k, v in sites.items()},
+        "batch_sizes_mean": {"N0": float(np.mean([s[0] for s in sizes])),
+                             "N1": float(np.mean([s[1] for s in sizes])),
+                             "P0": float(np.mean([s[2] for s in sizes]))},
+        "clocks": clk.summary(),
+        "setup_s": round(setup_s, 1),
+    }
+    if not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(cfg, budget_s=args.cpu_budget)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="papers", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -44,6 +44,12 @@ typedef enum {
 const char* hg_last_error(void);
 int hg_version(void);
 int hg_device_sync(void* stream); /* cudaStreamSynchronize + error-flag check */
+/* Kernel-launch counter (every kernel this library launches) and optional
+ * CUDA-event timing of kernel sites: 0 build, 1 layer-1 aggregate,
+ * 2 layer-1 GEMM, 3 layer-1 dW, 4 whole step, 5 layer-2 aggregate, 6 SGD. */
+int hg_launch_count(long long* out, int reset);
+int hg_prof_enable(int on);
+int hg_prof_read(int site, double* total_ms, int* count);
 
 /* ------------------------------------------------------------------------
  * 1. Reference kernel boundary (gnnsim.kernels, kernels.py:31-34)

@@ -73,6 +73,9 @@ PI64 = C.POINTER(C.c_int64)
 SIGNATURES = {
     "hg_version": [],
     "hg_device_sync": [V],
+    "hg_launch_count": [C.POINTER(C.c_longlong), C.c_int],
+    "hg_prof_enable": [C.c_int],
+    "hg_prof_read": [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int)],
     "hg_sample_frontier": [V, V, I64, V, I64, I32, U64, V, V, I64, PI64, V],
     "hg_feature_rows": [V, I64, I32, U64, V, V],
     "hg_feature_table": [I64, I64, I32, I32, U64, I32, V, V],
@@ -139,3 +142,23 @@ def flag_status(code: int, what: str) -> None:
     if code == 3:
         raise InvariantViolation(f"{what}: device invariant violated")
     raise RuntimeError(f"{what}: device error flag {code}")
+
+
+def launch_count(reset: bool = False) -> int:
+    v = C.c_longlong(0)
+    call("hg_launch_count", C.byref(v), int(reset))
+    return int(v.value)
+
+
+def prof_enable(on: bool) -> None:
+    call("hg_prof_enable", int(on))
+
+
+def prof_read(site: int):
+    """(total ms, launches) recorded at a profiling site since prof_enable."""
+    t, n = C.c_double(0), C.c_int(0)
+    call("hg_prof_read", site, C.byref(t), C.byref(n))
+    return t.value, n.value
+
+
+PROF_BUILD, PROF_AGG1, PROF_GEMM1, PROF_DW1, PROF_STEP, PROF_AGG2, PROF_SGD = range(7)

@@ -32,3 +32,76 @@ extern "C" int hg_device_sync(void* stream) {
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;
 }
+
+// ---------------------------------------------------------------- accounting
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+namespace hg {
+static std::atomic<long long> g_launches{0};
+static bool g_prof_on = false;
+static std::mutex g_prof_mu;
+struct SiteEvents {
+  std::vector<cudaEvent_t> beg, end;
+  size_t used = 0;
+  bool open = false;
+};
+static SiteEvents g_sites[PROF_NSITES];
+
+void count_launch(int n) { g_launches += n; }
+
+void prof_begin(int site, cudaStream_t s) {
+  if (!g_prof_on) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  SiteEvents& e = g_sites[site];
+  if (e.used == e.beg.size()) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    e.beg.push_back(a);
+    e.end.push_back(b);
+  }
+  cudaEventRecord(e.beg[e.used], s);
+  e.open = true;
+}
+
+void prof_end(int site, cudaStream_t s) {
+  if (!g_prof_on) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  SiteEvents& e = g_sites[site];
+  if (!e.open) return;
+  cudaEventRecord(e.end[e.used], s);
+  e.used++;
+  e.open = false;
+}
+}  // namespace hg
+
+extern "C" int hg_prof_enable(int on) {
+  std::lock_guard<std::mutex> lk(hg::g_prof_mu);
+  hg::g_prof_on = on != 0;
+  for (auto& e : hg::g_sites) { e.used = 0; e.open = false; }
+  return HG_OK;
+}
+
+extern "C" int hg_prof_read(int site, double* total_ms, int* count) {
+  if (site < 0 || site >= hg::PROF_NSITES) return hg_fail(HG_ERANGE, "bad profiling site");
+  std::lock_guard<std::mutex> lk(hg::g_prof_mu);
+  hg::SiteEvents& e = hg::g_sites[site];
+  double t = 0;
+  for (size_t i = 0; i < e.used; ++i) {
+    HG_CUDA_TRY(cudaEventSynchronize(e.end[i]));
+    float ms = 0;
+    HG_CUDA_TRY(cudaEventElapsedTime(&ms, e.beg[i], e.end[i]));
+    t += ms;
+  }
+  *total_ms = t;
+  *count = (int)e.used;
+  return HG_OK;
+}
+
+extern "C" int hg_launch_count(long long* out, int reset) {
+  *out = hg::g_launches.load();
+  if (reset) hg::g_launches = 0;
+  return HG_OK;
+}

@@ -378,6 +378,7 @@ static void gemm(cudaStream_t s, const TA* A, int lda, const float* B, int ldb, 
                  const int32_t* M_dev, int M_cap, int N, const int32_t* K_dev, int K_cap,
                  const float* bias, const TM* mask, int ldm, int split) {
   dim3 grid((N + BN - 1) / BN, (M_cap + BM - 1) / BM, split);
+  count_launch();
   k_gemm<TA, AT, BT, EPI, TC, TM><<<grid, 256, 0, s>>>(A, lda, B, ldb, C, ldc, M_dev, M_cap, N,
                                                        K_dev, K_cap, bias, mask, ldm);
 }
@@ -390,10 +391,13 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
   const int32_t* tot = d->mg.totals;  // N_0..N_L on device
   const int nb = num_sms() * 4;
   // ---- forward
+  prof_begin(PROF_STEP, s);
   for (int k = 1; k <= L; ++k) {
     const int Wd = k == 1 ? d->feat_ld : H;
     const T* src = k == 1 ? (const T*)d->features : (const T*)d->h[k - 1];
     const int32_t* ids0 = k == 1 ? d->mg.need_ids[0] : nullptr;
+    prof_begin(k == 1 ? PROF_AGG1 : PROF_AGG2, s);
+    count_launch();
     if (sage)
       k_aggregate<T, true><<<nb, 256, 0, s>>>(src, Wd, ids0, d->feat_row, d->mg.self_pos[k],
                                               d->mg.nbr_off[k], d->mg.nbr_idx[k], tot + k, Wd,
@@ -402,17 +406,21 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
       k_aggregate<T, false><<<nb, 256, 0, s>>>(src, Wd, ids0, d->feat_row, d->mg.self_pos[k],
                                                d->mg.nbr_off[k], d->mg.nbr_idx[k], tot + k, Wd,
                                                (T*)d->agg[k], d->in_dim[k]);
+    prof_end(k == 1 ? PROF_AGG1 : PROF_AGG2, s);
+    if (k == 1) prof_begin(PROF_GEMM1, s);
     gemm<T, false, false, EPI_BIAS_RELU, T, T>(s, (const T*)d->agg[k], d->in_dim[k], d->W[k], H,
                                                (T*)d->h[k], H, tot + k, d->max_rows[k], H,
                                                nullptr, d->in_dim[k], d->b[k], nullptr, 0, 1);
+    if (k == 1) prof_end(PROF_GEMM1, s);
   }
   // logits = h_L[roots] @ Wc (need[L] rows are the roots, in order)
   gemm<T, false, false, EPI_STORE, float, T>(s, (const T*)d->h[L], H, d->Wc, C, d->logits, C,
                                              nullptr, n_roots, C, nullptr, H, nullptr, nullptr, 0,
                                              1);
+  count_launch();
   k_softmax_ce<<<(n_roots + 7) / 8, 256, 0, s>>>(d->logits, C, d->roots, n_roots,
                                                  d->label_state, d->loss);
-  if (!backward) return HG_OK;
+  if (!backward) { prof_end(PROF_STEP, s); return HG_OK; }
   // ---- backward (model.py:262-285)
   const int split_r = n_roots >= 4096 ? 8 : 1;
   // gWc += h_L^T dlogits
@@ -425,19 +433,22 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
                                                H, 1);
   {
     dim3 g((H + 31) / 32, 16);
+    count_launch();
     k_colsum<<<g, 256, 0, s>>>(d->dh[L], nullptr, n_roots, H, d->gb[L]);
   }
   for (int k = L; k >= 1; --k) {
     // gW_k += agg_k^T dz_k   (reduction over the N_k rows, split across CTAs)
+    if (k == 1) prof_begin(PROF_DW1, s);
     gemm<T, true, false, EPI_ATOMIC, float, T>(s, (const T*)d->agg[k], d->in_dim[k], d->dh[k], H,
                                                d->gW[k], H, nullptr, d->in_dim[k], H, tot + k,
                                                d->max_rows[k], nullptr, nullptr, 0,
                                                k == L ? split_r : d->split_k);
-    if (k == 1) break;  // layer-1 dX is unused (features are not trainable)
+    if (k == 1) { prof_end(PROF_DW1, s); break; }  // layer-1 dX is unused (features are not trainable)
     // dagg_k = dz_k W_k^T
     gemm<float, false, true, EPI_STORE, float, T>(s, d->dh[k], H, d->W[k], H, d->dagg,
                                                   d->in_dim[k], tot + k, d->max_rows[k],
                                                   d->in_dim[k], nullptr, H, nullptr, nullptr, 0, 1);
+    count_launch(3);
     k_zero_rows<<<nb, 256, 0, s>>>(d->dh[k - 1], tot + (k - 1), H);
     const int grid = (d->max_rows[k] + 7) / 8;
     if (sage)
@@ -452,6 +463,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     k_mask_colsum<T><<<g, 256, 0, s>>>(d->dh[k - 1], (const T*)d->h[k - 1], tot + (k - 1), H,
                                        d->gb[k - 1]);
   }
+  prof_end(PROF_STEP, s);
   return HG_OK;
 }
 
@@ -491,7 +503,10 @@ extern "C" int hg_sgd_update(float* params, float* grads, void* shadow_bf16, int
                              float inv_batch, void* stream) {
   if (n <= 0) return HG_OK;
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  count_launch();
+  prof_begin(PROF_SGD, (cudaStream_t)stream);
   k_sgd<<<grid, 256, 0, (cudaStream_t)stream>>>(params, grads, (bf16*)shadow_bf16, n, lr, inv_batch);
+  prof_end(PROF_SGD, (cudaStream_t)stream);
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;
 }

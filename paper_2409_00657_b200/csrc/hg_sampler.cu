@@ -529,6 +529,8 @@ extern "C" int hg_mg_build(const int64_t* offsets, const int32_t* targets, int64
   if (n_roots == 0) return HG_OK;
   HG_CUDA_TRY(cudaFuncSetAttribute(k_mg_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    c.smem_bytes));
+  count_launch(3);
+  prof_begin(PROF_BUILD, s);
   k_mg_build<<<n_roots, kBuildThreads, c.smem_bytes, s>>>(offsets, targets, n_vertices, roots,
                                                           n_roots, iter_state, roots_per_state,
                                                           c, ws, err_flag);
@@ -536,6 +538,7 @@ extern "C" int hg_mg_build(const int64_t* offsets, const int32_t* targets, int64
   k_mg_scan<<<1, 1024, 0, s>>>(ws, n_roots, c, *out);
   HG_CUDA_TRY(cudaGetLastError());
   k_mg_finalize<<<n_roots, 128, 0, s>>>(ws, n_roots, c, *out);
+  prof_end(PROF_BUILD, s);
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;
 }

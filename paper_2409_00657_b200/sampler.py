@@ -209,8 +209,10 @@ class MicrographBuilder:
         if n > self.max_roots:
             raise ValueError(f"{n} roots > builder capacity {self.max_roots}")
         s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        rp = roots if isinstance(roots, int) else roots.data_ptr()
+        kp = keys if isinstance(keys, int) else keys.data_ptr()
         _lib.call("hg_mg_build", g.offsets.data_ptr(), g.targets.data_ptr(), g.n_vertices,
-                  roots.data_ptr(), n, keys.data_ptr(), int(roots_per_state),
+                  rp, n, kp, int(roots_per_state),
                   C.byref(self.layout), self.ws.data_ptr(), C.byref(self.cbatch),
                   self.err.data_ptr(), s)
         return MicrographBatch(self.L, n, self.tensors)
