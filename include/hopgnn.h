@@ -205,6 +205,13 @@ typedef struct {
 int hg_train_step(const hg_step_desc* d, int32_t n_roots, void* stream);
 /* Forward only: fills logits (and agg/h).  Used by parity tests. */
 int hg_forward(const hg_step_desc* d, int32_t n_roots, void* stream);
+/* bf16 tcgen05 GEMM, fp32 accumulate: C[MxN] = A(m,k) B(k,n).
+ * A K-major: [M x K] row-major, MN-major: [K x M];  B K-major: [N x K], MN-major: [K x N].
+ * epi 0: C f32 store; 1: C bf16 = relu(acc + bias); 2: C f32 += acc (atomic, split-K).
+ * Supported: (K,K) with epi 0/1 and (MN,MN) with epi 0/2; N in {64,128,192,256}. */
+int hg_gemm_bf16(const void* A, int64_t lda, int a_mn_major, const void* B, int64_t ldb,
+                 int b_mn_major, void* C, int64_t ldc, int32_t M, int32_t N, int32_t K,
+                 int32_t epi, const float* bias, int32_t split, void* stream);
 /* theta -= lr * (g * inv_batch); g = 0; refresh bf16 shadow (model.py:315-324). */
 int hg_sgd_update(float* params, float* grads, void* shadow_bf16, int64_t n, float lr,
                   float inv_batch, void* stream);

@@ -92,6 +92,7 @@ SIGNATURES = {
     "hg_train_step": [C.POINTER(StepDesc), I32, V],
     "hg_forward": [C.POINTER(StepDesc), I32, V],
     "hg_sgd_update": [V, V, V, I64, C.c_float, C.c_float, V],
+    "hg_gemm_bf16": [V, I64, C.c_int, V, I64, C.c_int, V, I64, I32, I32, I32, I32, V, I32, V],
 }
 
 
