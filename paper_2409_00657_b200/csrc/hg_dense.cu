@@ -19,6 +19,8 @@
 //   k_sgd          fused update + gradient reset + bf16 shadow refresh
 #include <cuda_bf16.h>
 
+#include <algorithm>
+
 #include "hg_common.cuh"
 
 namespace hg {
@@ -290,10 +292,12 @@ k_scatter(const float* __restrict__ dagg, int ld, const int32_t* __restrict__ se
 }
 
 // dz = dh * (h > 0) in place; gb[c] += sum_rows dz[., c]
+// Optional bf16 copy of dz for the tensor-core dW GEMM, whose row reduction
+// reads up to the next multiple of 64 rows: those padding rows are zeroed.
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_mask_colsum(float* __restrict__ dh, const T* __restrict__ h, const int32_t* __restrict__ n_rows_dev,
-              int H, float* __restrict__ gb) {
+              int H, float* __restrict__ gb, bf16* __restrict__ lowp, int cap_rows) {
   const int n_rows = *n_rows_dev;
   const int c = blockIdx.x * 32 + (threadIdx.x & 31);
   const int r0 = blockIdx.y * 8 + (threadIdx.x >> 5);
@@ -304,7 +308,12 @@ k_mask_colsum(float* __restrict__ dh, const T* __restrict__ h, const int32_t* __
       float v = dh[i];
       v = to_f(h[i]) > 0.f ? v : 0.f;
       dh[i] = v;
+      if (lowp) lowp[i] = __float2bfloat16_rn(v);
       s += v;
+    }
+    if (lowp) {
+      const int pad = min(cap_rows, (n_rows + 63) / 64 * 64);
+      for (int r = n_rows + r0; r < pad; r += gridDim.y * 8) lowp[(int64_t)r * H + c] = __float2bfloat16_rn(0.f);
     }
   }
   __shared__ float red[8][33];
@@ -321,13 +330,22 @@ k_mask_colsum(float* __restrict__ dh, const T* __restrict__ h, const int32_t* __
 // column sums of an already-masked matrix (bias grad of the top layer)
 __global__ void __launch_bounds__(256)
 k_colsum(const float* __restrict__ x, const int32_t* __restrict__ n_rows_dev, int n_rows_host,
-         int H, float* __restrict__ gb) {
+         int H, float* __restrict__ gb, bf16* __restrict__ lowp, int cap_rows) {
   const int n_rows = n_rows_dev ? *n_rows_dev : n_rows_host;
   const int c = blockIdx.x * 32 + (threadIdx.x & 31);
   const int r0 = blockIdx.y * 8 + (threadIdx.x >> 5);
   float s = 0.f;
-  if (c < H)
-    for (int r = r0; r < n_rows; r += gridDim.y * 8) s += x[(int64_t)r * H + c];
+  if (c < H) {
+    for (int r = r0; r < n_rows; r += gridDim.y * 8) {
+      const float v = x[(int64_t)r * H + c];
+      if (lowp) lowp[(int64_t)r * H + c] = __float2bfloat16_rn(v);
+      s += v;
+    }
+    if (lowp) {
+      const int pad = min(cap_rows, (n_rows + 63) / 64 * 64);
+      for (int r = n_rows + r0; r < pad; r += gridDim.y * 8) lowp[(int64_t)r * H + c] = __float2bfloat16_rn(0.f);
+    }
+  }
   __shared__ float red[8][33];
   red[threadIdx.x >> 5][threadIdx.x & 31] = s;
   __syncthreads();
@@ -337,6 +355,33 @@ k_colsum(const float* __restrict__ x, const int32_t* __restrict__ n_rows_dev, in
     for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
     atomicAdd(gb + c, t);
   }
+}
+
+// WT[c][r] = bf16(W[r][c]): K-major B operand of the tensor-core layer GEMM
+__global__ void k_transpose_bf16(const float* __restrict__ W, int rows, int cols,
+                                 bf16* __restrict__ WT) {
+  __shared__ float tile[32][33];
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = r0 + i, c = c0 + threadIdx.x;
+    tile[i][threadIdx.x] = (r < rows && c < cols) ? W[(int64_t)r * cols + c] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int c = c0 + i, r = r0 + threadIdx.x;
+    if (c < cols && r < rows) WT[(int64_t)c * rows + r] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+  }
+}
+
+// zero rows [n_rows, min(roundup64(n_rows), cap)) of a bf16 [rows x W] matrix
+__global__ void k_zero_pad_rows(bf16* __restrict__ x, const int32_t* __restrict__ n_rows_dev, int W,
+                                int cap_rows) {
+  const int n = *n_rows_dev;
+  const int pad = min(cap_rows, (n + 63) / 64 * 64);
+  const int64_t total = (int64_t)(pad - n) * W;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x)
+    x[(int64_t)n * W + i] = __float2bfloat16_rn(0.f);
 }
 
 __global__ void k_zero_rows(float* __restrict__ x, const int32_t* __restrict__ n_rows_dev, int W) {
@@ -361,6 +406,10 @@ __global__ void k_sgd(float* __restrict__ p, float* __restrict__ g, bf16* __rest
 }
 
 // ------------------------------------------------------------------ launchers
+
+int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb, bool b_mn,
+              void* C, int64_t ldc, int M, int N, int K, const int32_t* M_dev,
+              const int32_t* K_dev, int epi, const float* bias, int split, cudaStream_t s);
 
 static int g_num_sms = 0;
 static int num_sms() {
@@ -390,8 +439,17 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
   const int H = d->hidden, C = d->n_classes;
   const int32_t* tot = d->mg.totals;  // N_0..N_L on device
   const int nb = num_sms() * 4;
+  // tensor-core path: bf16 operands, H a multiple of 64 up to 256 (one N tile)
+  const bool tc = sizeof(T) == 2 && d->use_tc && H % 64 == 0 && H <= 256;
   // ---- forward
   prof_begin(PROF_STEP, s);
+  if (tc) {
+    for (int k = 1; k <= L; ++k) {
+      dim3 g((H + 31) / 32, (d->in_dim[k] + 31) / 32), b(32, 8);
+      count_launch();
+      k_transpose_bf16<<<g, b, 0, s>>>(d->W[k], d->in_dim[k], H, (bf16*)d->Wlp[k]);
+    }
+  }
   for (int k = 1; k <= L; ++k) {
     const int Wd = k == 1 ? d->feat_ld : H;
     const T* src = k == 1 ? (const T*)d->features : (const T*)d->h[k - 1];
@@ -408,9 +466,19 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
                                                (T*)d->agg[k], d->in_dim[k]);
     prof_end(k == 1 ? PROF_AGG1 : PROF_AGG2, s);
     if (k == 1) prof_begin(PROF_GEMM1, s);
-    gemm<T, false, false, EPI_BIAS_RELU, T, T>(s, (const T*)d->agg[k], d->in_dim[k], d->W[k], H,
-                                               (T*)d->h[k], H, tot + k, d->max_rows[k], H,
-                                               nullptr, d->in_dim[k], d->b[k], nullptr, 0, 1);
+    if (tc) {
+      if (backward) {
+        count_launch();
+        k_zero_pad_rows<<<4, 256, 0, s>>>((bf16*)d->agg[k], tot + k, d->in_dim[k], d->max_rows[k]);
+      }
+      int st = umma_gemm(d->agg[k], d->in_dim[k], false, d->Wlp[k], d->in_dim[k], false, d->h[k], H,
+                         d->max_rows[k], H, d->in_dim[k], tot + k, nullptr, 1, d->b[k], 1, s);
+      if (st) return st;
+    } else {
+      gemm<T, false, false, EPI_BIAS_RELU, T, T>(s, (const T*)d->agg[k], d->in_dim[k], d->W[k], H,
+                                                 (T*)d->h[k], H, tot + k, d->max_rows[k], H,
+                                                 nullptr, d->in_dim[k], d->b[k], nullptr, 0, 1);
+    }
     if (k == 1) prof_end(PROF_GEMM1, s);
   }
   // logits = h_L[roots] @ Wc (need[L] rows are the roots, in order)
@@ -434,15 +502,27 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
   {
     dim3 g((H + 31) / 32, 16);
     count_launch();
-    k_colsum<<<g, 256, 0, s>>>(d->dh[L], nullptr, n_roots, H, d->gb[L]);
+    k_colsum<<<g, 256, 0, s>>>(d->dh[L], nullptr, n_roots, H, d->gb[L],
+                               tc ? (bf16*)d->lowp_scratch : nullptr, d->max_rows[L]);
   }
   for (int k = L; k >= 1; --k) {
     // gW_k += agg_k^T dz_k   (reduction over the N_k rows, split across CTAs)
     if (k == 1) prof_begin(PROF_DW1, s);
-    gemm<T, true, false, EPI_ATOMIC, float, T>(s, (const T*)d->agg[k], d->in_dim[k], d->dh[k], H,
-                                               d->gW[k], H, nullptr, d->in_dim[k], H, tot + k,
-                                               d->max_rows[k], nullptr, nullptr, 0,
-                                               k == L ? split_r : d->split_k);
+    if (tc) {
+      // both operands MN-major straight from their row-major buffers
+      const int kblocks = (d->max_rows[k] + 63) / 64;
+      const int tiles = (d->in_dim[k] + 127) / 128;
+      int split = (kblocks + 5) / 6;
+      split = std::max(1, std::min(split, std::max(1, num_sms() / tiles)));
+      int st = umma_gemm(d->agg[k], d->in_dim[k], true, d->lowp_scratch, H, true, d->gW[k], H,
+                         d->in_dim[k], H, d->max_rows[k], nullptr, tot + k, 2, nullptr, split, s);
+      if (st) return st;
+    } else {
+      gemm<T, true, false, EPI_ATOMIC, float, T>(s, (const T*)d->agg[k], d->in_dim[k], d->dh[k], H,
+                                                 d->gW[k], H, nullptr, d->in_dim[k], H, tot + k,
+                                                 d->max_rows[k], nullptr, nullptr, 0,
+                                                 k == L ? split_r : d->split_k);
+    }
     if (k == 1) { prof_end(PROF_DW1, s); break; }  // layer-1 dX is unused (features are not trainable)
     // dagg_k = dz_k W_k^T
     gemm<float, false, true, EPI_STORE, float, T>(s, d->dh[k], H, d->W[k], H, d->dagg,
@@ -461,7 +541,8 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
                                             d->dh[k - 1]);
     dim3 g((H + 31) / 32, 64);
     k_mask_colsum<T><<<g, 256, 0, s>>>(d->dh[k - 1], (const T*)d->h[k - 1], tot + (k - 1), H,
-                                       d->gb[k - 1]);
+                                       d->gb[k - 1], tc ? (bf16*)d->lowp_scratch : nullptr,
+                                       d->max_rows[k - 1]);
   }
   prof_end(PROF_STEP, s);
   return HG_OK;

@@ -150,8 +150,8 @@ class ModelState:
         """theta -= lr * acc / batch_total; acc = 0 (model.py:315-324)."""
         inv = 1.0 / batch_total if batch_total > 0 else 1.0
         s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
-        _lib.call("hg_sgd_update", self.flat.data_ptr(), self.grad.data_ptr(),
-                  self.shadow.data_ptr(), self.flat.numel(), float(lr), float(inv), s)
+        _lib.call("hg_sgd_update", self.flat.data_ptr(), self.grad.data_ptr(), None,
+                  self.flat.numel(), float(lr), float(inv), s)
 
 
 def init_model(arch: str, feat_dim: int, hidden: int, n_layers: int, n_classes: int,
