@@ -72,11 +72,11 @@ int hg_feature_rows(const int64_t* ids, int64_t n, int32_t dim, uint64_t state, 
  * 2. Counter RNG products (rng.py, engine.py:268-287, model.py:69-109)
  * --------------------------------------------------------------------- */
 
-/* Feature table init: row v of a shard = feature_rows(v) (featstore.py:161-184).
- * Writes rows for ids [first, first+count) into out with row stride `ld`
- * elements (ld >= dim, padding columns zeroed).  dtype 0 = f32, 1 = bf16 (RNE). */
-int hg_feature_table(int64_t first, int64_t count, int32_t dim, int32_t ld, uint64_t state,
-                     int32_t dtype, void* out, void* stream);
+/* Feature table init: row i of a shard = feature_rows(v_i) (featstore.py:161-184),
+ * v_i = ids[i] (ids != NULL) or first + i.  Row stride `ld` elements (ld >= dim,
+ * padding columns zeroed).  dtype 0 = f32, 1 = bf16 (RNE). */
+int hg_feature_table(const int64_t* ids, int64_t first, int64_t count, int32_t dim, int32_t ld,
+                     uint64_t state, int32_t dtype, void* out, void* stream);
 
 /* Epoch permutation: stable argsort of chain(state, v) for v < n
  * (engine.py:273-275).  perm_out int64[n].  ws_bytes query when ws == NULL. */

@@ -78,7 +78,7 @@ SIGNATURES = {
     "hg_prof_read": [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int)],
     "hg_sample_frontier": [V, V, I64, V, I64, I32, U64, V, V, I64, PI64, V],
     "hg_feature_rows": [V, I64, I32, U64, V, V],
-    "hg_feature_table": [I64, I64, I32, I32, U64, I32, V, V],
+    "hg_feature_table": [V, I64, I64, I32, I32, U64, I32, V, V],
     "hg_epoch_permutation": [I64, U64, V, V, PSZ, V],
     "hg_glorot": [I32, I32, U64, I32, V, V],
     "hg_graph_raw_degrees": [C.POINTER(GraphTables), V, V],

@@ -23,11 +23,12 @@ __global__ void k_feature_rows(const int64_t* __restrict__ ids, int64_t n, int d
 
 // One warp per row; 8-column chunks so each lane writes 16 B (bf16) / 32 B (f32).
 template <typename T>
-__global__ void k_feature_table(int64_t first, int64_t count, int dim, int ld, uint64_t state,
-                                T* __restrict__ out) {
+__global__ void k_feature_table(const int64_t* __restrict__ ids, int64_t first, int64_t count,
+                                int dim, int ld, uint64_t state, T* __restrict__ out) {
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (row >= count) return;
-  const uint64_t rk = mix64(state ^ (uint64_t)(first + row));
+  const int64_t v = ids ? ids[row] : first + row;
+  const uint64_t rk = mix64(state ^ (uint64_t)v);
   T* dst = out + row * (int64_t)ld;
   for (int col = (threadIdx.x & 31); col < ld; col += 32) {
     const float v = col < dim ? feature_value(rk, col) : 0.0f;
@@ -68,16 +69,17 @@ extern "C" int hg_feature_rows(const int64_t* ids, int64_t n, int32_t dim, uint6
   return HG_OK;
 }
 
-extern "C" int hg_feature_table(int64_t first, int64_t count, int32_t dim, int32_t ld,
-                                uint64_t state, int32_t dtype, void* out, void* stream) {
+extern "C" int hg_feature_table(const int64_t* ids, int64_t first, int64_t count, int32_t dim,
+                                int32_t ld, uint64_t state, int32_t dtype, void* out,
+                                void* stream) {
   if (dim < 1 || ld < dim) return hg_fail(HG_ERANGE, "need 1 <= dim <= ld");
   if (count == 0) return HG_OK;
   const unsigned grid = (unsigned)((count + 7) / 8);
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == 0)
-    k_feature_table<float><<<grid, 256, 0, s>>>(first, count, dim, ld, state, (float*)out);
+    k_feature_table<float><<<grid, 256, 0, s>>>(ids, first, count, dim, ld, state, (float*)out);
   else if (dtype == 1)
-    k_feature_table<__nv_bfloat16><<<grid, 256, 0, s>>>(first, count, dim, ld, state,
+    k_feature_table<__nv_bfloat16><<<grid, 256, 0, s>>>(ids, first, count, dim, ld, state,
                                                        (__nv_bfloat16*)out);
   else
     return hg_fail(HG_ECONFIG, "dtype must be 0 (f32) or 1 (bf16)");

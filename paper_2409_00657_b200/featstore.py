@@ -118,12 +118,14 @@ class FeatureTable:
     def act_dtype(self) -> int:
         return 1 if self.dtype == torch.bfloat16 else 0
 
-    def fill_generated(self, first_vertex: int, count: int, state: int, row0: int = 0) -> None:
-        """Rows row0.. = feature_rows(first_vertex..first_vertex+count) (bit-exact f32;
-        bf16 tables hold the round-to-nearest-even cast)."""
+    def fill_generated(self, first_vertex: int, count: int, state: int, row0: int = 0,
+                       ids: torch.Tensor = None) -> None:
+        """Rows row0.. = feature_rows(first_vertex..first_vertex+count), or of the
+        int64 device `ids` (bit-exact f32; bf16 tables hold the RNE cast)."""
         code = 1 if self.dtype == torch.bfloat16 else 0
         ptr = self.table.data_ptr() + row0 * self.ld * self.table.element_size()
-        _lib.call("hg_feature_table", int(first_vertex), int(count), self.dim, self.ld,
+        _lib.call("hg_feature_table", ids.data_ptr() if ids is not None else None,
+                  int(first_vertex), int(count), self.dim, self.ld,
                   int(state) & ((1 << 64) - 1), code, ptr,
                   torch.cuda.current_stream(self.device).cuda_stream)
 
