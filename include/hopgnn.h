@@ -198,6 +198,7 @@ typedef struct {
   float* logits;                         /* [max_roots x C] (dlogits after backward)   */
   float* loss;                           /* [max_roots] per-root softmax-CE            */
   void* lowp_scratch;                    /* bf16 [max_rows[1] x H] (tcgen05 dW path)    */
+  void* Wb[HG_MAX_LAYERS + 1];           /* bf16 copies of W (tcgen05 dX path)          */
 } hg_step_desc;
 
 /* Forward + backward of the batch in d->mg for n_roots roots; gradients are

@@ -62,7 +62,8 @@ class StepDesc(C.Structure):
                 ("W", _P7V), ("b", _P7V), ("Wc", C.c_void_p), ("Wlp", _P7V), ("Wclp", C.c_void_p),
                 ("gW", _P7V), ("gb", _P7V), ("gWc", C.c_void_p),
                 ("agg", _P7V), ("h", _P7V), ("dh", _P7V), ("dagg", C.c_void_p),
-                ("logits", C.c_void_p), ("loss", C.c_void_p), ("lowp_scratch", C.c_void_p)]
+                ("logits", C.c_void_p), ("loss", C.c_void_p), ("lowp_scratch", C.c_void_p),
+                ("Wb", _P7V)]
 
 
 V, I32, I64, U64, SZ = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_size_t

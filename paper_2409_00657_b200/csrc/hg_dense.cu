@@ -255,6 +255,80 @@ __global__ void k_softmax_ce(float* __restrict__ logits, int C, const int64_t* _
   if (lane == 0) loss[r] = logf(s) - (xl - mx);
 }
 
+// Fused classifier head (model.py:246, 253-265): per root, logits = h_L @ W_c
+// (no bias), softmax-CE with the label hashed on the fly, dlogits, then
+// dz_L = (dlogits @ W_cᵀ) * (h_L > 0) and the bias gradient of layer L.
+// One warp per root; W_c staged once per CTA in shared memory with an odd
+// row pitch so both the class-parallel and the hidden-parallel loops are
+// bank-conflict free.
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_head(const T* __restrict__ hL, const float* __restrict__ Wc, int H, int C,
+       const int64_t* __restrict__ roots, int n_roots, uint64_t label_state,
+       float* __restrict__ dlogits, float* __restrict__ loss, float* __restrict__ dz,
+       bf16* __restrict__ dz_lowp, int cap_rows, float* __restrict__ gb, int backward) {
+  extern __shared__ float sm[];
+  const int pitch = C | 1;
+  float* ws = sm;                                   // [H][pitch]
+  float* gbs = ws + (size_t)H * pitch;              // [H]
+  float* rowbuf = gbs + H;                          // [8][H]
+  float* dlbuf = rowbuf + 8 * H;                    // [8][C]
+  for (int i = threadIdx.x; i < H * C; i += blockDim.x) ws[(i / C) * pitch + i % C] = Wc[i];
+  for (int i = threadIdx.x; i < H; i += blockDim.x) gbs[i] = 0.f;
+  __syncthreads();
+  const int w = warp_id(), lane = lane_id();
+  float* hrow = rowbuf + w * H;
+  float* dl = dlbuf + w * C;
+  for (int r = blockIdx.x * 8 + w; r < n_roots; r += gridDim.x * 8) {
+    for (int h = lane; h < H; h += 32) hrow[h] = to_f(hL[(int64_t)r * H + h]);
+    __syncwarp();
+    float mx = -INFINITY;
+    for (int c = lane; c < C; c += 32) {
+      float acc = 0.f;
+      for (int h = 0; h < H; ++h) acc = fmaf(hrow[h], ws[h * pitch + c], acc);
+      dl[c] = acc;
+      mx = fmaxf(mx, acc);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float s = 0.f;
+    for (int c = lane; c < C; c += 32) s += expf(dl[c] - mx);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const int label = (int)(mix64(label_state ^ (uint64_t)roots[r]) % (uint64_t)C);
+    __syncwarp();
+    const float xl = dl[label];
+    __syncwarp();
+    const float inv = 1.0f / s;
+    for (int c = lane; c < C; c += 32) {
+      const float g = expf(dl[c] - mx) * inv - (c == label ? 1.f : 0.f);
+      dl[c] = g;
+      if (backward) dlogits[(int64_t)r * C + c] = g;
+    }
+    if (lane == 0) loss[r] = logf(s) - (xl - mx);
+    __syncwarp();
+    if (backward) {
+      for (int h = lane; h < H; h += 32) {
+        float acc = 0.f;
+        for (int c = 0; c < C; ++c) acc = fmaf(dl[c], ws[h * pitch + c], acc);
+        const float v = hrow[h] > 0.f ? acc : 0.f;
+        dz[(int64_t)r * H + h] = v;
+        if (dz_lowp) dz_lowp[(int64_t)r * H + h] = __float2bfloat16_rn(v);
+        atomicAdd(gbs + h, v);
+      }
+    }
+    __syncwarp();
+  }
+  if (backward && dz_lowp && blockIdx.x == 0) {  // zero padding rows for the tensor-core dW
+    const int pad = min(cap_rows, (n_roots + 63) / 64 * 64);
+    for (int64_t i = (int64_t)n_roots * H + threadIdx.x; i < (int64_t)pad * H; i += blockDim.x)
+      dz_lowp[i] = __float2bfloat16_rn(0.f);
+  }
+  __syncthreads();
+  if (backward)
+    for (int h = threadIdx.x; h < H; h += blockDim.x) atomicAdd(gb + h, gbs[h]);
+}
+
 // ------------------------------------------------------------------ backward
 
 // Transpose of k_aggregate (model.py:266-285): warp per destination row.
@@ -359,12 +433,14 @@ k_colsum(const float* __restrict__ x, const int32_t* __restrict__ n_rows_dev, in
 
 // WT[c][r] = bf16(W[r][c]): K-major B operand of the tensor-core layer GEMM
 __global__ void k_transpose_bf16(const float* __restrict__ W, int rows, int cols,
-                                 bf16* __restrict__ WT) {
+                                 bf16* __restrict__ WT, bf16* __restrict__ Wplain) {
   __shared__ float tile[32][33];
   const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int r = r0 + i, c = c0 + threadIdx.x;
-    tile[i][threadIdx.x] = (r < rows && c < cols) ? W[(int64_t)r * cols + c] : 0.f;
+    const float v = (r < rows && c < cols) ? W[(int64_t)r * cols + c] : 0.f;
+    tile[i][threadIdx.x] = v;
+    if (Wplain && r < rows && c < cols) Wplain[(int64_t)r * cols + c] = __float2bfloat16_rn(v);
   }
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -447,7 +523,8 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     for (int k = 1; k <= L; ++k) {
       dim3 g((H + 31) / 32, (d->in_dim[k] + 31) / 32), b(32, 8);
       count_launch();
-      k_transpose_bf16<<<g, b, 0, s>>>(d->W[k], d->in_dim[k], H, (bf16*)d->Wlp[k]);
+      k_transpose_bf16<<<g, b, 0, s>>>(d->W[k], d->in_dim[k], H, (bf16*)d->Wlp[k],
+                                       backward && k >= 2 ? (bf16*)d->Wb[k] : nullptr);
     }
   }
   for (int k = 1; k <= L; ++k) {
@@ -481,30 +558,28 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     }
     if (k == 1) prof_end(PROF_GEMM1, s);
   }
-  // logits = h_L[roots] @ Wc (need[L] rows are the roots, in order)
-  gemm<T, false, false, EPI_STORE, float, T>(s, (const T*)d->h[L], H, d->Wc, C, d->logits, C,
-                                             nullptr, n_roots, C, nullptr, H, nullptr, nullptr, 0,
-                                             1);
-  count_launch();
-  k_softmax_ce<<<(n_roots + 7) / 8, 256, 0, s>>>(d->logits, C, d->roots, n_roots,
-                                                 d->label_state, d->loss);
+  // classifier head: logits, softmax-CE, dlogits, dz_L, gb_L (one fused kernel)
+  {
+    const size_t smem = ((size_t)H * (C | 1) + H + 8 * H + 8 * C) * sizeof(float);
+    static size_t smem_set = 0;
+    if (smem > 48 * 1024 && smem > smem_set) {
+      cudaFuncSetAttribute(k_head<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      smem_set = smem;
+    }
+    const int grid = std::max(1, std::min(num_sms(), (n_roots + 7) / 8));
+    count_launch();
+    k_head<T><<<grid, 256, smem, s>>>((const T*)d->h[L], d->Wc, H, C, d->roots, n_roots,
+                                      d->label_state, d->logits, d->loss, d->dh[L],
+                                      tc ? (bf16*)d->lowp_scratch : nullptr, d->max_rows[L],
+                                      d->gb[L], backward ? 1 : 0);
+  }
   if (!backward) { prof_end(PROF_STEP, s); return HG_OK; }
   // ---- backward (model.py:262-285)
-  const int split_r = n_roots >= 4096 ? 8 : 1;
+  const int split_r = std::max(1, std::min(32, n_roots / 64));
   // gWc += h_L^T dlogits
   gemm<T, true, false, EPI_ATOMIC, float, T>(s, (const T*)d->h[L], H, d->logits, C, d->gWc, C,
                                              nullptr, H, C, nullptr, n_roots, nullptr, nullptr, 0,
                                              split_r);
-  // dz_L = (dlogits Wc^T) * (h_L > 0)
-  gemm<float, false, true, EPI_MASK, float, T>(s, d->logits, C, d->Wc, C, d->dh[L], H, nullptr,
-                                               n_roots, H, nullptr, C, nullptr, (const T*)d->h[L],
-                                               H, 1);
-  {
-    dim3 g((H + 31) / 32, 16);
-    count_launch();
-    k_colsum<<<g, 256, 0, s>>>(d->dh[L], nullptr, n_roots, H, d->gb[L],
-                               tc ? (bf16*)d->lowp_scratch : nullptr, d->max_rows[L]);
-  }
   for (int k = L; k >= 1; --k) {
     // gW_k += agg_k^T dz_k   (reduction over the N_k rows, split across CTAs)
     if (k == 1) prof_begin(PROF_DW1, s);
@@ -525,9 +600,16 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     }
     if (k == 1) { prof_end(PROF_DW1, s); break; }  // layer-1 dX is unused (features are not trainable)
     // dagg_k = dz_k W_k^T
-    gemm<float, false, true, EPI_STORE, float, T>(s, d->dh[k], H, d->W[k], H, d->dagg,
-                                                  d->in_dim[k], tot + k, d->max_rows[k],
-                                                  d->in_dim[k], nullptr, H, nullptr, nullptr, 0, 1);
+    if (tc && d->in_dim[k] % 64 == 0 && d->Wb[k]) {
+      int st = umma_gemm(d->lowp_scratch, H, false, d->Wb[k], H, false, d->dagg, d->in_dim[k],
+                         d->max_rows[k], d->in_dim[k], H, tot + k, nullptr, 0, nullptr, 1, s);
+      if (st) return st;
+    } else {
+      gemm<float, false, true, EPI_STORE, float, T>(s, d->dh[k], H, d->W[k], H, d->dagg,
+                                                    d->in_dim[k], tot + k, d->max_rows[k],
+                                                    d->in_dim[k], nullptr, H, nullptr, nullptr, 0,
+                                                    1);
+    }
     count_launch(3);
     k_zero_rows<<<nb, 256, 0, s>>>(d->dh[k - 1], tot + (k - 1), H);
     const int grid = (d->max_rows[k] + 7) / 8;

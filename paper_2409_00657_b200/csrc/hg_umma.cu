@@ -346,7 +346,8 @@ static int launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const UmmaArgs
 int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb, bool b_mn,
               void* C, int64_t ldc, int M, int N, int K, const int32_t* M_dev,
               const int32_t* K_dev, int epi, const float* bias, int split, cudaStream_t s) {
-  if (N % 64 || N > 256 || N <= 0) return hg_fail(HG_ECONFIG, "umma N must be 64..256, multiple of 64");
+  if (N % 64 || N <= 0 || (N > 256 && N % 256)) return hg_fail(HG_ECONFIG, "umma N must be a multiple of 64 (<= 256) or of 256");
+  const int bn = N > 256 ? 256 : N;  // N tile (grid.y covers the rest)
   if (lda % 8 || ldb % 8) return hg_fail(HG_ECONFIG, "umma leading dims must be multiples of 8");
   CUtensorMap ma, mb;
   int st;
@@ -355,10 +356,10 @@ int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
   else st = make_map(&ma, A, (uint64_t)K, (uint64_t)M, lda, BK_T, BM_T);
   if (st) return st;
   if (b_mn) st = make_map(&mb, B, (uint64_t)N, (uint64_t)K, ldb, 64, BK_T);
-  else st = make_map(&mb, B, (uint64_t)K, (uint64_t)N, ldb, BK_T, (uint32_t)N);
+  else st = make_map(&mb, B, (uint64_t)K, (uint64_t)N, ldb, BK_T, (uint32_t)bn);
   if (st) return st;
   UmmaArgs a{M, N, K, M_dev, K_dev, C, ldc, bias};
-  const int bn = N;  // one N tile
+
 #define HG_UMMA_CASE(AM, BMJ, BNV, E)                                                       \
   if (a_mn == AM && b_mn == BMJ && bn == BNV && epi == E)                                   \
     return launch_t<AM, BMJ, BNV, E>(ma, mb, a, split, s);

@@ -79,6 +79,9 @@ class CellRunner:
         d.logits = self.logits.data_ptr()
         d.loss = self.loss.data_ptr()
         d.lowp_scratch = self.lowp.data_ptr()
+        self.wb16 = torch.empty(model.flat.numel(), dtype=torch.bfloat16, device=dev)
+        for k in range(1, L + 1):
+            d.Wb[k] = self.wb16.data_ptr() + 2 * int(model.offsets[k - 1])
         self.desc = d
         self.n_roots = 0
 
