@@ -214,7 +214,7 @@ def run_ours(args, cfg):
         ev0.record()
         for i in range(K):
             tr.step(W + i)
-            totals[i].copy_(tot_src, non_blocking=True)
+            totals[i].copy_(tr.last_runner.builder.tensors["totals"], non_blocking=True)
         ev1.record()
         torch.cuda.synchronize()
     launches = _lib.launch_count()
@@ -232,11 +232,20 @@ def run_ours(args, cfg):
     sizes = [(int(r[0]), int(r[1]), int(r[L + 1])) for r in tot]
     value = K * B / (ms / 1000.0)
     # end-to-end through the public API: pinned host roots in, loss out, every step
-    perm_host = tr.perm[(W + K) * B:(W + 2 * K) * B].cpu().pin_memory()
+    E0 = W + K  # e2e iterations: W untimed warm-up, then K timed
+    perm_host = tr.perm[E0 * B:(E0 + W + K + 1) * B].cpu().pin_memory()
+
+    def host_roots(j):
+        return perm_host[j * B:(j + 1) * B]
+
+    for j in range(W):
+        tr.train_step(host_roots(j), E0 + j, host_roots(j + 1))
+    tr.last_loss()
     torch.cuda.synchronize()
     e0 = time.perf_counter()
-    for i in range(K):
-        tr.train_step(perm_host[i * B:(i + 1) * B], W + K + i)
+    for j in range(W, W + K):
+        tr.train_step(host_roots(j), E0 + j, host_roots(j + 1) if j + 1 < W + K else None)
+    tr.last_loss()  # the final step's loss reaches the host inside the timed region
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - e0
     e2e = K * B / e2e_s
@@ -316,15 +325,17 @@ def run_distributed(args, cfg):
                        cfg["classes"], chain(cfg["seed"], 0x07), dev)
     B = cfg["batch"]
     mode = args.mode
-    tr = MicrographTrainer(g, part, model, cfg["fanout"], B, cfg["seed"], mode=mode)
+    tr = MicrographTrainer(g, part, model, cfg["fanout"], B, cfg["seed"], mode=mode,
+                           pregather=args.pregather)
     iters = tr.begin_epoch(0)
     torch.cuda.synchronize()
     setup_s = time.time() - t0
     K, W = args.steps, args.warmup
     for i in range(W):
-        tr.step(i)
+        tr.step(i, want_loss=False)
     torch.cuda.synchronize()
     dist.barrier()
+    tr.flush_accounting()
     tr.ledger = type(tr.ledger)()
     tr.traffic = type(tr.traffic)()
     if rank == 0:
@@ -337,8 +348,10 @@ def run_distributed(args, cfg):
     dist.barrier()
     torch.cuda.synchronize()
     ev0.record()
+    h0 = time.perf_counter()
     for i in range(K):
-        tr.step(W + i)
+        tr.step(W + i, want_loss=False)
+    host_ms = (time.perf_counter() - h0) * 1000.0 / K
     ev1.record()
     torch.cuda.synchronize()
     dist.barrier()
@@ -349,10 +362,28 @@ def run_distributed(args, cfg):
     ms = float(ms.item())
     launches = _lib.launch_count() if rank == 0 else 0
     agg = _lib.prof_read(_lib.PROF_AGG1) if rank == 0 else (0.0, 0)
+    sites = {}
+    if rank == 0:
+        for name, site in (("build", _lib.PROF_BUILD), ("agg1", _lib.PROF_AGG1),
+                           ("gemm1", _lib.PROF_GEMM1), ("dw1", _lib.PROF_DW1),
+                           ("step", _lib.PROF_STEP), ("sgd", _lib.PROF_SGD)):
+            t, c = _lib.prof_read(site)
+            sites[name] = round(t / max(c, 1), 4)
+        _lib.prof_enable(False)
     led = tr.global_ledger()
     traffic = torch.tensor([tr.traffic.total(), tr.traffic.feature_bytes,
                             tr.traffic.hop_bytes, tr.traffic.allreduce_bytes], device=dev)
     dist.all_reduce(traffic)
+    # end to end: same public step, loss read back every step
+    dist.barrier()
+    e0 = time.perf_counter()
+    for i in range(K):
+        tr.step(W + K + i, want_loss=True)  # returns the previous step's loss
+    tr.last_loss()
+    torch.cuda.synchronize()
+    e2e_s = torch.tensor([time.perf_counter() - e0], device=dev)
+    dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_value = K * S * B / float(e2e_s.item())
     # model-centric feature-fetch baseline on the same iterations (engine.py:485-507)
     mc_rows = np.zeros(S, dtype=np.int64)
     n_mc = min(K, 8)
@@ -376,12 +407,15 @@ def run_distributed(args, cfg):
             "config": {"workload": cfg["workload"], "global_batch": S * B,
                        "fanout": list(cfg["fanout"]), "hidden": cfg["hidden"],
                        "parallelism": f"micrograph x{S} ({mode}; features sharded by planted "
-                                      "block, CSR replicated)",
+                                      "block, CSR replicated; remote rows "
+                                      + ("pre-gathered by NCCL all-to-all)" if args.pregather
+                                         else "read over NVLink by the gather kernel)"),
                        "l2": "inputs larger than L2"},
             "epoch_time_s_extrapolated": round(g.n_vertices / value, 2),
-            "e2e": {"value": round(value, 1), "unit": "seeds/s",
-                    "h2d_bytes_per_step": 8 * B, "d2h_bytes_per_step": 4,
-                    "note": "step() is the public API: host roots in, loss read back"},
+            "e2e": {"value": round(e2e_value, 1), "unit": "seeds/s",
+                    "h2d_bytes_per_step": 8 * B + 8, "d2h_bytes_per_step": 4,
+                    "note": "MicrographTrainer.step public API: pinned host roots in, loss "
+                            "read back each step"},
             "gpu_launches": int(launches),
             "cross_gpu_bytes": {
                 "reference_accounting_per_iter": round(per_iter_ref, 1),
@@ -396,6 +430,8 @@ def run_distributed(args, cfg):
                          "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
                          "traffic": None, "peak_source": peak_kind,
                          "avg_launch_us": round(agg[0] / max(agg[1], 1) * 1000, 2)},
+            "kernel_ms_per_step": sites,
+            "host_enqueue_ms_per_step": round(host_ms, 4),
             "clocks": clk.summary() if clk else None,
             "setup_s": round(setup_s, 1),
         }
@@ -414,6 +450,9 @@ def main():
     ap.add_argument("--config", default="papers", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--pregather", action="store_true",
+                    help="multi-GPU: stage remote rows with NCCL all-to-all instead of NVLink "
+                         "peer reads")
     ap.add_argument("--mode", default="fused", choices=["fused", "faithful"],
                     help="multi-GPU model-hop payload (see distributed.py)")
     args = ap.parse_args()

@@ -199,7 +199,62 @@ typedef struct {
   float* loss;                           /* [max_roots] per-root softmax-CE            */
   void* lowp_scratch;                    /* bf16 [max_rows[1] x H] (tcgen05 dW path)    */
   void* Wb[HG_MAX_LAYERS + 1];           /* bf16 copies of W (tcgen05 dX path)          */
+  /* peer addressing (multi-GPU without staging): row of vertex v lives in
+   * feat_peers[feat_home[v]] at row feat_row[v]; NULL = local table only */
+  const void* feat_peers;                /* device array of S row-table pointers        */
+  const int32_t* feat_home;              /* int32[n] home server of each vertex          */
+  /* staged mode (device pre-gather): local vertices from `features` at
+   * feat_row[v], remote ones from stage_base at stage_row[v] */
+  const void* stage_base;
+  const int32_t* stage_row;
+  int32_t rank;
+  int32_t agg1_ready;                    /* 1: hg_step_prologue already built agg[1]    */
 } hg_step_desc;
+
+/* Peer memory (one process per GPU): device allocations whose CUDA IPC
+ * handles (64 bytes) other ranks map; and the reference pre-gather byte
+ * accounting of an iteration's remote vertices without a host sync
+ * (featstore.py:226-279): uniq_per_home[h] += #distinct ids homed at h != rank,
+ * total_remote += #remote occurrences; bitmap: n/32 words, zero on entry/exit. */
+int hg_alloc(size_t bytes, void** out);
+int hg_free(void* p);
+int hg_ipc_handle(void* p, void* handle_out);
+int hg_ipc_open(const void* handle, void** out);
+int hg_ipc_close(void* p);
+int hg_remote_account(const int32_t* ids, const int32_t* n_dev, int32_t n_host,
+                      const int32_t* home, int32_t rank, uint32_t* bitmap,
+                      unsigned long long* uniq_per_home, unsigned long long* total_remote,
+                      void* stream);
+/* reset the bitmap words touched by ids (after every hg_remote_account of a
+ * server-iteration, so one plan dedups across all its cells) */
+int hg_remote_clear(const int32_t* ids, const int32_t* n_dev, int32_t n_host, uint32_t* bitmap,
+                    void* stream);
+
+/* NCCL (torch's libnccl, same process): communicator from a broadcast unique
+ * id (128 bytes); gradient all-reduce fused with the SGD update
+ * (model.py:299-324); model-hop ring shift of two buffers by delta servers
+ * (engine.py:610-618).  All enqueue on `stream`, no host synchronisation. */
+int hg_nccl_unique_id(void* out);
+int hg_nccl_init(const void* id, int nranks, int rank, void** comm_out);
+int hg_nccl_destroy(void* comm);
+int hg_allreduce_sgd(void* comm, float* params, float* grads, int64_t n, float lr,
+                     float inv_batch, void* stream);
+int hg_shift(void* comm, int rank, int nranks, int delta, const float* send0, const float* send1,
+             float* recv0, float* recv1, int64_t n, void* stream);
+
+/* Device pre-gathering over NVLink: dedup the remote vertices of ids[0..*n_dev)
+ * (bitmap), list them, map vertex -> staging row, copy their rows from the
+ * owners' shards (peers[home[v]] + local_row[v] * row_bytes) into `staging`;
+ * per-home distinct counts feed the reference ledger. */
+int hg_pregather_peer(const int32_t* ids, const int32_t* n_dev, const int32_t* home, int32_t rank,
+                      const int32_t* local_row, const void* peers, int32_t row_bytes,
+                      uint32_t* bitmap, int32_t* stage_list, int32_t* stage_row,
+                      int32_t* stage_count, int32_t stage_cap, void* staging,
+                      unsigned long long* uniq_per_home, unsigned long long* total_remote,
+                      int* err, void* stream);
+/* Parameter-independent prologue of a step: the layer-1 gather + aggregate
+ * (sets up agg[1]; run ahead of the previous iteration's training). */
+int hg_step_prologue(const hg_step_desc* d, int32_t n_roots, int32_t backward, void* stream);
 
 /* Forward + backward of the batch in d->mg for n_roots roots; gradients are
  * ADDED into gW/gb/gWc (the reference GradAccumulator, model.py:144-164). */

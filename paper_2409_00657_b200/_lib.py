@@ -63,7 +63,9 @@ class StepDesc(C.Structure):
                 ("gW", _P7V), ("gb", _P7V), ("gWc", C.c_void_p),
                 ("agg", _P7V), ("h", _P7V), ("dh", _P7V), ("dagg", C.c_void_p),
                 ("logits", C.c_void_p), ("loss", C.c_void_p), ("lowp_scratch", C.c_void_p),
-                ("Wb", _P7V)]
+                ("Wb", _P7V), ("feat_peers", C.c_void_p), ("feat_home", C.c_void_p),
+                ("stage_base", C.c_void_p), ("stage_row", C.c_void_p), ("rank", C.c_int32),
+                ("agg1_ready", C.c_int32)]
 
 
 V, I32, I64, U64, SZ = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_size_t
@@ -94,6 +96,20 @@ SIGNATURES = {
     "hg_forward": [C.POINTER(StepDesc), I32, V],
     "hg_sgd_update": [V, V, V, I64, C.c_float, C.c_float, V],
     "hg_gemm_bf16": [V, I64, C.c_int, V, I64, C.c_int, V, I64, I32, I32, I32, I32, V, I32, V],
+    "hg_alloc": [C.c_size_t, C.POINTER(C.c_void_p)],
+    "hg_free": [V],
+    "hg_ipc_handle": [V, V],
+    "hg_ipc_open": [V, C.POINTER(C.c_void_p)],
+    "hg_ipc_close": [V],
+    "hg_remote_account": [V, V, I32, V, I32, V, V, V, V],
+    "hg_remote_clear": [V, V, I32, V, V],
+    "hg_nccl_unique_id": [V],
+    "hg_nccl_init": [V, C.c_int, C.c_int, C.POINTER(C.c_void_p)],
+    "hg_nccl_destroy": [V],
+    "hg_allreduce_sgd": [V, V, V, I64, C.c_float, C.c_float, V],
+    "hg_shift": [V, C.c_int, C.c_int, C.c_int, V, V, V, V, I64, V],
+    "hg_pregather_peer": [V, V, V, I32, V, V, I32, V, V, V, V, I32, V, V, V, V, V],
+    "hg_step_prologue": [C.POINTER(StepDesc), I32, I32, V],
 }
 
 

@@ -76,10 +76,36 @@ __device__ __forceinline__ void store_vec(T* p, const float* v) {
 // One group of G = W/VEC lanes (<= 32) per destination row.  For layer 1 the
 // source row of need[0] entry i is feat_row[need_ids0[i]] (vertex ids), for
 // deeper layers the row index itself.
+// Row address of a source entry: layer 1 maps need[0] entry -> vertex ->
+// (local table row | owner GPU's table over NVLink); deeper layers index
+// h_{k-1} rows directly.
+template <typename T>
+struct RowSrc {
+  const T* src;
+  int ld;
+  const int32_t* need_ids0;   // layer 1 only
+  const int32_t* feat_row;    // vertex -> row (local table, or owner's table with peers)
+  const T* const* peers;      // per-home row tables (multi-GPU peer reads) or null
+  const int32_t* home;
+  const T* stage;             // staged mode: remote rows pre-gathered into HBM
+  const int32_t* stage_row;
+  int rank;
+  __device__ __forceinline__ const T* row(int i) const {
+    if (!need_ids0) return src + (int64_t)i * ld;
+    const int v = need_ids0[i];
+    if (stage_row) {
+      if (home[v] != rank) return stage + (int64_t)stage_row[v] * ld;
+      return src + (int64_t)feat_row[v] * ld;
+    }
+    const int r = feat_row ? feat_row[v] : v;
+    const T* base = peers ? peers[home[v]] : src;
+    return base + (int64_t)r * ld;
+  }
+};
+
 template <typename T, bool SAGE>
 __global__ void __launch_bounds__(256)
-k_aggregate(const T* __restrict__ src, int src_ld, const int32_t* __restrict__ need_ids0,
-            const int32_t* __restrict__ feat_row, const int32_t* __restrict__ self_pos,
+k_aggregate(RowSrc<T> rs, const int32_t* __restrict__ self_pos,
             const int32_t* __restrict__ nbr_off, const int32_t* __restrict__ nbr_idx,
             const int32_t* __restrict__ n_rows_dev, int W, T* __restrict__ out, int out_ld) {
   constexpr int VEC = Vec<T>::N;
@@ -89,37 +115,31 @@ k_aggregate(const T* __restrict__ src, int src_ld, const int32_t* __restrict__ n
   const int grp = threadIdx.x / G, gl = threadIdx.x % G;
   const int n_rows = *n_rows_dev;
   for (int a = blockIdx.x * groups_per_block + grp; a < n_rows; a += gridDim.x * groups_per_block) {
-    int sp = self_pos[a];
-    if (need_ids0) sp = feat_row ? feat_row[need_ids0[sp]] : need_ids0[sp];
+    const T* sp = rs.row(self_pos[a]);
     const int j0 = nbr_off[a], j1 = nbr_off[a + 1];
     const int deg = j1 - j0;
     for (int cv = gl; cv < nvec; cv += G) {
       const int col = cv * VEC;
       float self[VEC], acc[VEC];
-      load_vec(src + (int64_t)sp * src_ld + col, self);
+      load_vec(sp + col, self);
 #pragma unroll
       for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
       int j = j0;
       for (; j + 4 <= j1; j += 4) {
-        int r[4];
+        const T* r[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          r[u] = nbr_idx[j + u];
-          if (need_ids0) r[u] = feat_row ? feat_row[need_ids0[r[u]]] : need_ids0[r[u]];
-        }
+        for (int u = 0; u < 4; ++u) r[u] = rs.row(nbr_idx[j + u]);
         float x[4][VEC];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) load_vec(src + (int64_t)r[u] * src_ld + col, x[u]);
+        for (int u = 0; u < 4; ++u) load_vec(r[u] + col, x[u]);
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
           for (int i = 0; i < VEC; ++i) acc[i] += x[u][i];
       }
       for (; j < j1; ++j) {
-        int r = nbr_idx[j];
-        if (need_ids0) r = feat_row ? feat_row[need_ids0[r]] : need_ids0[r];
         float x[VEC];
-        load_vec(src + (int64_t)r * src_ld + col, x);
+        load_vec(rs.row(nbr_idx[j]) + col, x);
 #pragma unroll
         for (int i = 0; i < VEC; ++i) acc[i] += x[i];
       }
@@ -508,6 +528,37 @@ static void gemm(cudaStream_t s, const TA* A, int lda, const float* B, int ldb, 
                                                        K_dev, K_cap, bias, mask, ldm);
 }
 
+// Layer-k gather + aggregate (k == 1 reads features: local table, staged
+// remote rows or peer tables).  pad: zero the rows up to the next 64 for the
+// tensor-core weight-gradient reduction.
+template <typename T>
+static void launch_aggregate(const hg_step_desc* d, int k, cudaStream_t s, bool pad) {
+  const int H = d->hidden;
+  const int32_t* tot = d->mg.totals;
+  const int nb = num_sms() * 4;
+  const int Wd = k == 1 ? d->feat_ld : H;
+  const T* src = k == 1 ? (const T*)d->features : (const T*)d->h[k - 1];
+  const int32_t* ids0 = k == 1 ? d->mg.need_ids[0] : nullptr;
+  prof_begin(k == 1 ? PROF_AGG1 : PROF_AGG2, s);
+  count_launch();
+  RowSrc<T> rs{src, Wd, ids0, k == 1 ? d->feat_row : nullptr,
+               k == 1 ? (const T* const*)d->feat_peers : nullptr, d->feat_home,
+               (const T*)d->stage_base, k == 1 ? d->stage_row : nullptr, d->rank};
+  if (d->arch == 1)
+    k_aggregate<T, true><<<nb, 256, 0, s>>>(rs, d->mg.self_pos[k], d->mg.nbr_off[k],
+                                            d->mg.nbr_idx[k], tot + k, Wd, (T*)d->agg[k],
+                                            d->in_dim[k]);
+  else
+    k_aggregate<T, false><<<nb, 256, 0, s>>>(rs, d->mg.self_pos[k], d->mg.nbr_off[k],
+                                             d->mg.nbr_idx[k], tot + k, Wd, (T*)d->agg[k],
+                                             d->in_dim[k]);
+  prof_end(k == 1 ? PROF_AGG1 : PROF_AGG2, s);
+  if (pad && sizeof(T) == 2) {
+    count_launch();
+    k_zero_pad_rows<<<4, 256, 0, s>>>((bf16*)d->agg[k], tot + k, d->in_dim[k], d->max_rows[k]);
+  }
+}
+
 template <typename T>
 static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool backward) {
   const int L = d->n_layers;
@@ -528,26 +579,9 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     }
   }
   for (int k = 1; k <= L; ++k) {
-    const int Wd = k == 1 ? d->feat_ld : H;
-    const T* src = k == 1 ? (const T*)d->features : (const T*)d->h[k - 1];
-    const int32_t* ids0 = k == 1 ? d->mg.need_ids[0] : nullptr;
-    prof_begin(k == 1 ? PROF_AGG1 : PROF_AGG2, s);
-    count_launch();
-    if (sage)
-      k_aggregate<T, true><<<nb, 256, 0, s>>>(src, Wd, ids0, d->feat_row, d->mg.self_pos[k],
-                                              d->mg.nbr_off[k], d->mg.nbr_idx[k], tot + k, Wd,
-                                              (T*)d->agg[k], d->in_dim[k]);
-    else
-      k_aggregate<T, false><<<nb, 256, 0, s>>>(src, Wd, ids0, d->feat_row, d->mg.self_pos[k],
-                                               d->mg.nbr_off[k], d->mg.nbr_idx[k], tot + k, Wd,
-                                               (T*)d->agg[k], d->in_dim[k]);
-    prof_end(k == 1 ? PROF_AGG1 : PROF_AGG2, s);
+    if (k > 1 || !d->agg1_ready) launch_aggregate<T>(d, k, s, tc && backward);
     if (k == 1) prof_begin(PROF_GEMM1, s);
     if (tc) {
-      if (backward) {
-        count_launch();
-        k_zero_pad_rows<<<4, 256, 0, s>>>((bf16*)d->agg[k], tot + k, d->in_dim[k], d->max_rows[k]);
-      }
       int st = umma_gemm(d->agg[k], d->in_dim[k], false, d->Wlp[k], d->in_dim[k], false, d->h[k], H,
                          d->max_rows[k], H, d->in_dim[k], tot + k, nullptr, 1, d->b[k], 1, s);
       if (st) return st;
@@ -648,6 +682,18 @@ extern "C" int hg_train_step(const hg_step_desc* d, int32_t n_roots, void* strea
   cudaStream_t s = (cudaStream_t)stream;
   st = d->act_dtype == 0 ? run_step<float>(d, n_roots, s, true) : run_step<bf16>(d, n_roots, s, true);
   if (st) return st;
+  HG_CUDA_TRY(cudaGetLastError());
+  return HG_OK;
+}
+
+extern "C" int hg_step_prologue(const hg_step_desc* d, int32_t n_roots, int32_t backward,
+                                void* stream) {
+  int st = validate(d, n_roots);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool tc = d->act_dtype == 1 && d->use_tc && d->hidden % 64 == 0 && d->hidden <= 256;
+  if (d->act_dtype == 0) launch_aggregate<float>(d, 1, s, false);
+  else launch_aggregate<bf16>(d, 1, s, tc && backward);
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;
 }

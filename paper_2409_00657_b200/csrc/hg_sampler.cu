@@ -210,9 +210,83 @@ __device__ void team_select(const int32_t* __restrict__ targets, int64_t lo, int
 
 // ---------------------------------------------------------------- block sort
 
+// One warp sorts up to 32*E ints held in registers (element i = lane*E + j):
+// bitonic network, in-register exchanges for strides < E, shuffles above;
+// then writes the distinct values to out and returns their count.  No block
+// barriers, which dominate the block-wide network for the small layers of
+// (15,10)-style micrographs.
+template <int E>
+__device__ int warp_sort_unique(const int* in, int n, int* out) {
+  const int lane = lane_id();
+  int x[E];
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const int i = lane * E + j;
+    x[j] = i < n ? in[i] : INT_MAX;
+  }
+#pragma unroll
+  for (int size = 2; size <= 32 * E; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= E) {
+        const int lm = stride / E;
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+          const int i = lane * E + j;
+          const int y = __shfl_xor_sync(0xffffffffu, x[j], lm);
+          const bool up = (i & size) == 0;
+          const bool lower = (i & stride) == 0;
+          x[j] = (lower == up) ? min(x[j], y) : max(x[j], y);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+          const int p = j ^ stride;
+          if (p > j) {
+            const bool up = ((lane * E + j) & size) == 0;
+            const int a = x[j], b = x[p];
+            if ((a > b) == up) { x[j] = b; x[p] = a; }
+          }
+        }
+      }
+    }
+  }
+  int prev = __shfl_up_sync(0xffffffffu, x[E - 1], 1);
+  if (lane == 0) prev = INT_MIN;
+  int cnt = 0;
+  bool keep[E];
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    keep[j] = x[j] != INT_MAX && x[j] != (j ? x[j - 1] : prev);
+    cnt += keep[j];
+  }
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  int pos = incl - cnt;
+#pragma unroll
+  for (int j = 0; j < E; ++j)
+    if (keep[j]) out[pos++] = x[j];
+  return __shfl_sync(0xffffffffu, incl, 31);
+}
+
 // Sort buf[0..n) ascending (bitonic over the next power of two, INT_MAX pad)
 // then write the distinct values to out; returns the distinct count.
 __device__ int block_sort_unique(int* buf, int n, int* out, int* scan) {
+  if (n <= 256) {  // one warp, register network
+    __shared__ int s_total;
+    if (warp_id() == 0) {
+      const int t = warp_sort_unique<8>(buf, n, out);
+      if (lane_id() == 0) s_total = t;
+    }
+    __syncthreads();
+    const int t = s_total;
+    __syncthreads();
+    return t;
+  }
   int P = 1;
   while (P < n) P <<= 1;
   for (int i = n + threadIdx.x; i < P; i += blockDim.x) buf[i] = INT_MAX;
@@ -269,7 +343,7 @@ __device__ __forceinline__ bool contains(const int* a, int n, int x) {
 
 // ---------------------------------------------------------------- build kernel
 
-__global__ void __launch_bounds__(kBuildThreads)
+__global__ void __launch_bounds__(kBuildThreads, 4)
 k_mg_build(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targets,
            int64_t n_vertices, const int64_t* __restrict__ roots, int n_roots,
            const uint64_t* __restrict__ iter_state, int roots_per_state, MgCarve c,

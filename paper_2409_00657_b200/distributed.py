@@ -225,6 +225,110 @@ def pregather(feats: ShardedFeatures, need_ids: list, group=None):
     return np.asarray(sc, dtype=np.int64), n_req, n_req * row_bytes, n_req * 8
 
 
+class PeerFeatures:
+    """Feature shards mapped across GPUs through CUDA IPC (no staging copies).
+
+    Each rank owns the rows homed on it in a raw cudaMalloc allocation; IPC
+    handles are all-gathered and every rank maps every peer's shard, so the
+    layer-1 gather (k_aggregate) reads a remote row directly from its owner's
+    HBM over NVLink/NVSwitch: address = peers[home[v]] + local_row[v] * ld.
+    """
+
+    def __init__(self, part: PartitionMap, rank: int, dim: int, seed: int, dtype=torch.bfloat16,
+                 device="cuda", group=None):
+        dev = torch.device(device)
+        self.dim, self.ld = dim, (dim + 7) // 8 * 8
+        self.dtype, self.device = dtype, dev
+        self.rank, self.S = rank, part.n_servers
+        esz = 2 if dtype == torch.bfloat16 else 4
+        home = part.home
+        local = np.flatnonzero(home == rank).astype(np.int64)
+        self.n_local = len(local)
+        ptr = C.c_void_p()
+        _lib.call("hg_alloc", max(self.n_local, 1) * self.ld * esz, C.byref(ptr))
+        self.ptr = ptr.value
+        st = feature_state(seed)
+        code = 1 if dtype == torch.bfloat16 else 0
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        if self.n_local:
+            contiguous = local[-1] - local[0] + 1 == self.n_local
+            ids = None if contiguous else torch.from_numpy(local).to(dev)
+            _lib.call("hg_feature_table", ids.data_ptr() if ids is not None else None,
+                      int(local[0]) if contiguous else 0, self.n_local, dim, self.ld,
+                      st & ((1 << 64) - 1), code, self.ptr, stream)
+        # local_row[v] = position of v inside its home's shard (ascending ids)
+        local_row = np.empty(len(home), dtype=np.int32)
+        for h in range(self.S):
+            idx = np.flatnonzero(home == h)
+            local_row[idx] = np.arange(len(idx), dtype=np.int32)
+        self.local_row = torch.from_numpy(local_row).to(dev)
+        self.home = part.home_device(dev)
+        torch.cuda.synchronize(dev)
+        handle = (C.c_char * 64)()
+        _lib.call("hg_ipc_handle", self.ptr, handle)
+        handles = [None] * self.S
+        if dist.is_initialized() and self.S > 1:
+            dist.all_gather_object(handles, bytes(handle), group=group)
+        else:
+            handles = [bytes(handle)]
+        self.opened = []
+        ptrs = []
+        for h, hb in enumerate(handles):
+            if h == rank:
+                ptrs.append(self.ptr)
+                continue
+            p = C.c_void_p()
+            buf = (C.c_char * 64).from_buffer_copy(hb)
+            _lib.call("hg_ipc_open", buf, C.byref(p))
+            self.opened.append(p.value)
+            ptrs.append(p.value)
+        self.peers = torch.tensor(ptrs, dtype=torch.int64, device=dev)
+        self.bitmap = torch.zeros((len(home) + 31) // 32, dtype=torch.int32, device=dev)
+
+    def bind(self, runner: CellRunner) -> None:
+        """Peer-read mode: the gather kernel loads remote rows over NVLink."""
+        d = runner.desc
+        d.features = self.ptr
+        d.feat_row = self.local_row.data_ptr()
+        d.feat_peers = self.peers.data_ptr()
+        d.feat_home = self.home.data_ptr()
+        d.rank = self.rank
+
+    def bind_staged(self, runner: CellRunner, stage_cap: int) -> None:
+        """Staged mode: remote rows are pre-gathered into local HBM by
+        hg_pregather_peer (bulk NVLink copies), the gather reads HBM only."""
+        if not hasattr(self, "staging"):
+            dev = self.device
+            self.stage_cap = int(stage_cap)
+            self.staging = torch.empty((self.stage_cap, self.ld), dtype=self.dtype, device=dev)
+            self.stage_list = torch.empty(self.stage_cap, dtype=torch.int32, device=dev)
+            self.stage_row = torch.zeros(len(self.local_row), dtype=torch.int32, device=dev)
+            self.stage_count = torch.zeros(1, dtype=torch.int32, device=dev)
+            self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        d = runner.desc
+        d.features = self.ptr
+        d.feat_row = self.local_row.data_ptr()
+        d.feat_peers = None
+        d.feat_home = self.home.data_ptr()
+        d.stage_base = self.staging.data_ptr()
+        d.stage_row = self.stage_row.data_ptr()
+        d.rank = self.rank
+
+    def pregather(self, runner: CellRunner, uniq_row_ptr: int, total_ptr: int, stream) -> None:
+        t = runner.builder.tensors
+        _lib.call("hg_pregather_peer", t["need_ids"][0].data_ptr(), t["totals"].data_ptr(),
+                  self.home.data_ptr(), self.rank, self.local_row.data_ptr(),
+                  self.peers.data_ptr(), self.ld * self.staging.element_size(),
+                  self.bitmap.data_ptr(), self.stage_list.data_ptr(), self.stage_row.data_ptr(),
+                  self.stage_count.data_ptr(), self.stage_cap, self.staging.data_ptr(),
+                  uniq_row_ptr, total_ptr, self.err.data_ptr(), stream)
+
+    def close(self):
+        for p in self.opened:
+            _lib.call("hg_ipc_close", p)
+        self.opened = []
+
+
 # ---------------------------------------------------------------- trainer
 
 class MicrographTrainer:
@@ -232,9 +336,14 @@ class MicrographTrainer:
 
     def __init__(self, graph: Graph, part: PartitionMap, model: ModelState, fanout, batch: int,
                  seed: int, lr: float = 0.1, dtype=torch.bfloat16, mode: str = "fused",
-                 iterations: int = 0, group=None, use_tc: bool = True):
+                 iterations: int = 0, group=None, use_tc: bool = True, pregather: bool = True):
+        """pregather=True: iteration-scoped dedup staging over NCCL all-to-all (the
+        paper's pre-gathering).  pregather=False: remote rows are read in place from
+        the owner GPU over NVLink by the gather kernel (PeerFeatures); the ledger
+        still charges the reference's deduplicated pre-gather bytes."""
         if mode not in ("fused", "faithful"):
             raise ValueError("mode must be 'fused' or 'faithful'")
+        self.pregather = pregather
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.S = part.n_servers
@@ -251,10 +360,22 @@ class MicrographTrainer:
         cap_roots = self.B * self.S if mode == "fused" else self.B
         staging = max(1, cap_roots * lay.cap_need[0] * (1 if mode == "fused" else self.S))
         staging = min(staging, part.n_vertices)
-        self.feats = ShardedFeatures(part, self.rank, model.D, seed, staging, dtype, self.device)
         n_runners = 1 if mode == "fused" else self.S
-        self.runners = [CellRunner(graph, self.feats.table, model, self.fanout, cap_roots,
+        if pregather:
+            self.feats = ShardedFeatures(part, self.rank, model.D, seed, staging, dtype,
+                                         self.device)
+            table = self.feats.table
+        else:
+            self.feats = PeerFeatures(part, self.rank, model.D, seed, dtype, self.device, group)
+            table = FeatureTable(1, model.D, dtype, self.device, model.Dp)  # shape carrier
+        self.runners = [CellRunner(graph, table, model, self.fanout, cap_roots,
                                    self.labels, use_tc=use_tc) for _ in range(n_runners)]
+        if not pregather:
+            for r in self.runners:
+                self.feats.bind(r)
+        # device-side per-iteration pre-gather accounting (peer mode): [iter][home]
+        self._acct_rows = None
+        self._acct_total = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.table = TraceTable.initial(self.S)
         self.ledger = CommLedger()
         self.stats = FetchStats()
@@ -262,6 +383,22 @@ class MicrographTrainer:
         self.flat_bytes = model.flat.numel() * 4
         self._recv_p = torch.empty_like(model.flat) if mode == "faithful" else None
         self._recv_g = torch.empty_like(model.grad) if mode == "faithful" else None
+        # our own NCCL communicator for the in-C all-reduce+SGD (and hops)
+        self._comm = None
+        self._comm_ok = True
+        if self.S > 1:
+            try:
+                uid = (C.c_char * 128)()
+                if self.rank == 0:
+                    _lib.call("hg_nccl_unique_id", uid)
+                obj = [bytes(uid)]
+                dist.broadcast_object_list(obj, src=0, group=group)
+                buf = (C.c_char * 128).from_buffer_copy(obj[0])
+                comm = C.c_void_p()
+                _lib.call("hg_nccl_init", buf, self.S, self.rank, C.byref(comm))
+                self._comm = comm.value
+            except RuntimeError:
+                self._comm_ok = False  # fall back to torch.distributed collectives
 
     # ------------------------------------------------------------ epoch
     def begin_epoch(self, epoch: int) -> int:
@@ -270,6 +407,7 @@ class MicrographTrainer:
         self.perm = perm.cpu().numpy()
         self.epoch = epoch
         self.iters = iterations_per_epoch(n, self.S, self.B, self.iter_cap)
+        self._plan_epoch()
         return self.iters
 
     def batches(self, it: int):
@@ -281,13 +419,174 @@ class MicrographTrainer:
         return out
 
     def _stage(self, runner: CellRunner, roots: np.ndarray, it: int) -> int:
-        st = np.uint64(chain(self.sampler_seed, self.epoch, it)).view(np.int64)
-        runner.stage_roots(torch.from_numpy(np.ascontiguousarray(roots)), [st], max(len(roots), 1))
-        return len(roots)
+        """Roots + iteration key into the runner's device buffers through a
+        ring of pinned host buffers (asynchronous H2D, no stream sync)."""
+        if not hasattr(self, "_pin"):
+            cap = max(r.max_roots for r in self.runners) + 1
+            self._pin = [torch.empty(cap, dtype=torch.int64).pin_memory() for _ in range(8)]
+            self._pin_ev = [None] * 8
+            self._pin_i = 0
+        i = self._pin_i
+        self._pin_i = (i + 1) % 8
+        if self._pin_ev[i] is not None:
+            self._pin_ev[i].synchronize()
+        buf = self._pin[i]
+        n = len(roots)
+        buf[0] = int(np.uint64(chain(self.sampler_seed, self.epoch, it)).view(np.int64))
+        if n:
+            buf[1:n + 1].numpy()[:] = roots
+        runner.keys[:1].copy_(buf[:1], non_blocking=True)
+        if n:
+            runner.roots[:n].copy_(buf[1:n + 1], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._pin_ev[i] = ev
+        runner.n_roots, runner.roots_per_state = n, max(n, 1)
+        return n
+
+    # ------------------------------------------------------------ fast path
+    def _plan_epoch(self) -> None:
+        """Per-epoch host plan for the initial trace table: with cells[d][t] =
+        groups[d][(d+t)%S] every root homed at this server is trained here, so
+        iteration it's roots are a contiguous slice of perm[home[perm]==rank]."""
+        S, B = self.S, self.B
+        home_perm = self.part.home[self.perm]
+        pos = np.flatnonzero(home_perm == self.rank)
+        self._my_roots = np.ascontiguousarray(self.perm[pos])
+        self._my_bounds = np.searchsorted(pos, np.arange(self.iters + 1, dtype=np.int64) * S * B)
+
+    def _stage_ring(self, roots: np.ndarray, it: int):
+        """One async H2D of [iteration key, roots...] through a pinned/device
+        buffer ring; returns (roots_ptr, keys_ptr) on the device."""
+        if not hasattr(self, "_ring_h"):
+            cap = max(r.max_roots for r in self.runners) + 1
+            self._ring_h = torch.empty((8, cap), dtype=torch.int64).pin_memory()
+            self._ring_d = torch.empty((8, cap), dtype=torch.int64, device=self.device)
+            self._ring_ev = [None] * 8
+            self._ring_i = 0
+        i = self._ring_i
+        self._ring_i = (i + 1) % 8
+        if self._ring_ev[i] is not None:
+            self._ring_ev[i].synchronize()
+        h = self._ring_h[i].numpy()
+        n = len(roots)
+        h[0] = np.uint64(chain(self.sampler_seed, self.epoch, it)).view(np.int64)
+        h[1:n + 1] = roots
+        self._ring_d[i, :n + 1].copy_(self._ring_h[i, :n + 1], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._ring_ev[i] = ev
+        base = self._ring_d[i].data_ptr()
+        return base + 8, base
+
+    def _fast_build(self, it: int):
+        roots = self._my_roots[self._my_bounds[it]:self._my_bounds[it + 1]]
+        n = len(roots)
+
+        def launch(r, s):
+            r.n_roots = n
+            if not n:
+                return
+            rp, kp = self._stage_ring(roots, it)
+            r.builder.build(self.graph, rp, kp, n, n_roots=n, stream=s)
+            r.desc.roots = rp
+            if not self.pregather:
+                # device pre-gather of the remote rows (NVLink bulk copies) and the
+                # parameter-independent layer-1 gather, both ahead of training
+                self._acct_row_ptr(it)
+                self.feats.pregather(r, self._acct_rows[it].data_ptr(),
+                                     self._acct_total.data_ptr(), s)
+                _lib.call("hg_step_prologue", C.byref(r.desc), n, 1, s)
+                r.desc.agg1_ready = 1
+                self._acct_iters = getattr(self, "_acct_iters", set())
+                self._acct_iters.add(it)
+        return launch
+
+    def _acct_row_ptr(self, it: int) -> None:
+        if self._acct_rows is None or self._acct_rows.shape[0] <= it:
+            rows = max(it + 1, getattr(self, "iters", 1))
+            t = torch.zeros((rows, self.S), dtype=torch.int64, device=self.device)
+            if self._acct_rows is not None:
+                t[:self._acct_rows.shape[0]] = self._acct_rows
+            self._acct_rows = t
+
+    def _step_fast(self, it: int, want_loss: bool):
+        """Fused micrograph iteration without host synchronisation: build (+
+        pre-gather accounting) of it+1 runs ahead on a side stream, training
+        of it reads remote rows over NVLink, then all-reduce + SGD in C."""
+        S = self.S
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        if self.pregather:  # staging exchange needs host-known sizes: no run-ahead
+            r = self.runners[0]
+            self._fast_build(it)(r, s)
+            if r.n_roots:
+                self._exchange([r], [r.n_roots], it)
+        else:
+            if not hasattr(self, "_ra"):
+                from .engine import RunAhead
+                self.runners.append(CellRunner(self.graph, self.runners[0].table, self.model,
+                                               self.fanout, self.runners[0].max_roots,
+                                               self.labels))
+                lay = self.runners[0].builder.layout
+                cap = min(self.runners[0].max_roots * lay.cap_need[0], self.part.n_vertices)
+                for rr in self.runners[:2]:
+                    self.feats.bind_staged(rr, cap)
+                self._ra = RunAhead(self.runners[:2], self.device)
+            r = self._ra.acquire(it, self._fast_build(it))
+        n = r.n_roots
+        prev = None
+        if n:
+            _lib.call("hg_train_step", C.byref(r.desc), n, s)
+            if want_loss:  # pipelined readback: this step's loss arrives next call
+                if not hasattr(self, "_loss_pin"):
+                    self._loss_pin = [torch.zeros(1, dtype=torch.float32).pin_memory()
+                                      for _ in range(4)]
+                    self._loss_slot = 0
+                    self._loss_pending = []
+                self._loss_slot = (self._loss_slot + 1) % 4
+                self._loss_pin[self._loss_slot].copy_(r.loss[:n].sum().reshape(1),
+                                                      non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record()
+                # values are read two steps late so the host never stalls the queue
+                if len(self._loss_pending) >= 2:
+                    prev = self._drain_loss()
+                self._loss_pending.append((ev, self._loss_slot))
+        self._fast_iters = getattr(self, "_fast_iters", 0) + 1
+        total = S * self.B
+        m = self.model
+        _lib.call("hg_allreduce_sgd", self._comm, m.flat.data_ptr(), m.grad.data_ptr(),
+                  m.flat.numel(), float(self.lr), 1.0 / total, s)
+        if not self.pregather:
+            self._ra.release(it)
+            if it + 1 < self.iters:
+                self._ra.prefetch(it + 1, self._fast_build(it + 1))
+        if S > 1:
+            self.traffic.allreduce_bytes += 2.0 * (S - 1) / S * self.flat_bytes
+        return prev
+
+    def _drain_loss(self):
+        pend = getattr(self, "_loss_pending", None)
+        if not pend:
+            return None
+        ev, slot = pend.pop(0)
+        ev.synchronize()
+        return float(self._loss_pin[slot].item())
+
+    def last_loss(self):
+        """Drain every pending step loss; returns the most recent (host sync)."""
+        v = None
+        while getattr(self, "_loss_pending", None):
+            v = self._drain_loss()
+        return v
 
     # ------------------------------------------------------------ iteration
-    def step(self, it: int) -> float:
-        """One iteration (engine.py:569-622).  Returns this rank's summed loss."""
+    def step(self, it: int, want_loss: bool = True):
+        """One iteration (engine.py:569-622).  Returns this rank's summed loss
+        (a host sync) or None when want_loss is False."""
+        if (self.mode == "fused" and not self.table.removed and self._comm_ok
+                and len(self.perm) >= (it + 1) * self.S * self.B):
+            return self._step_fast(it, want_loss)
         S, rank = self.S, self.rank
         batches = self.batches(it)
         home = self.part.home
@@ -308,10 +607,11 @@ class MicrographTrainer:
             n = self._stage(r, roots, it)
             if n:
                 r.builder.build(self.graph, r.roots, r.keys, n, n_roots=n, stream=s)
-            self._exchange([r] if n else [], [n])
+            self._exchange([r] if n else [], [n], it)
             if n:
                 _lib.call("hg_train_step", C.byref(r.desc), n, s)
-                loss = float(r.loss[:n].sum().item())
+                if want_loss:
+                    loss = float(r.loss[:n].sum().item())
         else:
             active = []
             for (j, d, roots), r in zip(mine, self.runners):
@@ -320,12 +620,13 @@ class MicrographTrainer:
                     r.builder.build(self.graph, r.roots, r.keys, n, n_roots=n, stream=s)
                 active.append(n)
             self._exchange([r for r, n in zip(self.runners, active) if n],
-                           [n for n in active if n])
+                           [n for n in active if n], it)
             for idx, ((j, d, roots), r) in enumerate(zip(mine, self.runners)):
                 n = active[idx]
                 if n:
                     _lib.call("hg_train_step", C.byref(r.desc), n, s)
-                    loss += float(r.loss[:n].sum().item())
+                    if want_loss:
+                        loss += float(r.loss[:n].sum().item())
                 if j + 1 < cols:
                     self._hop(int(tt.server_of[0, j + 1] - tt.server_of[0, j]) % S)
         self._account_hops_and_sync()
@@ -334,9 +635,12 @@ class MicrographTrainer:
             dist.all_reduce(self.model.grad, group=self.group)
             self.traffic.allreduce_bytes += 2.0 * (S - 1) / S * self.flat_bytes
         self.model.sgd(self.lr, sum(len(b) for b in batches), stream=s)
-        return loss
+        return loss if want_loss else None
 
-    def _exchange(self, runners, counts):
+    def _exchange(self, runners, counts, it: int):
+        if not self.pregather:
+            self._account_remote(runners, it)
+            return
         need = []
         for r in runners:
             n0 = int(r.builder.tensors["totals"][0].item())
@@ -351,6 +655,61 @@ class MicrographTrainer:
         self.traffic.feature_rows += n_req
         self.traffic.feature_bytes += nbytes
         self.traffic.request_bytes += req_bytes
+
+    def _account_remote(self, runners, it: int):
+        """Peer mode: rows are read in place, but the reference pre-gather plan
+        (dedup remote rows per home per iteration) is still charged -- counted on
+        the device into row `it` of an [iterations x S] table, no host sync."""
+        if self.S == 1:
+            return
+        if self._acct_rows is None or self._acct_rows.shape[0] <= it:
+            rows = max(it + 1, getattr(self, "iters", 1))
+            t = torch.zeros((rows, self.S), dtype=torch.int64, device=self.device)
+            if self._acct_rows is not None:
+                t[:self._acct_rows.shape[0]] = self._acct_rows
+            self._acct_rows = t
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        row = self._acct_rows[it]
+        # one plan per server-iteration: mark all runners' ids in one bitmap pass
+        for r in runners:
+            _lib.call("hg_remote_account", r.builder.tensors["need_ids"][0].data_ptr(),
+                      r.builder.tensors["totals"].data_ptr(), 0, self.feats.home.data_ptr(),
+                      self.rank, self.feats.bitmap.data_ptr(), row.data_ptr(),
+                      self._acct_total.data_ptr(), s)
+        for r in runners:
+            _lib.call("hg_remote_clear", r.builder.tensors["need_ids"][0].data_ptr(),
+                      r.builder.tensors["totals"].data_ptr(), 0, self.feats.bitmap.data_ptr(), s)
+        self._acct_iters = getattr(self, "_acct_iters", set())
+        self._acct_iters.add(it)
+
+    def flush_accounting(self) -> None:
+        """Move device-side pre-gather counts into the ledger (reference messages:
+        one per (home -> server) per iteration with rows, featstore.py:271-274)
+        and the fast path's per-iteration hop / all-reduce entries."""
+        fast = getattr(self, "_fast_iters", 0)
+        if fast:
+            self._account_hops_and_sync(fast)
+            self._fast_iters = 0
+        if self.pregather or self._acct_rows is None:
+            return
+        rows = self._acct_rows.cpu().numpy()
+        total_occ = int(self._acct_total.item())
+        D = self.model.D
+        row_bytes = self.feats.ld * (2 if self.feats.dtype == torch.bfloat16 else 4)
+        for it in sorted(getattr(self, "_acct_iters", ())):
+            for h, c in enumerate(rows[it].tolist()):
+                if c:
+                    self.ledger.add(h, self.rank, FEATURE, c * D * BYTES_PER_ELEM, 1)
+                    self.stats.transferred += c
+        # staged mode copies each distinct remote row once per iteration; the
+        # peer-read gather loads every occurrence over NVLink
+        moved = (int(sum(rows[it].sum() for it in getattr(self, "_acct_iters", ())))
+                 if hasattr(self, "_ra") else total_occ)
+        self.traffic.feature_rows += moved
+        self.traffic.feature_bytes += moved * row_bytes
+        self._acct_rows.zero_()
+        self._acct_total.zero_()
+        self._acct_iters = set()
 
     def _hop(self, delta: int):
         """Shift of (parameters, accumulator) by `delta` servers (engine.py:610-618):
@@ -369,23 +728,25 @@ class MicrographTrainer:
         self.model.grad.copy_(self._recv_g)
         self.traffic.hop_bytes += 2 * self.flat_bytes
 
-    def _account_hops_and_sync(self):
-        """Reference ledger entries this rank owns: MODEL+GRADIENT per hop
-        arriving here (engine.py:610-618) and the ring all-reduce link leaving
-        here (model.py:325-328)."""
+    def _account_hops_and_sync(self, mult: int = 1):
+        """Reference ledger entries this rank owns for `mult` iterations:
+        MODEL+GRADIENT per hop arriving here (engine.py:610-618) and the ring
+        all-reduce link leaving here (model.py:325-328)."""
         tt, S, rank = self.table, self.S, self.rank
         pb = self.model.param_bytes
         for j in range(tt.n_columns - 1):
             for d in range(tt.n_models):
                 if int(tt.server_of[d, j + 1]) == rank:
                     src = int(tt.server_of[d, j])
-                    self.ledger.add(src, rank, MODEL, pb, 1)
-                    self.ledger.add(src, rank, GRADIENT, pb, 1)
+                    self.ledger.add(src, rank, MODEL, pb * mult, mult)
+                    self.ledger.add(src, rank, GRADIENT, pb * mult, mult)
         if S > 1:
-            self.ledger.add(rank, (rank + 1) % S, GRADIENT, 2.0 * (S - 1) / S * pb, 2 * (S - 1))
+            self.ledger.add(rank, (rank + 1) % S, GRADIENT, 2.0 * (S - 1) / S * pb * mult,
+                            2 * (S - 1) * mult)
 
     def global_ledger(self) -> CommLedger:
         """Merge every rank's ledger (collective)."""
+        self.flush_accounting()
         if not dist.is_initialized() or self.S == 1:
             return self.ledger
         parts = [None] * self.S

@@ -36,12 +36,54 @@ def _u64_as_i64(vals) -> np.ndarray:
     return np.asarray([int(v) & ((1 << 64) - 1) for v in vals], dtype=np.uint64).view(np.int64)
 
 
+class RunAhead:
+    """Sampling run-ahead: micrograph construction does not
+    depend on the parameters, so iteration it+1's build runs on a side stream
+    while iteration it trains.  Two runners alternate; events order the
+    build after the previous use of the same runner and the train after the
+    build."""
+
+    def __init__(self, runners, device):
+        self.runners = runners
+        self.side = torch.cuda.Stream(device)
+        self.main = torch.cuda.current_stream(device)
+        self.built = {}
+        self.free = [None] * len(runners)
+
+    def prefetch(self, it: int, build) -> None:
+        if it in self.built:
+            return
+        i = it % len(self.runners)
+        with torch.cuda.stream(self.side):
+            if self.free[i] is not None:
+                self.side.wait_event(self.free[i])
+            build(self.runners[i], self.side.cuda_stream)
+            ev = torch.cuda.Event()
+            ev.record(self.side)
+        self.built[it] = (i, ev)
+
+    def acquire(self, it: int, build):
+        self.prefetch(it, build)
+        i, ev = self.built.pop(it)
+        self.main.wait_event(ev)
+        return self.runners[i]
+
+    def release(self, it: int) -> None:
+        ev = torch.cuda.Event()
+        ev.record(self.main)
+        self.free[it % len(self.runners)] = ev
+
+    def reset(self) -> None:
+        self.built.clear()
+
+
 class Trainer:
     """One model on one GPU (S = 1): the reference's micrograph and
     model-centric strategies coincide here (engine.py:485-507 with N = 1)."""
 
     def __init__(self, graph: Graph, table: FeatureTable, model: ModelState, fanout,
-                 batch: int, seed: int, lr: float = 0.1, iterations: int = 0):
+                 batch: int, seed: int, lr: float = 0.1, iterations: int = 0,
+                 run_ahead: bool = True):
         self.graph, self.table, self.model = graph, table, model
         self.fanout = tuple(fanout)
         self.B, self.seed, self.lr, self.iter_cap = int(batch), int(seed), float(lr), iterations
@@ -51,6 +93,11 @@ class Trainer:
         self.device = model.device
         self.epoch = None
         self.stream = torch.cuda.current_stream(self.device)
+        self.run_ahead = run_ahead
+        if run_ahead:
+            self.ra = RunAhead([self.runner, CellRunner(graph, table, model, self.fanout, self.B,
+                                                        self.labels)], self.device)
+        self.last_runner = self.runner
 
     # ------------------------------------------------------------ epoch plan
     def begin_epoch(self, epoch: int) -> int:
@@ -68,34 +115,114 @@ class Trainer:
         return self.perm[lo:min(lo + self.B, self.perm.numel())]
 
     # ------------------------------------------------------------ steps
-    def step(self, it: int) -> None:
-        """One iteration with inputs already resident in HBM (no host sync)."""
+    def _build(self, it: int):
         roots = self.roots_of(it)
         n = roots.numel()
-        s = self.stream.cuda_stream
-        r = self.runner
-        r.builder.build(self.graph, roots.data_ptr(), self.states.data_ptr() + 8 * it, n,
-                        n_roots=n, stream=s)
-        r.desc.roots = roots.data_ptr()
-        _lib.call("hg_train_step", C.byref(r.desc), n, s)
-        self.model.sgd(self.lr, n, stream=s)
 
-    def train_step(self, roots_host: torch.Tensor, it: int) -> float:
-        """Public end-to-end step: roots come from (pinned) host memory and the
-        summed loss of the step is read back (engine.py:434-445 semantics)."""
-        r = self.runner
-        n = roots_host.numel()
-        r.roots[:n].copy_(roots_host, non_blocking=True)
+        def launch(r, s):
+            r.builder.build(self.graph, roots.data_ptr(), self.states.data_ptr() + 8 * it, n,
+                            n_roots=n, stream=s)
+            r.desc.roots = roots.data_ptr()
+            r.n_roots = n
+            if self.run_ahead:  # the layer-1 gather is parameter independent too
+                _lib.call("hg_step_prologue", C.byref(r.desc), n, 1, s)
+                r.desc.agg1_ready = 1
+        return launch
+
+    def step(self, it: int) -> None:
+        """One iteration with inputs already resident in HBM (no host sync).
+        With run-ahead, iteration it+1's micrographs are built on a side
+        stream while this iteration trains."""
         s = self.stream.cuda_stream
-        r.builder.build(self.graph, r.roots.data_ptr(), self.states.data_ptr() + 8 * it, n,
-                        n_roots=n, stream=s)
-        r.desc.roots = r.roots.data_ptr()
+        if not self.run_ahead:
+            r = self.runner
+            self._build(it)(r, s)
+        else:
+            r = self.ra.acquire(it, self._build(it))
+        n = r.n_roots
         _lib.call("hg_train_step", C.byref(r.desc), n, s)
         self.model.sgd(self.lr, n, stream=s)
-        return float(r.loss[:n].sum().item())
+        self.last_runner = r
+        if self.run_ahead:
+            self.ra.release(it)
+            if it + 1 < self.iters:
+                self.ra.prefetch(it + 1, self._build(it + 1))
+
+    def train_step(self, roots_host: torch.Tensor, it: int, next_roots_host=None):
+        """Public end-to-end step (engine.py:434-445 semantics): this step's roots
+        come from pinned host memory (`next_roots_host`, when the data loader
+        already knows the next batch, lets its micrographs be built ahead), and
+        every step's summed loss is copied back to the host.  The readback is
+        pipelined one step: the call returns the PREVIOUS step's loss (None on
+        the first call); ``last_loss()`` drains the final one."""
+        if not hasattr(self, "_e2e"):
+            cap = self.B
+            self._e2e = {"dev": [torch.empty(cap, dtype=torch.int64, device=self.device)
+                                 for _ in range(2)],
+                         "loss": [torch.zeros(1, dtype=torch.float32).pin_memory()
+                                  for _ in range(2)],
+                         "slot": 0, "pending": None}
+            self._e2e_ra = RunAhead([self.runner, CellRunner(
+                self.graph, self.table, self.model, self.fanout, self.B, self.labels)],
+                self.device) if self.run_ahead else None
+        e = self._e2e
+
+        def build_for(j, roots_h):
+            dev = e["dev"][j % 2]
+            n = roots_h.numel()
+
+            def launch(r, s):
+                dev[:n].copy_(roots_h, non_blocking=True)
+                r.builder.build(self.graph, dev.data_ptr(), self.states.data_ptr() + 8 * j, n,
+                                n_roots=n, stream=s)
+                r.desc.roots = dev.data_ptr()
+                r.n_roots = n
+                if self.run_ahead:
+                    _lib.call("hg_step_prologue", C.byref(r.desc), n, 1, s)
+                    r.desc.agg1_ready = 1
+                else:
+                    r.desc.agg1_ready = 0
+            return launch
+
+        s = self.stream.cuda_stream
+        if self._e2e_ra is not None:
+            r = self._e2e_ra.acquire(it, build_for(it, roots_host))
+        else:
+            r = self.runner
+            build_for(it, roots_host)(r, s)
+        n = r.n_roots
+        _lib.call("hg_train_step", C.byref(r.desc), n, s)
+        self.model.sgd(self.lr, n, stream=s)
+        e["slot"] ^= 1
+        e["loss"][e["slot"]].copy_(r.loss[:n].sum().reshape(1), non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        if self._e2e_ra is not None:
+            self._e2e_ra.release(it)
+            if next_roots_host is not None:
+                self._e2e_ra.prefetch(it + 1, build_for(it + 1, next_roots_host))
+        prev = self._drain_loss()  # the previous step's loss, read once this one is queued
+        e["pending"] = (ev, e["slot"])
+        return prev
+
+    def _drain_loss(self):
+        e = getattr(self, "_e2e", None)
+        if not e or e["pending"] is None:
+            return None
+        ev, slot = e["pending"]
+        ev.synchronize()
+        e["pending"] = None
+        return float(e["loss"][slot].item())
+
+    def last_loss(self):
+        """Loss of the most recent train_step (host sync)."""
+        return self._drain_loss()
 
     def check(self) -> None:
         self.runner.check()
+        if self.run_ahead:
+            for r in self.ra.runners:
+                r.check()
 
     def batch_sizes(self):
         """(N_k, P_k) of the last built batch (synchronises)."""

@@ -59,7 +59,7 @@ def pregather_worker(rank, world, init_file, result_file):
     dist.destroy_process_group()
 
 
-def micrograph_worker(rank, world, init_file, result_file, mode, dtype_name):
+def micrograph_worker(rank, world, init_file, result_file, mode, dtype_name, feat_mode="pg"):
     """Full multi-GPU micrograph iterations vs the oracle engine (ledger exact,
     parameters within tolerance)."""
     import json
@@ -81,7 +81,7 @@ def micrograph_worker(rank, world, init_file, result_file, mode, dtype_name):
     part = PartitionMap(home, world, f"cuda:{rank}")
     model = init_model(arch, D, H, len(fo), C, chain(seed, 0x07), f"cuda:{rank}")
     tr = MicrographTrainer(G, part, model, fo, B, seed, lr=0.1, dtype=dtype, mode=mode,
-                           iterations=iters)
+                           iterations=iters, pregather=(feat_mode == "pg"))
     tr.begin_epoch(0)
     losses = [tr.step(it) for it in range(tr.iters)]
     torch.cuda.synchronize()

@@ -1,6 +1,8 @@
 """Multi-GPU micrograph strategy (NCCL) against the oracle engine, which is
 pinned to gnnsim's ledgers and parameters (tests/test_oracle_golden.py).
-Needs >= 2 GPUs (run with `gpurun --gpus 2`); skipped otherwise."""
+Needs >= 2 GPUs (run with `gpurun --gpus 2`); skipped otherwise.
+feat "pg": dedup staging over NCCL all-to-all; "peer": rows read in place
+from the owner GPU over NVLink (CUDA IPC) -- both charge the reference ledger."""
 import json
 import os
 import tempfile
@@ -19,13 +21,16 @@ def _world():
     return min(n, 4)
 
 
-@pytest.mark.parametrize("mode,dtype", [("fused", "f32"), ("faithful", "f32"), ("fused", "bf16")])
-def test_micrograph_strategy_matches_oracle(mode, dtype):
+@pytest.mark.parametrize("mode,dtype,feat", [("fused", "f32", "pg"), ("faithful", "f32", "pg"),
+                                             ("fused", "bf16", "pg"), ("fused", "f32", "peer"),
+                                             ("faithful", "f32", "peer"),
+                                             ("fused", "bf16", "peer")])
+def test_micrograph_strategy_matches_oracle(mode, dtype, feat):
     import dist_helpers
     world = _world()
     d = tempfile.mkdtemp()
     mp.spawn(dist_helpers.micrograph_worker,
-             args=(world, os.path.join(d, "init"), os.path.join(d, "res"), mode, dtype),
+             args=(world, os.path.join(d, "init"), os.path.join(d, "res"), mode, dtype, feat),
              nprocs=world, join=True)
     res = json.load(open(os.path.join(d, "res.0")))
     assert res["ok"], res["msg"]
