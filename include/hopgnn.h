@@ -209,6 +209,10 @@ typedef struct {
   const int32_t* stage_row;
   int32_t rank;
   int32_t agg1_ready;                    /* 1: hg_step_prologue already built agg[1]    */
+  /* tensor-core classifier head (bf16 path): Cp = C rounded up to 64 */
+  void* WcT;                             /* bf16 [C x H]  (K-major B of the logits)    */
+  void* Wcp;                             /* bf16 [H x Cp] (K-major B of dz_L)          */
+  void* dl_lowp;                         /* bf16 [max_roots x Cp] dlogits               */
 } hg_step_desc;
 
 /* Peer memory (one process per GPU): device allocations whose CUDA IPC

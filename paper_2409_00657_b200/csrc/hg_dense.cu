@@ -254,7 +254,8 @@ k_gemm(const TA* __restrict__ A, int lda, const float* __restrict__ B, int ldb, 
 // warp per root: softmax-CE on the root logits (model.py:253-259); logits are
 // overwritten with dlogits = softmax - onehot(label).
 __global__ void k_softmax_ce(float* __restrict__ logits, int C, const int64_t* __restrict__ roots,
-                             int n_roots, uint64_t label_state, float* __restrict__ loss) {
+                             int n_roots, uint64_t label_state, float* __restrict__ loss,
+                             bf16* __restrict__ dl_lowp, int ldp) {
   const int r = blockIdx.x * (blockDim.x / 32) + warp_id();
   if (r >= n_roots) return;
   const int lane = lane_id();
@@ -271,8 +272,26 @@ __global__ void k_softmax_ce(float* __restrict__ logits, int C, const int64_t* _
   const float xl = x[label];
   __syncwarp();
   const float inv = 1.0f / s;
-  for (int c = lane; c < C; c += 32) x[c] = expf(x[c] - mx) * inv - (c == label ? 1.f : 0.f);
+  for (int c = lane; c < C; c += 32) {
+    const float g = expf(x[c] - mx) * inv - (c == label ? 1.f : 0.f);
+    x[c] = g;
+    if (dl_lowp) dl_lowp[(int64_t)r * ldp + c] = __float2bfloat16_rn(g);
+  }
+  if (dl_lowp)
+    for (int c = C + lane; c < ldp; c += 32) dl_lowp[(int64_t)r * ldp + c] = __float2bfloat16_rn(0.f);
   if (lane == 0) loss[r] = logf(s) - (xl - mx);
+}
+
+// out[r][c] = bf16(W[r][c]) for c < cols, 0 for cols <= c < ld (K-major operand
+// with a 16-byte-aligned row pitch for TMA)
+__global__ void k_pad_bf16(const float* __restrict__ W, int rows, int cols, bf16* __restrict__ out,
+                           int ld) {
+  const int64_t total = (int64_t)rows * ld;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / ld), c = (int)(i % ld);
+    out[i] = __float2bfloat16_rn(c < cols ? W[(int64_t)r * cols + c] : 0.f);
+  }
 }
 
 // Fused classifier head (model.py:246, 253-265): per root, logits = h_L @ W_c
@@ -293,7 +312,8 @@ k_head(const T* __restrict__ hL, const float* __restrict__ Wc, int H, int C,
   float* gbs = ws + (size_t)H * pitch;              // [H]
   float* rowbuf = gbs + H;                          // [8][H]
   float* dlbuf = rowbuf + 8 * H;                    // [8][C]
-  for (int i = threadIdx.x; i < H * C; i += blockDim.x) ws[(i / C) * pitch + i % C] = Wc[i];
+  for (int h = warp_id(); h < H; h += blockDim.x / 32)
+    for (int c = lane_id(); c < C; c += 32) ws[h * pitch + c] = Wc[(int64_t)h * C + c];
   for (int i = threadIdx.x; i < H; i += blockDim.x) gbs[i] = 0.f;
   __syncthreads();
   const int w = warp_id(), lane = lane_id();
@@ -592,8 +612,41 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     }
     if (k == 1) prof_end(PROF_GEMM1, s);
   }
-  // classifier head: logits, softmax-CE, dlogits, dz_L, gb_L (one fused kernel)
-  {
+  // classifier head (model.py:246, 253-265)
+  const bool tc_head = tc && C <= 256 && d->WcT && d->Wcp && d->dl_lowp;
+  const int Cp = (C + 63) / 64 * 64;
+  if (tc_head) {
+    // logits = h_L @ W_c on tcgen05 (B = W_cᵀ bf16, K-major); softmax-CE writes
+    // dlogits (f32 in place + bf16 padded copy for the backward GEMMs)
+    {
+      dim3 g((C + 31) / 32, (H + 31) / 32), b(32, 8);
+      count_launch(2);
+      k_transpose_bf16<<<g, b, 0, s>>>(d->Wc, H, C, (bf16*)d->WcT, nullptr);
+      k_pad_bf16<<<64, 256, 0, s>>>(d->Wc, H, C, (bf16*)d->Wcp, Cp);
+    }
+    int st = umma_gemm(d->h[L], H, false, d->WcT, H, false, d->logits, C, n_roots, C, H,
+                       nullptr, nullptr, 0, nullptr, 1, s);
+    if (st) return st;
+    count_launch();
+    k_softmax_ce<<<(n_roots + 7) / 8, 256, 0, s>>>(d->logits, C, d->roots, n_roots,
+                                                   d->label_state, d->loss,
+                                                   (bf16*)d->dl_lowp, Cp);
+    if (backward) {
+      // dz_L = (dlogits @ W_cᵀ) * (h_L > 0); gb_L; bf16 dz_L for the dW GEMM
+      st = umma_gemm(d->dl_lowp, Cp, false, d->Wcp, Cp, false, d->dh[L], H, n_roots, H, Cp,
+                     nullptr, nullptr, 0, nullptr, 1, s);
+      if (st) return st;
+      dim3 g((H + 31) / 32, 16);
+      count_launch();
+      k_mask_colsum<T><<<g, 256, 0, s>>>(d->dh[L], (const T*)d->h[L], tot + L, H, d->gb[L],
+                                         (bf16*)d->lowp_scratch, d->max_rows[L]);
+      // gW_c += h_Lᵀ dlogits (both MN-major, reduction over the roots)
+      const int split = std::max(1, std::min(16, n_roots / 256));
+      st = umma_gemm(d->h[L], H, true, d->dl_lowp, Cp, true, d->gWc, C, H, C, n_roots,
+                     nullptr, nullptr, 2, nullptr, split, s);
+      if (st) return st;
+    }
+  } else {
     const size_t smem = ((size_t)H * (C | 1) + H + 8 * H + 8 * C) * sizeof(float);
     static size_t smem_set = 0;
     if (smem > 48 * 1024 && smem > smem_set) {
@@ -611,9 +664,10 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
   // ---- backward (model.py:262-285)
   const int split_r = std::max(1, std::min(32, n_roots / 64));
   // gWc += h_L^T dlogits
-  gemm<T, true, false, EPI_ATOMIC, float, T>(s, (const T*)d->h[L], H, d->logits, C, d->gWc, C,
-                                             nullptr, H, C, nullptr, n_roots, nullptr, nullptr, 0,
-                                             split_r);
+  if (!tc_head)
+    gemm<T, true, false, EPI_ATOMIC, float, T>(s, (const T*)d->h[L], H, d->logits, C, d->gWc, C,
+                                               nullptr, H, C, nullptr, n_roots, nullptr, nullptr,
+                                               0, split_r);
   for (int k = L; k >= 1; --k) {
     // gW_k += agg_k^T dz_k   (reduction over the N_k rows, split across CTAs)
     if (k == 1) prof_begin(PROF_DW1, s);

@@ -110,6 +110,26 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Issue a 16-column TMEM load without waiting; tmem_wait16 completes it and
+// ties the registers to the wait so no use is scheduled before it.
+__device__ __forceinline__ void tmem_ld16_issue(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"
+      " [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait16(uint32_t* r) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]),
+                 "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]),
+                 "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :
+               : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"
@@ -228,10 +248,19 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   asm volatile("tcgen05.fence::after_thread_sync;");
   const int row = m0 + warp * 32 + lane;
   const bool valid = row < M;
+  constexpr int CH = BN_T % 64 == 0 ? 64 : 16;  // columns per TMEM round trip
 #pragma unroll 1
-  for (int c = 0; c < BN_T; c += 16) {
-    uint32_t r[16];
-    tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + c, r);
+  for (int cb = 0; cb < BN_T; cb += CH) {
+    uint32_t rr[CH];
+#pragma unroll
+    for (int q = 0; q < CH; q += 16)
+      tmem_ld16_issue(tmem + ((uint32_t)(warp * 32) << 16) + cb + q, rr + q);
+#pragma unroll
+    for (int q = 0; q < CH; q += 16) tmem_wait16(rr + q);
+#pragma unroll
+  for (int q = 0; q < CH; q += 16) {
+    const uint32_t* r = rr + q;
+    const int c = cb + q;
     if (!valid) continue;
     const int col = n0 + c;
     if (col >= args.N) continue;
@@ -249,19 +278,30 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       reinterpret_cast<uint4*>(out)[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
     } else if constexpr (EPI == UEPI_ATOMIC_F32) {
       float* out = reinterpret_cast<float*>(args.C) + (int64_t)row * args.ldc + col;
+      const int nv = min(16, args.N - col);  // partial last chunk (N not a multiple of 16)
+      if (nv == 16) {
 #pragma unroll
-      for (int j = 0; j < 16; j += 4)
-        atomicAdd(reinterpret_cast<float4*>(out + j),
-                  make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                              __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
+        for (int j = 0; j < 16; j += 4)
+          atomicAdd(reinterpret_cast<float4*>(out + j),
+                    make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])));
+      } else {
+        for (int j = 0; j < nv; ++j) atomicAdd(out + j, __uint_as_float(r[j]));
+      }
     } else {
       float* out = reinterpret_cast<float*>(args.C) + (int64_t)row * args.ldc + col;
+      const int nv = min(16, args.N - col);
+      if (nv == 16) {
 #pragma unroll
-      for (int j = 0; j < 16; j += 4)
-        *reinterpret_cast<float4*>(out + j) =
-            make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                        __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+        for (int j = 0; j < 16; j += 4)
+          *reinterpret_cast<float4*>(out + j) =
+              make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                          __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+      } else {
+        for (int j = 0; j < nv; ++j) out[j] = __uint_as_float(r[j]);
+      }
     }
+  }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -346,8 +386,8 @@ static int launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const UmmaArgs
 int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb, bool b_mn,
               void* C, int64_t ldc, int M, int N, int K, const int32_t* M_dev,
               const int32_t* K_dev, int epi, const float* bias, int split, cudaStream_t s) {
-  if (N % 64 || N <= 0 || (N > 256 && N % 256)) return hg_fail(HG_ECONFIG, "umma N must be a multiple of 64 (<= 256) or of 256");
-  const int bn = N > 256 ? 256 : N;  // N tile (grid.y covers the rest)
+  if (N <= 0 || (N > 256 && N % 256)) return hg_fail(HG_ECONFIG, "umma N must be <= 256 or a multiple of 256");
+  const int bn = N > 256 ? 256 : (N + 63) / 64 * 64;  // N tile (grid.y covers the rest)
   if (lda % 8 || ldb % 8) return hg_fail(HG_ECONFIG, "umma leading dims must be multiples of 8");
   CUtensorMap ma, mb;
   int st;

@@ -82,6 +82,11 @@ class CellRunner:
         self.wb16 = torch.empty(model.flat.numel(), dtype=torch.bfloat16, device=dev)
         for k in range(1, L + 1):
             d.Wb[k] = self.wb16.data_ptr() + 2 * int(model.offsets[k - 1])
+        Cp = (model.C + 63) // 64 * 64
+        self.wct = torch.empty((model.C, H), dtype=torch.bfloat16, device=dev)
+        self.wcp = torch.zeros((H, Cp), dtype=torch.bfloat16, device=dev)
+        self.dl16 = torch.zeros((max_roots, Cp), dtype=torch.bfloat16, device=dev)
+        d.WcT, d.Wcp, d.dl_lowp = self.wct.data_ptr(), self.wcp.data_ptr(), self.dl16.data_ptr()
         self.desc = d
         self.n_roots = 0
 

@@ -79,7 +79,8 @@ def forward_bf16(m, x_rows, P, tc=False):
         aggs.append(agg)
         zs.append(z)
         h.append(_bf(np.maximum(z, 0.0)))
-    return dict(need=need, steps=steps, h=h, aggs=aggs, zs=zs, logits=h[-1][0] @ P.Wc)
+    return dict(need=need, steps=steps, h=h, aggs=aggs, zs=zs,
+                logits=h[-1][0] @ (_bf(P.Wc) if tc else P.Wc))
 
 
 def grads_bf16(st, label, P, tc):
@@ -94,8 +95,10 @@ def grads_bf16(st, label, P, tc):
     dl = e / e.sum()
     dl[label] -= 1.0
     L = len(P.W)
+    # tensor-core head: bf16 dlogits and bf16 W_c operands
+    G.Wc[...] = np.outer(st["h"][L][0], _bf(dl))
     dh = np.zeros_like(st["h"][L])
-    dh[0] = P.Wc @ dl
+    dh[0] = _bf(P.Wc) @ _bf(dl)
     for k in range(L, 0, -1):
         self_pos, dpos, spos, deg = st["steps"][k - 1]
         dz = dh * (st["zs"][k - 1] > 0.0)
