@@ -422,6 +422,12 @@ def run_distributed(args, cfg):
                 "by_category_per_iter": {k: round(v / K, 1) for k, v in by_cat.items()},
                 "model_centric_reference_accounting_per_iter": round(mc_iter, 1),
                 "ratio_model_centric_over_micrograph": round(mc_iter / max(per_iter_ref, 1), 3),
+                # this implementation's default payload ("fused": parameters are
+                # replicated, so no per-column MODEL/GRADIENT hop is shipped)
+                "micrograph_fused_payload_per_iter": round(
+                    by_cat["feature"] / K + 2.0 * (S - 1) * pb, 1),
+                "ratio_model_centric_over_micrograph_fused": round(
+                    mc_iter / max(by_cat["feature"] / K + 2.0 * (S - 1) * pb, 1), 3),
                 "actual_nvlink_bytes_per_iter": round(float(traffic[0].item()) / K, 1),
                 "epoch_reference_accounting": round(per_iter_ref * iters, 1),
                 "epoch_model_centric": round(mc_iter * iters, 1),
