@@ -48,6 +48,18 @@ CONFIGS = {
                      n=2_400_000, avg_deg=27.0, beta=0.6, p_in=0.9, n_blocks=8, d_cap=1 << 14,
                      arch="sage-mean", fanout=(15, 10), dim=100, hidden=256, classes=47,
                      batch=1024, seed=0),
+    # BASELINE.json configs[2]
+    "reddit": dict(workload="cfg3: GCN-3 fanout[10,10,10] hidden256, synthetic Reddit-shaped "
+                            "graph (233K V, ~115M E, 602-d feats)",
+                   n=233_000, avg_deg=520.0, beta=0.5, p_in=0.9, n_blocks=8, d_cap=1 << 15,
+                   arch="gcn", fanout=(10, 10, 10), dim=602, hidden=256, classes=41,
+                   batch=1024, seed=0),
+    # BASELINE.json configs[4]
+    "deep": dict(workload="cfg5: GraphSAGE-4 fanout[10,10,5,5] hidden256 bf16 on the "
+                          "papers100M shape (deep-hop stress)",
+                 n=111_000_000, avg_deg=15.6, beta=0.6, p_in=0.95, n_blocks=8, d_cap=1 << 15,
+                 arch="sage-mean", fanout=(10, 10, 5, 5), dim=128, hidden=256, classes=172,
+                 batch=1024, seed=0),
     "small": dict(workload="smoke: GraphSAGE-2 fanout[10,5] on a 100K-vertex power-law graph",
                   n=100_000, avg_deg=18.5, beta=0.8, p_in=0.9, n_blocks=8, d_cap=1 << 14,
                   arch="sage-mean", fanout=(10, 5), dim=128, hidden=128, classes=16,

@@ -279,7 +279,7 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     } else if constexpr (EPI == UEPI_ATOMIC_F32) {
       float* out = reinterpret_cast<float*>(args.C) + (int64_t)row * args.ldc + col;
       const int nv = min(16, args.N - col);  // partial last chunk (N not a multiple of 16)
-      if (nv == 16) {
+      if (nv == 16 && (args.ldc & 3) == 0) {  // float4 only on 16-byte aligned rows
 #pragma unroll
         for (int j = 0; j < 16; j += 4)
           atomicAdd(reinterpret_cast<float4*>(out + j),
@@ -291,7 +291,7 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     } else {
       float* out = reinterpret_cast<float*>(args.C) + (int64_t)row * args.ldc + col;
       const int nv = min(16, args.N - col);
-      if (nv == 16) {
+      if (nv == 16 && (args.ldc & 3) == 0) {
 #pragma unroll
         for (int j = 0; j < 16; j += 4)
           *reinterpret_cast<float4*>(out + j) =
