@@ -48,6 +48,8 @@ int hg_device_sync(void* stream); /* cudaStreamSynchronize + error-flag check */
  * CUDA-event timing of kernel sites: 0 build, 1 layer-1 aggregate,
  * 2 layer-1 GEMM, 3 layer-1 dW, 4 whole step, 5 layer-2 aggregate, 6 SGD. */
 int hg_launch_count(long long* out, int reset);
+/* per-CTA clock64 phase stamps of hg_mg_build (builds with -DHG_BUILD_PROFILE only) */
+int hg_debug_build_phases(long long* out, int n);
 int hg_prof_enable(int on);
 int hg_prof_read(int site, double* total_ms, int* count);
 

@@ -111,6 +111,7 @@ SIGNATURES = {
     "hg_shift": [V, C.c_int, C.c_int, C.c_int, V, V, V, V, I64, V],
     "hg_pregather_peer": [V, V, V, I32, V, V, I32, V, V, V, V, I32, V, V, V, V, V],
     "hg_step_prologue": [C.POINTER(StepDesc), I32, I32, V],
+    "hg_debug_build_phases": [C.POINTER(C.c_longlong), C.c_int],
 }
 
 

@@ -18,7 +18,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         "-Xptxas", "-warn-spills", "-DNDEBUG"]
+         "-Xptxas", "-warn-spills", "-DNDEBUG"] + os.environ.get("HG_EXTRA_FLAGS", "").split()
 
 
 def _nccl_flags():

@@ -28,7 +28,7 @@ namespace hg {
 
 constexpr int kBuildThreads = 256;
 constexpr int kBuildWarps = kBuildThreads / 32;
-constexpr int kBigTask = 1024;
+constexpr int kBigTask = 4096;  // degree above which the whole CTA draws one vertex
 
 struct MgCarve {
   int L;
@@ -341,7 +341,66 @@ __device__ __forceinline__ bool contains(const int* a, int n, int x) {
   return p < n && a[p] == x;
 }
 
+// Sorted-unique of buf[0..n) for n <= blockDim.x by ranking: thread i keeps
+// buf[i] if no equal value precedes it, then places it at the number of
+// distinct smaller values.  Two O(n) passes, 2 barriers, no sorting network.
+// `flag` needs n ints of scratch.
+__device__ int rank_sort_unique(const int* buf, int n, int* out, int* flag, int* s_total) {
+  const int i = threadIdx.x;
+  int x = 0;
+  bool first = false;
+  if (i < n) {
+    x = buf[i];
+    first = true;
+    for (int j = 0; j < i; ++j) first &= buf[j] != x;
+    flag[i] = first;
+  }
+  if (i == 0) *s_total = 0;
+  __syncthreads();
+  if (first) {
+    int pos = 0;
+    for (int j = 0; j < n; ++j) pos += flag[j] && buf[j] < x;
+    out[pos] = x;
+    atomicAdd(s_total, 1);
+  }
+  __syncthreads();
+  const int t = *s_total;
+  __syncthreads();
+  return t;
+}
+
+// out = sorted union of two sorted-unique lists A[0..a) and B[0..b) by merge
+// positions (binary searches), B's members of A dropped; b <= blockDim.x.
+// `flag` needs b+1 ints of scratch.  Returns the union size.
+__device__ int union_sorted(const int* A, int a, const int* B, int b, int* out, int* flag,
+                            int* scan) {
+  // flag[j] = 1 if B[j] is not in A; exclusive prefix over B
+  const int i = threadIdx.x;
+  int nd = 0;
+  if (i < b) nd = contains(A, a, B[i]) ? 0 : 1;
+  int tot_b;
+  const int pre = block_exclusive_scan(nd, scan, &tot_b);  // all threads participate
+  if (i < b) flag[i] = pre;
+  if (i == 0) flag[b] = tot_b;
+  __syncthreads();
+  for (int k = i; k < a; k += blockDim.x) {
+    const int x = A[k];
+    out[k + flag[lower_bound(B, b, x)]] = x;
+  }
+  if (i < b && nd) out[pre + lower_bound(A, a, B[i])] = B[i];
+  __syncthreads();
+  return a + tot_b;
+}
+
 // ---------------------------------------------------------------- build kernel
+
+#ifdef HG_BUILD_PROFILE
+__device__ long long g_phase[4096][16];
+#define HG_PHASE(i) \
+  if (threadIdx.x == 0 && r < 4096) g_phase[r][(i)] = clock64();
+#else
+#define HG_PHASE(i)
+#endif
 
 __global__ void __launch_bounds__(kBuildThreads, 4)
 k_mg_build(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targets,
@@ -372,6 +431,7 @@ k_mg_build(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targ
     nlay[L] = 1;
   }
   __syncthreads();
+  HG_PHASE(0);
 
   for (int h = 1; h <= L; ++h) {
     const int k = L - h;
@@ -392,6 +452,7 @@ k_mg_build(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targ
     }
     __syncthreads();
     const int T = block_scan_small(cnt, off, F, scan);
+    HG_PHASE(1 + 4 * (h - 1));
     // small tasks: one warp each
     for (int i = warp_id(); i < F; i += kBuildWarps) {
       const int d = degs[i];
@@ -408,6 +469,7 @@ k_mg_build(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targ
       }
     }
     __syncthreads();
+    HG_PHASE(2 + 4 * (h - 1));
     // hubs: the whole CTA
     for (int i = 0; i < F; ++i) {
       const int d = degs[i];
@@ -418,12 +480,20 @@ k_mg_build(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targ
                              c.cand_cap, warp_ctr + kBuildWarps, tslots + kBuildWarps, err);
     }
     __syncthreads();
+    HG_PHASE(3 + 4 * (h - 1));
     int* sb = sm + c.sm_sort;
-    for (int i = threadIdx.x; i < T; i += blockDim.x) sb[i] = flat[i];
-    __syncthreads();
-    const int u = block_sort_unique(sb, T, sm + c.sm_lay[k], scan);
+    int u;
+    if (T <= (int)blockDim.x) {
+      __shared__ int s_tot;
+      u = rank_sort_unique(flat, T, sm + c.sm_lay[k], sb, &s_tot);
+    } else {
+      for (int i = threadIdx.x; i < T; i += blockDim.x) sb[i] = flat[i];
+      __syncthreads();
+      u = block_sort_unique(sb, T, sm + c.sm_lay[k], scan);
+    }
     if (threadIdx.x == 0) { nlay[k] = u; ntot[h] = T; }
     __syncthreads();
+    HG_PHASE(4 + 4 * (h - 1));
   }
 
   // need-chain sets: need[L] = [root], need[k] = union(layers[k], need[k+1])
@@ -432,14 +502,20 @@ k_mg_build(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targ
   for (int k = L - 1; k >= 0; --k) {
     int* sb = sm + c.sm_sort;
     const int a = nlay[k], b = nneed[k + 1];
-    for (int i = threadIdx.x; i < a; i += blockDim.x) sb[i] = sm[c.sm_lay[k] + i];
-    for (int i = threadIdx.x; i < b; i += blockDim.x) sb[a + i] = sm[c.sm_need[k + 1] + i];
-    __syncthreads();
-    const int u = block_sort_unique(sb, a + b, sm + c.sm_need[k], scan);
+    int u;
+    if (b < (int)blockDim.x) {  // merge of two sorted-unique lists
+      u = union_sorted(sm + c.sm_lay[k], a, sm + c.sm_need[k + 1], b, sm + c.sm_need[k], sb, scan);
+    } else {
+      for (int i = threadIdx.x; i < a; i += blockDim.x) sb[i] = sm[c.sm_lay[k] + i];
+      for (int i = threadIdx.x; i < b; i += blockDim.x) sb[a + i] = sm[c.sm_need[k + 1] + i];
+      __syncthreads();
+      u = block_sort_unique(sb, a + b, sm + c.sm_need[k], scan);
+    }
     if (threadIdx.x == 0) nneed[k] = u;
     __syncthreads();
   }
 
+  HG_PHASE(13);
   // padded per-root outputs
   int32_t* w = ws + (size_t)r * c.ws_root_ints;
   for (int k = 0; k <= L; ++k) {
@@ -472,6 +548,8 @@ k_mg_build(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targ
     for (int k = 0; k <= L; ++k) w[c.ws_cnt + k] = nneed[k];
     for (int k = 1; k <= L; ++k) w[c.ws_cnt + L + k] = ntot[L - k + 1];
   }
+  __syncthreads();
+  HG_PHASE(14);
 }
 
 // Exclusive scans of the per-root counts (one CTA).  cols 0..L: need sizes,
@@ -668,4 +746,13 @@ extern "C" int hg_sample_frontier(const int64_t* offsets, const int32_t* targets
   HG_CUDA_TRY(cudaFreeAsync(pos, s));
   HG_CUDA_TRY(cudaFreeAsync(err, s));
   return rc;
+}
+
+extern "C" int hg_debug_build_phases(long long* out, int n) {
+#ifdef HG_BUILD_PROFILE
+  HG_CUDA_TRY(cudaMemcpyFromSymbol(out, hg::g_phase, sizeof(long long) * 16 * (n < 4096 ? n : 4096)));
+  return HG_OK;
+#else
+  return hg_fail(HG_ECONFIG, "built without HG_BUILD_PROFILE");
+#endif
 }
