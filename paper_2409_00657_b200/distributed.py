@@ -336,13 +336,22 @@ class MicrographTrainer:
 
     def __init__(self, graph: Graph, part: PartitionMap, model: ModelState, fanout, batch: int,
                  seed: int, lr: float = 0.1, dtype=torch.bfloat16, mode: str = "fused",
-                 iterations: int = 0, group=None, use_tc: bool = True, pregather: bool = True):
-        """pregather=True: iteration-scoped dedup staging over NCCL all-to-all (the
+                 iterations: int = 0, group=None, use_tc: bool = True, pregather: bool = True,
+                 strategy: str = "micrograph"):
+        """strategy="micrograph": HopGNN feature-centric training (engine.py:562-623);
+        "model-centric": the baseline it is measured against (engine.py:482-507) --
+        GPU d trains all of batch d, fetching every remote row its micrographs
+        need, no hops, same all-reduce.  pregather=True: iteration-scoped dedup staging over NCCL all-to-all (the
         paper's pre-gathering).  pregather=False: remote rows are read in place from
         the owner GPU over NVLink by the gather kernel (PeerFeatures); the ledger
         still charges the reference's deduplicated pre-gather bytes."""
         if mode not in ("fused", "faithful"):
             raise ValueError("mode must be 'fused' or 'faithful'")
+        if strategy not in ("micrograph", "model-centric"):
+            raise ValueError("strategy must be 'micrograph' or 'model-centric'")
+        if strategy == "model-centric":
+            mode = "fused"  # one cell per GPU, nothing to hop
+        self.strategy = strategy
         self.pregather = pregather
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -358,6 +367,8 @@ class MicrographTrainer:
         from .sampler import plan_layout
         lay = plan_layout(self.fanout)
         cap_roots = self.B * self.S if mode == "fused" else self.B
+        if strategy == "model-centric":
+            cap_roots = self.B
         staging = max(1, cap_roots * lay.cap_need[0] * (1 if mode == "fused" else self.S))
         staging = min(staging, part.n_vertices)
         n_runners = 1 if mode == "fused" else self.S
@@ -479,8 +490,15 @@ class MicrographTrainer:
         base = self._ring_d[i].data_ptr()
         return base + 8, base
 
+    def _iter_roots(self, it: int) -> np.ndarray:
+        """Roots this GPU trains in iteration `it` under the initial table."""
+        if self.strategy == "model-centric":
+            lo = (it * self.S + self.rank) * self.B
+            return self.perm[lo:lo + self.B]
+        return self._my_roots[self._my_bounds[it]:self._my_bounds[it + 1]]
+
     def _fast_build(self, it: int):
-        roots = self._my_roots[self._my_bounds[it]:self._my_bounds[it + 1]]
+        roots = self._iter_roots(it)
         n = len(roots)
 
         def launch(r, s):
@@ -584,11 +602,13 @@ class MicrographTrainer:
     def step(self, it: int, want_loss: bool = True):
         """One iteration (engine.py:569-622).  Returns this rank's summed loss
         (a host sync) or None when want_loss is False."""
-        if (self.mode == "fused" and not self.table.removed and self._comm_ok
-                and len(self.perm) >= (it + 1) * self.S * self.B):
+        if (self.mode == "fused" and (not self.table.removed or self.strategy == "model-centric")
+                and self._comm_ok and len(self.perm) >= (it + 1) * self.S * self.B):
             return self._step_fast(it, want_loss)
         S, rank = self.S, self.rank
         batches = self.batches(it)
+        if self.strategy == "model-centric":
+            return self._step_model_centric(it, batches, want_loss)
         home = self.part.home
         groups = [tuple(b[home[b] == s] for s in range(S)) for b in batches]
         cells = assign_cell_roots(self.table, groups, chain(self.seed, SEED_MERGE, self.epoch, it))
@@ -634,6 +654,26 @@ class MicrographTrainer:
         if S > 1:
             dist.all_reduce(self.model.grad, group=self.group)
             self.traffic.allreduce_bytes += 2.0 * (S - 1) / S * self.flat_bytes
+        self.model.sgd(self.lr, sum(len(b) for b in batches), stream=s)
+        return loss if want_loss else None
+
+    def _step_model_centric(self, it: int, batches, want_loss: bool):
+        """Slow-path model-centric iteration (ragged last batch / no own comm)."""
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        r = self.runners[0]
+        n = self._stage(r, batches[self.rank], it)
+        if n:
+            r.builder.build(self.graph, r.roots, r.keys, n, n_roots=n, stream=s)
+        self._exchange([r] if n else [], [n], it)
+        loss = 0.0
+        if n:
+            _lib.call("hg_train_step", C.byref(r.desc), n, s)
+            if want_loss:
+                loss = float(r.loss[:n].sum().item())
+        self._account_hops_and_sync()
+        if self.S > 1:
+            dist.all_reduce(self.model.grad, group=self.group)
+            self.traffic.allreduce_bytes += 2.0 * (self.S - 1) / self.S * self.flat_bytes
         self.model.sgd(self.lr, sum(len(b) for b in batches), stream=s)
         return loss if want_loss else None
 
@@ -734,7 +774,8 @@ class MicrographTrainer:
         all-reduce link leaving here (model.py:325-328)."""
         tt, S, rank = self.table, self.S, self.rank
         pb = self.model.param_bytes
-        for j in range(tt.n_columns - 1):
+        hops = 0 if self.strategy == "model-centric" else tt.n_columns - 1
+        for j in range(hops):
             for d in range(tt.n_models):
                 if int(tt.server_of[d, j + 1]) == rank:
                     src = int(tt.server_of[d, j])
@@ -743,6 +784,11 @@ class MicrographTrainer:
         if S > 1:
             self.ledger.add(rank, (rank + 1) % S, GRADIENT, 2.0 * (S - 1) / S * pb * mult,
                             2 * (S - 1) * mult)
+
+    def close(self) -> None:
+        """Release peer mappings (CUDA IPC) held by this trainer."""
+        if hasattr(self.feats, "close"):
+            self.feats.close()
 
     def global_ledger(self) -> CommLedger:
         """Merge every rank's ledger (collective)."""
@@ -775,3 +821,105 @@ def model_centric_feature_rows(trainer: MicrographTrainer, it: int):
     counts = torch.bincount(h, minlength=S).cpu().numpy()
     counts[rank] = 0
     return counts
+
+
+# ---------------------------------------------------------------- merging controller
+
+@dataclass
+class MergeEvent:
+    """One controller decision (engine.py:764-770)."""
+    epoch_start: int
+    epochs: int
+    columns: int
+    avg_seconds: float
+    action: str  # baseline | accepted | rejected | settled
+
+
+def run_epoch(trainer: MicrographTrainer, epoch: int) -> float:
+    """Train one epoch on the trainer's current trace table; returns its
+    device-timed duration in seconds, max over ranks (identical on every
+    rank, so controller decisions agree without further exchange)."""
+    iters = trainer.begin_epoch(epoch)
+    dev = trainer.device
+    if dist.is_initialized() and trainer.S > 1:
+        dist.barrier(group=trainer.group)
+    torch.cuda.synchronize(dev)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for it in range(iters):
+        trainer.step(it, want_loss=False)
+    t1.record()
+    torch.cuda.synchronize(dev)
+    trainer.flush_accounting()  # fast-path entries belong to this epoch's table
+    sec = torch.tensor([t0.elapsed_time(t1) / 1e3], dtype=torch.float64, device=dev)
+    if dist.is_initialized() and trainer.S > 1:
+        dist.all_reduce(sec, op=dist.ReduceOp.MAX, group=trainer.group)
+    return float(sec.item())
+
+
+def counts_for_next_epoch(trainer: MicrographTrainer, tt: TraceTable, epoch: int) -> np.ndarray:
+    """Cell root counts of `epoch`'s first iteration under `tt`
+    (engine.py:836-842): the controller decides before running it."""
+    S, B = trainer.S, trainer.B
+    perm = epoch_permutation(trainer.seed, epoch, trainer.graph.n_vertices,
+                             trainer.device).cpu().numpy()
+    home = trainer.part.home
+    batches = [perm[min(d * B, len(perm)):min((d + 1) * B, len(perm))] for d in range(S)]
+    groups = [tuple(b[home[b] == s] for s in range(S)) for b in batches]
+    cells = assign_cell_roots(tt, groups, chain(trainer.seed, SEED_MERGE, epoch, 0))
+    return cell_counts(cells)
+
+
+def merge_controller(trainer: MicrographTrainer, epochs: int, merge_k: int, cost=None):
+    """Greedy column removal (engine.py:773-833): run K epochs, tentatively drop
+    the column with the fewest roots, keep the drop only if the average epoch
+    cost strictly shrinks, else revert and settle.  The cost is the measured
+    epoch time (max over ranks) unless ``cost(table, seconds)`` overrides it
+    (the reference uses its simulated clock).  Merged tables run through the
+    general cell path; every rank reaches identical decisions.
+    Returns (final table, [MergeEvent], per-epoch seconds)."""
+    if trainer.strategy != "micrograph":
+        raise ValueError("merging applies to the micrograph strategy")
+    cost = cost or (lambda table, seconds: seconds)
+    K = int(merge_k)
+    tt = TraceTable.initial(trainer.S)
+    history, times = [], []
+    epoch = 0
+
+    def run_block(table: TraceTable, count: int) -> float:
+        nonlocal epoch
+        vals = []
+        for _ in range(count):
+            trainer.table = table
+            sec = run_epoch(trainer, epoch)
+            times.append(sec)
+            vals.append(float(cost(table, sec)))
+            epoch += 1
+        return float(np.mean(vals)) if vals else 0.0
+
+    baseline = min(K, epochs)
+    old = run_block(tt, baseline)
+    history.append(MergeEvent(0, baseline, tt.n_columns, old, "baseline"))
+    settled = False
+    while not settled and epoch + K <= epochs and tt.n_columns >= 2:
+        probe = tt.copy()
+        probe.root_counts = counts_for_next_epoch(trainer, tt, epoch)
+        target = find_fewest_column(probe)
+        if target is None:
+            break
+        tentative = delete_column_and_redistribute(probe, target)
+        tentative.validate()
+        start = epoch
+        new = run_block(tentative, K)
+        if new < old:
+            tt, old = tentative, new
+            history.append(MergeEvent(start, K, tt.n_columns, new, "accepted"))
+        else:
+            history.append(MergeEvent(start, K, tentative.n_columns, new, "rejected"))
+            settled = True
+    if epoch < epochs:
+        start = epoch
+        avg = run_block(tt, epochs - epoch)
+        history.append(MergeEvent(start, epochs - start, tt.n_columns, avg, "settled"))
+    trainer.table = tt
+    return tt, history, times

@@ -59,9 +59,10 @@ def pregather_worker(rank, world, init_file, result_file):
     dist.destroy_process_group()
 
 
-def micrograph_worker(rank, world, init_file, result_file, mode, dtype_name, feat_mode="pg"):
-    """Full multi-GPU micrograph iterations vs the oracle engine (ledger exact,
-    parameters within tolerance)."""
+def micrograph_worker(rank, world, init_file, result_file, mode, dtype_name, feat_mode="pg",
+                      strategy="micrograph"):
+    """Full multi-GPU micrograph (or model-centric) iterations vs the oracle
+    engine (ledger exact, parameters within tolerance)."""
     import json
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", init_method=f"file://{init_file}", rank=rank,
@@ -81,7 +82,7 @@ def micrograph_worker(rank, world, init_file, result_file, mode, dtype_name, fea
     part = PartitionMap(home, world, f"cuda:{rank}")
     model = init_model(arch, D, H, len(fo), C, chain(seed, 0x07), f"cuda:{rank}")
     tr = MicrographTrainer(G, part, model, fo, B, seed, lr=0.1, dtype=dtype, mode=mode,
-                           iterations=iters, pregather=(feat_mode == "pg"))
+                           iterations=iters, pregather=(feat_mode == "pg"), strategy=strategy)
     tr.begin_epoch(0)
     losses = [tr.step(it) for it in range(tr.iters)]
     torch.cuda.synchronize()
@@ -93,23 +94,92 @@ def micrograph_worker(rank, world, init_file, result_file, mode, dtype_name, fea
         P = w.fresh_params()
         oled = OE.Ledger()
         for it, batches in enumerate(OE.epoch_batches(seed, 0, 3000, world, B, iters)):
-            OE.micrograph_iteration(w, P, 0, it, batches, OE.initial_table(world), (), True, oled)
-        got = {k: v for k, v in led.counters.items()}
-        want = {k: tuple(v) for k, v in oled.cells.items()}
-        for k in set(got) | set(want):
-            gb, gm = got.get(k, (0.0, 0))
-            wb, wm = want.get(k, (0.0, 0))
-            if abs(gb - wb) > 1e-9 * max(1.0, abs(wb)) or gm != wm:
-                out = {"ok": False, "msg": f"ledger {k}: got {gb},{gm} want {wb},{wm}"}
-                break
-        # bf16: numerics are pinned by test_step_gpu against a bf16-emulating oracle;
-        # here only gross agreement with the exact float64 oracle is required
-        tol = 1e-3 if dtype_name == "f32" else 1e-1
-        for i, (a, b) in enumerate(zip(model.params(), P.arrays())):
-            err = float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
-            if out["ok"] and err > tol:
-                out = {"ok": False, "msg": f"param {i} rel err {err}"}
+            if strategy == "model-centric":
+                OE.model_centric_iteration(w, P, 0, it, batches, oled)
+            else:
+                OE.micrograph_iteration(w, P, 0, it, batches, OE.initial_table(world), (), True,
+                                        oled)
+        out = _compare(led, oled, model, P, dtype_name)
         out["losses"] = losses
+    with open(f"{result_file}.{rank}", "w") as f:
+        json.dump(out, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _compare(led, oled, model, P, dtype_name):
+    out = {"ok": True, "msg": ""}
+    got = {k: v for k, v in led.counters.items()}
+    want = {k: tuple(v) for k, v in oled.cells.items()}
+    for k in set(got) | set(want):
+        gb, gm = got.get(k, (0.0, 0))
+        wb, wm = want.get(k, (0.0, 0))
+        if abs(gb - wb) > 1e-9 * max(1.0, abs(wb)) or gm != wm:
+            out = {"ok": False, "msg": f"ledger {k}: got {gb},{gm} want {wb},{wm}"}
+            break
+    # bf16: numerics are pinned by test_step_gpu against a bf16-emulating oracle;
+    # here only gross agreement with the exact float64 oracle is required
+    tol = 1e-3 if dtype_name == "f32" else 1e-1
+    for i, (a, b) in enumerate(zip(model.params(), P.arrays())):
+        err = float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
+        if out["ok"] and err > tol:
+            out = {"ok": False, "msg": f"param {i} rel err {err}"}
+    return out
+
+
+def merge_worker(rank, world, init_file, result_file, feat_mode):
+    """Merging controller over 3 epochs (forced acceptance of the first drop)
+    vs the oracle replaying the same decision: tables, ledger, parameters."""
+    import json
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", init_method=f"file://{init_file}", rank=rank,
+                            world_size=world)
+    from oracle import engine as OE
+    from oracle.graphgen import GraphSpec as OSpec, build_csr, build_tables
+    from oracle.rng import chain, keyed
+    from paper_2409_00657_b200.distributed import MicrographTrainer, merge_controller
+    from paper_2409_00657_b200.graph import Graph, PartitionMap
+    from paper_2409_00657_b200.model import init_model
+    seed, arch, fo, D, H, C, B, iters, n = 4, "sage-mean", (10, 5), 16, 64, 5, 48, 2, 2500
+    off, tgt = build_csr(build_tables(OSpec(n=n, avg_deg=10.0, beta=0.7, p_in=0.9,
+                                            n_blocks=4, d_cap=500, seed=12)))
+    home = (keyed(chain(seed, 0x02, 0xA7), np.arange(n)) % np.uint64(world)).astype(np.int64)
+    G = Graph.from_host(off, tgt, f"cuda:{rank}")
+    part = PartitionMap(home, world, f"cuda:{rank}")
+    model = init_model(arch, D, H, len(fo), C, chain(seed, 0x07), f"cuda:{rank}")
+    tr = MicrographTrainer(G, part, model, fo, B, seed, lr=0.1, dtype=torch.float32,
+                           mode="fused", iterations=iters, pregather=(feat_mode == "pg"))
+    tt, hist, times = merge_controller(tr, epochs=3, merge_k=1,
+                                       cost=lambda table, sec: float(table.n_columns))
+    torch.cuda.synchronize()
+    led = tr.global_ledger()
+    out = {"ok": True, "msg": ""}
+    if rank == 0:
+        acts = [(h.action, h.columns) for h in hist]
+        want_acts = [("baseline", world), ("accepted", world - 1)]
+        want_acts += [("accepted", world - 2)] if world > 2 else [("settled", 1)]
+        w = OE.World(off, tgt, home, world, seed, arch, D, H, C, fo, B, iterations=iters)
+        P = w.fresh_params()
+        oled = OE.Ledger()
+        server_of, removed = OE.initial_table(world), ()
+        for epoch in range(3):
+            if epoch > 0 and server_of.shape[1] >= 2:
+                first = OE.epoch_batches(seed, epoch, n, world, B, iters)[0]
+                groups = [tuple(b[home[b] == s] for s in range(world)) for b in first]
+                cells = OE.assign_cells(groups, removed, chain(seed, 0x08, epoch, 0))
+                counts = np.array([[len(c) for c in row] for row in cells])
+                col = OE.fewest_column(counts)
+                server_of, _ = OE.delete_column(server_of, counts, col)
+                removed = removed + (col,)
+            for it, batches in enumerate(OE.epoch_batches(seed, epoch, n, world, B, iters)):
+                OE.micrograph_iteration(w, P, epoch, it, batches, server_of, removed, True, oled)
+        if acts != want_acts:
+            out = {"ok": False, "msg": f"events {acts} want {want_acts}"}
+        elif tuple(tt.removed) != tuple(removed) or not np.array_equal(tt.server_of, server_of):
+            out = {"ok": False, "msg": f"table {tt.removed} want {removed}"}
+        else:
+            out = _compare(led, oled, model, P, "f32")
+        out["times"] = times
     with open(f"{result_file}.{rank}", "w") as f:
         json.dump(out, f)
     dist.barrier()

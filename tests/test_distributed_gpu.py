@@ -34,3 +34,31 @@ def test_micrograph_strategy_matches_oracle(mode, dtype, feat):
              nprocs=world, join=True)
     res = json.load(open(os.path.join(d, "res.0")))
     assert res["ok"], res["msg"]
+
+
+@pytest.mark.parametrize("feat", ["pg", "peer"])
+def test_model_centric_matches_oracle(feat):
+    """Model-centric baseline (engine.py:482-507) on the GPUs: ledger exact."""
+    import dist_helpers
+    world = _world()
+    d = tempfile.mkdtemp()
+    mp.spawn(dist_helpers.micrograph_worker,
+             args=(world, os.path.join(d, "init"), os.path.join(d, "res"), "fused", "f32", feat,
+                   "model-centric"),
+             nprocs=world, join=True)
+    res = json.load(open(os.path.join(d, "res.0")))
+    assert res["ok"], res["msg"]
+
+
+@pytest.mark.parametrize("feat", ["pg", "peer"])
+def test_merge_controller_matches_oracle(feat):
+    """Merging controller (engine.py:773-833) with a forced-acceptance cost:
+    decisions, merged trace tables, ledger and parameters equal the oracle's."""
+    import dist_helpers
+    world = _world()
+    d = tempfile.mkdtemp()
+    mp.spawn(dist_helpers.merge_worker,
+             args=(world, os.path.join(d, "init"), os.path.join(d, "res"), feat),
+             nprocs=world, join=True)
+    res = json.load(open(os.path.join(d, "res.0")))
+    assert res["ok"], res["msg"]
