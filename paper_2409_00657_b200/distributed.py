@@ -292,6 +292,8 @@ class PeerFeatures:
         d.feat_row = self.local_row.data_ptr()
         d.feat_peers = self.peers.data_ptr()
         d.feat_home = self.home.data_ptr()
+        d.stage_base = None
+        d.stage_row = None
         d.rank = self.rank
 
     def bind_staged(self, runner: CellRunner, stage_cap: int) -> None:
@@ -453,6 +455,12 @@ class MicrographTrainer:
         ev.record()
         self._pin_ev[i] = ev
         runner.n_roots, runner.roots_per_state = n, max(n, 1)
+        # general (host-planned) path: roots live in the runner, layer 1 is
+        # gathered by the step itself, remote rows are read in place
+        runner.desc.roots = runner.roots.data_ptr()
+        runner.desc.agg1_ready = 0
+        if not self.pregather:
+            self.feats.bind(runner)
         return n
 
     # ------------------------------------------------------------ fast path
@@ -509,6 +517,7 @@ class MicrographTrainer:
             r.builder.build(self.graph, rp, kp, n, n_roots=n, stream=s)
             r.desc.roots = rp
             if not self.pregather:
+                self.feats.bind_staged(r, self._stage_cap)
                 # device pre-gather of the remote rows (NVLink bulk copies) and the
                 # parameter-independent layer-1 gather, both ahead of training
                 self._acct_row_ptr(it)
@@ -546,9 +555,8 @@ class MicrographTrainer:
                                                self.fanout, self.runners[0].max_roots,
                                                self.labels))
                 lay = self.runners[0].builder.layout
-                cap = min(self.runners[0].max_roots * lay.cap_need[0], self.part.n_vertices)
-                for rr in self.runners[:2]:
-                    self.feats.bind_staged(rr, cap)
+                self._stage_cap = min(self.runners[0].max_roots * lay.cap_need[0],
+                                      self.part.n_vertices)
                 self._ra = RunAhead(self.runners[:2], self.device)
             r = self._ra.acquire(it, self._fast_build(it))
         n = r.n_roots
