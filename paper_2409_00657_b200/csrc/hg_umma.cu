@@ -21,6 +21,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <mutex>
 #include <unordered_map>
 
@@ -69,6 +70,22 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* m
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
+}
+
+// smem box -> global (plain store or f32 add-reduction in L2), bulk-group completion
+template <bool REDUCE>
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* smem_src, int c0,
+                                             int c1) {
+  if constexpr (REDUCE)
+    asm volatile(
+        "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];"
+        ::"l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+        : "memory");
+  else
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+                 : "memory");
 }
 
 // UMMA shared-memory descriptor, 128B swizzle (sm_100 version 1).
@@ -148,12 +165,13 @@ struct UmmaArgs {
   void* C;
   int64_t ldc;
   const float* bias;
+  int tma_epi;               // 1: epilogue through smem + TMA store/reduce (map_c valid)
 };
 
 template <bool A_MN, bool B_MN, int BN_T, int EPI>
 __global__ void __launch_bounds__(128, 1)
 k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-            UmmaArgs args) {
+            const __grid_constant__ CUtensorMap map_c, UmmaArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-aligned stage ring
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -164,6 +182,7 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   constexpr uint32_t kTmemCols = BN_T <= 32 ? 32 : BN_T <= 64 ? 64 : BN_T <= 128 ? 128 : 256;
   __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], done_bar;
   __shared__ uint32_t tmem_base_sh;
+  __shared__ float bias_s[EPI == UEPI_BIAS_RELU_BF16 ? BN_T : 1];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * BM_T, n0 = blockIdx.y * BN_T;
@@ -185,6 +204,10 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     }
     mbar_init(&done_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if constexpr (EPI == UEPI_BIAS_RELU_BF16) {
+    for (int c = threadIdx.x; c < BN_T; c += blockDim.x)
+      bias_s[c] = n0 + c < args.N ? args.bias[n0 + c] : 0.f;
   }
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -247,7 +270,64 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   mbar_wait(&done_bar, 0);
   asm volatile("tcgen05.fence::after_thread_sync;");
   const int row = m0 + warp * 32 + lane;
+#ifdef HG_UMMA_NOEPI  // timing experiment: main loop only
+  const bool valid = false;
+  if (false) {
+#else
   const bool valid = row < M;
+  if (args.tma_epi) {
+#endif
+    // Coalesced epilogue: each warp stages its 32 rows x (128-byte column
+    // chunk) in the now idle pipeline smem, 128B-swizzled, and one lane hands
+    // the box to TMA (store, or f32 add-reduce in L2 for split-K partials).
+    // Rows past the device count are written as zeros (inside the capacity).
+    constexpr int EB = EPI == UEPI_BIAS_RELU_BF16 ? 2 : 4;
+    constexpr int CW = 128 / EB;             // columns per 128-byte row
+    constexpr int NCH = (BN_T + CW - 1) / CW;
+    uint8_t* stage = smem + warp * (NCH * 4096);
+    const bool warp_rows = m0 + warp * 32 < M;
+#pragma unroll 1
+    for (int ch = 0; ch < NCH; ++ch) {
+      const int c = ch * CW;
+      if (n0 + c >= args.N || !warp_rows) break;
+      uint32_t rr[CW];
+#pragma unroll
+      for (int q = 0; q < CW; q += 16)
+        tmem_ld16_issue(tmem + ((uint32_t)(warp * 32) << 16) + c + q, rr + q);
+#pragma unroll
+      for (int q = 0; q < CW; q += 16) tmem_wait16(rr + q);
+      uint8_t* box = stage + ch * 4096 + lane * 128;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        uint4 v;
+        if constexpr (EPI == UEPI_BIAS_RELU_BF16) {
+          uint32_t pk[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int cc = c + u * 8 + 2 * j;
+            const float x0 = valid ? fmaxf(__uint_as_float(rr[u * 8 + 2 * j]) + bias_s[cc], 0.f) : 0.f;
+            const float x1 = valid ? fmaxf(__uint_as_float(rr[u * 8 + 2 * j + 1]) + bias_s[cc + 1], 0.f) : 0.f;
+            const __nv_bfloat162 t = __floats2bfloat162_rn(x0, x1);
+            pk[j] = *reinterpret_cast<const uint32_t*>(&t);
+          }
+          v = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        } else {
+          v = valid ? make_uint4(rr[u * 4], rr[u * 4 + 1], rr[u * 4 + 2], rr[u * 4 + 3])
+                    : make_uint4(0, 0, 0, 0);
+        }
+        *reinterpret_cast<uint4*>(box + ((u ^ (lane & 7)) << 4)) = v;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        tma_store_2d<EPI == UEPI_ATOMIC_F32>(&map_c, stage + ch * 4096, n0 + c, m0 + warp * 32);
+    }
+    if (lane == 0) {
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    __syncwarp();
+  } else {
   constexpr int CH = BN_T % 64 == 0 ? 64 : 16;  // columns per TMEM round trip
 #pragma unroll 1
   for (int cb = 0; cb < BN_T; cb += CH) {
@@ -303,6 +383,7 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     }
   }
   }
+  }  // row-per-thread epilogue
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 2)
@@ -332,11 +413,11 @@ static EncodeFn encoder() {
 
 // 2D bf16 tensor map: inner dim (contiguous) x outer dim, row pitch in elements.
 static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t pitch,
-                    uint32_t box_inner, uint32_t box_outer) {
+                    uint32_t box_inner, uint32_t box_outer, int elem_bytes = 2) {
   struct Key {
-    const void* p; uint64_t a, b, c; uint32_t d, e;
+    const void* p; uint64_t a, b, c; uint32_t d, e; int f;
     bool operator==(const Key& o) const {
-      return p == o.p && a == o.a && b == o.b && c == o.c && d == o.d && e == o.e;
+      return p == o.p && a == o.a && b == o.b && c == o.c && d == o.d && e == o.e && f == o.f;
     }
   };
   struct H {
@@ -347,17 +428,17 @@ static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
   };
   static std::mutex mu;
   static std::unordered_map<Key, CUtensorMap, H> cache;
-  Key key{base, inner, outer, pitch, box_inner, box_outer};
+  Key key{base, inner, outer, pitch, box_inner, box_outer, elem_bytes};
   std::lock_guard<std::mutex> lk(mu);
   auto it = cache.find(key);
   if (it != cache.end()) { *m = it->second; return HG_OK; }
   EncodeFn enc = encoder();
   if (!enc) return hg_fail(HG_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {pitch * 2};
+  cuuint64_t strides[1] = {pitch * (uint64_t)elem_bytes};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+  CUresult r = enc(m, elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return hg_fail(HG_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -366,8 +447,8 @@ static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
 }
 
 template <bool A_MN, bool B_MN, int BN_T, int EPI>
-static int launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const UmmaArgs& a, int split,
-                    cudaStream_t s) {
+static int launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                    const UmmaArgs& a, int split, cudaStream_t s) {
   constexpr int smem = kStages * (BM_T * BK_T * 2 + BN_T * BK_T * 2) + 1024;
   auto kern = k_umma_gemm<A_MN, B_MN, BN_T, EPI>;
   static bool attr = false;
@@ -377,7 +458,7 @@ static int launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const UmmaArgs
   }
   dim3 grid((a.M + BM_T - 1) / BM_T, (a.N + BN_T - 1) / BN_T, split);
   count_launch();
-  kern<<<grid, 128, smem, s>>>(ma, mb, a);
+  kern<<<grid, 128, smem, s>>>(ma, mb, mc, a);
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;
 }
@@ -387,7 +468,21 @@ int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
               void* C, int64_t ldc, int M, int N, int K, const int32_t* M_dev,
               const int32_t* K_dev, int epi, const float* bias, int split, cudaStream_t s) {
   if (N <= 0 || (N > 256 && N % 256)) return hg_fail(HG_ECONFIG, "umma N must be <= 256 or a multiple of 256");
-  const int bn = N > 256 ? 256 : (N + 63) / 64 * 64;  // N tile (grid.y covers the rest)
+  // N tile (grid.y covers the rest): the widest tile that still spreads the
+  // problem over about half the SMs -- small-M GEMMs (one micrograph batch of
+  // roots) otherwise run on a handful of SMs, each streaming all of B
+  int bn = N > 256 ? 256 : (N + 63) / 64 * 64;
+  {
+    const int mt = (M + BM_T - 1) / BM_T;
+    auto ctas = [&](int b) { return mt * ((N + b - 1) / b) * std::max(split, 1); };
+    static int sms = [] {
+      int dev = 0, n = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+      return n > 0 ? n : 148;
+    }();
+    while (bn > 64 && ctas(bn) < sms / 2) bn = bn == 192 ? 128 : bn / 2;
+  }
   if (lda % 8 || ldb % 8) return hg_fail(HG_ECONFIG, "umma leading dims must be multiples of 8");
   CUtensorMap ma, mb;
   int st;
@@ -398,11 +493,19 @@ int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
   if (b_mn) st = make_map(&mb, B, (uint64_t)N, (uint64_t)K, ldb, 64, BK_T);
   else st = make_map(&mb, B, (uint64_t)K, (uint64_t)N, ldb, BK_T, (uint32_t)bn);
   if (st) return st;
-  UmmaArgs a{M, N, K, M_dev, K_dev, C, ldc, bias};
+  // TMA epilogue when C's rows are 16-byte aligned (else row-per-thread stores)
+  CUtensorMap mc;
+  const int eb = epi == UEPI_BIAS_RELU_BF16 ? 2 : 4;
+  int tma_epi = ((uintptr_t)C % 16 == 0 && (ldc * eb) % 16 == 0) ? 1 : 0;
+  if (tma_epi && make_map(&mc, C, (uint64_t)N, (uint64_t)M, ldc, 128 / eb, 32, eb) != HG_OK) {
+    tma_epi = 0;
+  }
+  if (!tma_epi) memset(&mc, 0, sizeof(mc));
+  UmmaArgs a{M, N, K, M_dev, K_dev, C, ldc, bias, tma_epi};
 
 #define HG_UMMA_CASE(AM, BMJ, BNV, E)                                                       \
   if (a_mn == AM && b_mn == BMJ && bn == BNV && epi == E)                                   \
-    return launch_t<AM, BMJ, BNV, E>(ma, mb, a, split, s);
+    return launch_t<AM, BMJ, BNV, E>(ma, mb, mc, a, split, s);
 #define HG_UMMA_N(AM, BMJ, E) \
   HG_UMMA_CASE(AM, BMJ, 64, E) HG_UMMA_CASE(AM, BMJ, 128, E) HG_UMMA_CASE(AM, BMJ, 192, E) HG_UMMA_CASE(AM, BMJ, 256, E)
   HG_UMMA_N(false, false, UEPI_BIAS_RELU_BF16)

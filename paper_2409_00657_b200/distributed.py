@@ -394,6 +394,11 @@ class MicrographTrainer:
         self.stats = FetchStats()
         self.traffic = Traffic()
         self.flat_bytes = model.flat.numel() * 4
+        # pinned loss slots for the pipelined readback (allocated up front:
+        # pinning costs ~10 ms, never inside a step)
+        self._loss_pin = [torch.zeros(1, dtype=torch.float32).pin_memory() for _ in range(4)]
+        self._loss_slot = 0
+        self._loss_pending = []
         self._recv_p = torch.empty_like(model.flat) if mode == "faithful" else None
         self._recv_g = torch.empty_like(model.grad) if mode == "faithful" else None
         # our own NCCL communicator for the in-C all-reduce+SGD (and hops)
@@ -564,11 +569,6 @@ class MicrographTrainer:
         if n:
             _lib.call("hg_train_step", C.byref(r.desc), n, s)
             if want_loss:  # pipelined readback: this step's loss arrives next call
-                if not hasattr(self, "_loss_pin"):
-                    self._loss_pin = [torch.zeros(1, dtype=torch.float32).pin_memory()
-                                      for _ in range(4)]
-                    self._loss_slot = 0
-                    self._loss_pending = []
                 self._loss_slot = (self._loss_slot + 1) % 4
                 self._loss_pin[self._loss_slot].copy_(r.loss[:n].sum().reshape(1),
                                                       non_blocking=True)
