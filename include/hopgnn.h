@@ -215,6 +215,9 @@ typedef struct {
   void* WcT;                             /* bf16 [C x H]  (K-major B of the logits)    */
   void* Wcp;                             /* bf16 [H x Cp] (K-major B of dz_L)          */
   void* dl_lowp;                         /* bf16 [max_roots x Cp] dlogits               */
+  /* per-root capacity of need[k] rows (hg_mg_layout.cap_need); 0 = unknown.
+   * Enables the per-root fused backward scatter when a root's rows fit smem. */
+  int32_t root_rows[HG_MAX_LAYERS + 1];
 } hg_step_desc;
 
 /* Peer memory (one process per GPU): device allocations whose CUDA IPC

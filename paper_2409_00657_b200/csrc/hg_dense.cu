@@ -405,6 +405,70 @@ k_scatter(const float* __restrict__ dagg, int ld, const int32_t* __restrict__ se
   }
 }
 
+// Fused backward of one aggregation layer, one root's micrograph at a time:
+// dh_{k-1} = scatterᵀ(dagg_k) (the transpose of k_aggregate), then
+// dz = dh * (h_{k-1} > 0), its bf16 copy for the tensor-core GEMMs, the f32
+// copy when a SIMT GEMM still needs it, and the bias-gradient column sums.
+// A root's need[k-1] rows are contiguous and every self/neighbour index of
+// its need[k] rows points inside them (k_mg_finalize), so the scatter runs in
+// shared memory with each thread owning whole columns: no atomics, no zeroing
+// pass, one read of dagg and h, one write of dz.  Replaces k_zero_rows +
+// k_scatter + k_mask_colsum when root_rows[k-1] * H floats fit in smem.
+template <bool SAGE, typename T>
+__global__ void __launch_bounds__(256)
+k_scatter_root(const float* __restrict__ dagg, int ld, const int32_t* __restrict__ need_off_p,
+               const int32_t* __restrict__ need_off_c, const int32_t* __restrict__ self_pos,
+               const int32_t* __restrict__ nbr_off, const int32_t* __restrict__ nbr_idx,
+               int n_roots, int H, const T* __restrict__ h, float* __restrict__ dh_out,
+               bf16* __restrict__ lowp, float* __restrict__ gb,
+               const int32_t* __restrict__ n_rows_dev, int cap_rows) {
+  extern __shared__ float acc[];  // [root_rows x H]
+  // each thread owns columns c and c + blockDim.x (H <= 2 * blockDim.x)
+  float colsum0 = 0.f, colsum1 = 0.f;
+  for (int r = blockIdx.x; r < n_roots; r += gridDim.x) {
+    const int q0 = need_off_p[r], nq = need_off_p[r + 1] - q0;
+    const int p0 = need_off_c[r], p1 = need_off_c[r + 1];
+    for (int c = threadIdx.x; c < H; c += blockDim.x) {
+      float colsum = 0.f;
+      for (int i = 0; i < nq; ++i) acc[i * H + c] = 0.f;
+      for (int p = p0; p < p1; ++p) {
+        const int s = self_pos[p] - q0;
+        const int j0 = nbr_off[p], j1 = nbr_off[p + 1];
+        const int deg = j1 - j0;
+        const float* g = dagg + (int64_t)p * ld;
+        if constexpr (SAGE) {
+          const float gs = g[c], gn = g[H + c];
+          acc[s * H + c] += deg > 0 ? gs : gs + gn;
+          const float v = deg > 0 ? gn / (float)deg : 0.f;
+          for (int j = j0; j < j1; ++j) acc[(nbr_idx[j] - q0) * H + c] += v;
+        } else {
+          const float v = g[c] / (float)(deg + 1);
+          acc[s * H + c] += v;
+          for (int j = j0; j < j1; ++j) acc[(nbr_idx[j] - q0) * H + c] += v;
+        }
+      }
+      for (int i = 0; i < nq; ++i) {
+        const int64_t o = (int64_t)(q0 + i) * H + c;
+        const float v = to_f(h[o]) > 0.f ? acc[i * H + c] : 0.f;
+        if (dh_out) dh_out[o] = v;
+        if (lowp) lowp[o] = __float2bfloat16_rn(v);
+        colsum += v;
+      }
+      if (c == threadIdx.x) colsum0 += colsum;
+      else colsum1 += colsum;
+    }
+  }
+  if (threadIdx.x < H) atomicAdd(gb + threadIdx.x, colsum0);
+  if (threadIdx.x + blockDim.x < H) atomicAdd(gb + threadIdx.x + blockDim.x, colsum1);
+  // the dW GEMM reduces over rows up to the next multiple of 64: zero the padding
+  if (lowp && blockIdx.x == 0) {
+    const int n_rows = *n_rows_dev;
+    const int pad = min(cap_rows, (n_rows + 63) / 64 * 64);
+    for (int64_t i = (int64_t)n_rows * H + threadIdx.x; i < (int64_t)pad * H; i += blockDim.x)
+      lowp[i] = __float2bfloat16_rn(0.f);
+  }
+}
+
 // dz = dh * (h > 0) in place; gb[c] += sum_rows dz[., c]
 // Optional bf16 copy of dz for the tensor-core dW GEMM, whose row reduction
 // reads up to the next multiple of 64 rows: those padding rows are zeroed.
@@ -579,6 +643,19 @@ static void launch_aggregate(const hg_step_desc* d, int k, cudaStream_t s, bool 
   }
 }
 
+constexpr size_t kScatterSmem = 96 * 1024;
+
+template <typename T>
+static void scatter_root_attrs() {
+  static bool done = false;
+  if (done) return;
+  cudaFuncSetAttribute(k_scatter_root<true, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kScatterSmem);
+  cudaFuncSetAttribute(k_scatter_root<false, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)kScatterSmem);
+  done = true;
+}
+
 template <typename T>
 static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool backward) {
   const int L = d->n_layers;
@@ -588,6 +665,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
   const int nb = num_sms() * 4;
   // tensor-core path: bf16 operands, H a multiple of 64 up to 256 (one N tile)
   const bool tc = sizeof(T) == 2 && d->use_tc && H % 64 == 0 && H <= 256;
+  scatter_root_attrs<T>();
   // ---- forward
   prof_begin(PROF_STEP, s);
   if (tc) {
@@ -697,6 +775,27 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
                                                     d->in_dim[k], tot + k, d->max_rows[k],
                                                     d->in_dim[k], nullptr, H, nullptr, nullptr, 0,
                                                     1);
+    }
+    const size_t root_smem = (size_t)d->root_rows[k - 1] * H * sizeof(float);
+    if (d->root_rows[k - 1] > 0 && root_smem <= kScatterSmem && H <= 512) {
+      // f32 dz is only needed where a SIMT GEMM consumes it (layer k-1's dX)
+      const bool tc_dx = tc && d->in_dim[k - 1] % 64 == 0 && d->Wb[k - 1];
+      const bool want_f32 = !tc || (k - 1 >= 2 && !tc_dx);
+      const int grid = std::min(n_roots, num_sms() * 2);
+      count_launch();
+      if (sage)
+        k_scatter_root<true, T><<<grid, 256, root_smem, s>>>(
+            d->dagg, d->in_dim[k], d->mg.need_off[k - 1], d->mg.need_off[k], d->mg.self_pos[k],
+            d->mg.nbr_off[k], d->mg.nbr_idx[k], n_roots, H, (const T*)d->h[k - 1],
+            want_f32 ? d->dh[k - 1] : nullptr, tc ? (bf16*)d->lowp_scratch : nullptr,
+            d->gb[k - 1], tot + (k - 1), d->max_rows[k - 1]);
+      else
+        k_scatter_root<false, T><<<grid, 256, root_smem, s>>>(
+            d->dagg, d->in_dim[k], d->mg.need_off[k - 1], d->mg.need_off[k], d->mg.self_pos[k],
+            d->mg.nbr_off[k], d->mg.nbr_idx[k], n_roots, H, (const T*)d->h[k - 1],
+            want_f32 ? d->dh[k - 1] : nullptr, tc ? (bf16*)d->lowp_scratch : nullptr,
+            d->gb[k - 1], tot + (k - 1), d->max_rows[k - 1]);
+      continue;
     }
     count_launch(3);
     k_zero_rows<<<nb, 256, 0, s>>>(d->dh[k - 1], tot + (k - 1), H);

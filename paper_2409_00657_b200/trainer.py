@@ -55,6 +55,7 @@ class CellRunner:
         d.max_roots = max_roots
         for k in range(L + 1):
             d.max_rows[k] = self.max_rows[k]
+            d.root_rows[k] = lay.cap_need[k]
             d.in_dim[k] = model.in_dim[k]
         d.split_k = split_k or max(1, min(64, self.max_rows[1] // 2048))
         d.use_tc = int(use_tc)
