@@ -85,6 +85,15 @@ int hg_feature_table(const int64_t* ids, int64_t first, int64_t count, int32_t d
 int hg_epoch_permutation(int64_t n, uint64_t state, int64_t* perm_out, void* ws,
                          size_t* ws_bytes, void* stream);
 
+/* Device-side iteration cursor for graph-replayed training loops: reads
+ * it = *it_dev, stages iteration it + ahead (if < iters) -- roots
+ * perm[(it+ahead)*batch ...] into roots_out (skipped when roots_out is NULL)
+ * and states[it+ahead] into key_out[0] -- then advances *it_dev by `advance`.
+ * Every argument is fixed across steps, so the launch can live in a CUDA graph. */
+int hg_iter_stage(const int64_t* perm, const uint64_t* states, int64_t iters, int64_t* it_dev,
+                  int32_t batch, int32_t ahead, int32_t advance, int64_t* roots_out,
+                  uint64_t* key_out, void* stream);
+
 /* Glorot init (model.py:87-90): out f64 or f32 [rows*cols] row-major. */
 int hg_glorot(int32_t rows, int32_t cols, uint64_t state, int32_t dtype, void* out,
               void* stream);

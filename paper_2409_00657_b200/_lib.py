@@ -85,6 +85,7 @@ SIGNATURES = {
     "hg_feature_table": [V, I64, I64, I32, I32, U64, I32, V, V],
     "hg_epoch_permutation": [I64, U64, V, V, PSZ, V],
     "hg_glorot": [I32, I32, U64, I32, V, V],
+    "hg_iter_stage": [V, V, I64, V, I32, I32, I32, V, V, V],
     "hg_graph_raw_degrees": [C.POINTER(GraphTables), V, V],
     "hg_graph_fill": [C.POINTER(GraphTables), I64, I64, V, V, V],
     "hg_graph_canonicalize": [I64, I64, V, V, V, V, PSZ, V],

@@ -111,6 +111,30 @@ extern "C" int hg_epoch_permutation(int64_t n, uint64_t state, int64_t* perm_out
   return HG_OK;
 }
 
+__global__ void k_iter_stage(const int64_t* __restrict__ perm, const uint64_t* __restrict__ states,
+                             int64_t iters, int64_t* it_dev, int batch, int ahead, int advance,
+                             int64_t* __restrict__ roots_out, uint64_t* __restrict__ key_out) {
+  const int64_t it = *it_dev + ahead;
+  if (it < iters) {
+    if (roots_out)
+      for (int i = threadIdx.x; i < batch; i += blockDim.x) roots_out[i] = perm[it * batch + i];
+    if (threadIdx.x == 0) key_out[0] = states[it];
+  }
+  __syncthreads();  // every thread has read *it_dev before it moves
+  if (threadIdx.x == 0 && advance) *it_dev += advance;
+}
+
+extern "C" int hg_iter_stage(const int64_t* perm, const uint64_t* states, int64_t iters,
+                             int64_t* it_dev, int32_t batch, int32_t ahead, int32_t advance,
+                             int64_t* roots_out, uint64_t* key_out, void* stream) {
+  if (batch < 0) return hg_fail(HG_ERANGE, "bad batch");
+  count_launch();
+  k_iter_stage<<<1, 1024, 0, (cudaStream_t)stream>>>(perm, states, iters, it_dev, batch, ahead,
+                                                      advance, roots_out, key_out);
+  HG_CUDA_TRY(cudaGetLastError());
+  return HG_OK;
+}
+
 extern "C" int hg_glorot(int32_t rows, int32_t cols, uint64_t state, int32_t dtype, void* out,
                          void* stream) {
   const int64_t total = (int64_t)rows * cols;

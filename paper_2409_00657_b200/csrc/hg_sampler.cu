@@ -14,7 +14,7 @@
 // only slots whose hash is below a threshold sized for ~fanout+4*sqrt(fanout)+8
 // expected survivors (ballot compaction into smem), then the exact `fanout`
 // smallest survivors are ranked in smem.  Cost is one mix64 per slot, no sort
-// of the hub's adjacency.  Vertices with degree <= 1024 are handled by one
+// of the hub's adjacency.  Vertices with degree <= 256 are handled by one
 // warp; larger hubs by the whole CTA.  A rare under/overflow of the survivor
 // buffer bisects the threshold and retries, so the result is always exact.
 #include <climits>
@@ -28,7 +28,7 @@ namespace hg {
 
 constexpr int kBuildThreads = 256;
 constexpr int kBuildWarps = kBuildThreads / 32;
-constexpr int kBigTask = 4096;  // degree above which the whole CTA draws one vertex
+constexpr int kBigTask = 256;  // degree above which the whole CTA draws one vertex
 
 struct MgCarve {
   int L;
@@ -150,21 +150,40 @@ __device__ void team_select(const int32_t* __restrict__ targets, int64_t lo, int
   for (int attempt = 0;; ++attempt) {
     if (Team::rank() == 0) *ctr = 0;
     Team::sync();
-    for (int base = Team::warp_in_team() * 32; base < d; base += Team::size()) {
-      const int j = base + lane;
-      bool take = false;
-      uint64_t key = 0;
-      if (j < d) {
-        const uint64_t h = mix64(hv ^ (uint64_t)j);
-        take = (h >> 32) < gh;
-        key = (h & kHi32) | (uint64_t)j;
+    // kU slots per lane per pass: independent hashes in flight, and the
+    // warp-uniform survivor count skips the shared-counter round trip on the
+    // (typical) passes where nothing falls below the threshold
+    constexpr int kU = 4;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int base = Team::warp_in_team() * 32 * kU; base < d; base += Team::size() * kU) {
+      bool take[kU];
+      uint64_t key[kU];
+      unsigned mask[kU];
+      int cw = 0;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int j = base + u * 32 + lane;
+        take[u] = false;
+        key[u] = 0;
+        if (j < d) {
+          const uint64_t h = mix64(hv ^ (uint64_t)j);
+          take[u] = (h >> 32) < gh;
+          key[u] = (h & kHi32) | (uint64_t)j;
+        }
+        mask[u] = __ballot_sync(0xffffffffu, take[u]);
+        cw += __popc(mask[u]);
       }
-      const unsigned mask = __ballot_sync(0xffffffffu, take);
-      int off = 0;
-      if (lane == 0 && mask) off = atomicAdd(ctr, __popc(mask));
-      off = __shfl_sync(0xffffffffu, off, 0);
-      const int pos = off + __popc(mask & ((1u << lane) - 1u));
-      if (take && pos < cap) cand[pos] = key;
+      if (cw) {
+        int off = 0;
+        if (lane == 0) off = atomicAdd(ctr, cw);
+        off = __shfl_sync(0xffffffffu, off, 0);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int pos = off + __popc(mask[u] & lt);
+          if (take[u] && pos < cap) cand[pos] = key[u];
+          off += __popc(mask[u]);
+        }
+      }
     }
     Team::sync();
     const int cnt = *ctr;
@@ -548,7 +567,6 @@ k_mg_build(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targ
     for (int k = 0; k <= L; ++k) w[c.ws_cnt + k] = nneed[k];
     for (int k = 1; k <= L; ++k) w[c.ws_cnt + L + k] = ntot[L - k + 1];
   }
-  __syncthreads();
   HG_PHASE(14);
 }
 

@@ -77,13 +77,72 @@ class RunAhead:
         self.built.clear()
 
 
+class GraphLoop:
+    """CUDA-graph replay of the run-ahead loop (S = 1).  Two graphs alternate:
+    graph x trains runner x (built by the previous replay) + SGD, and on a
+    forked branch stages, builds and pre-gathers the next iteration into
+    runner 1-x.  The iteration comes from a device cursor (hg_iter_stage), so
+    every replay has identical launch arguments: one host call per step
+    instead of ~30 launches, and the build branch overlaps the training branch
+    inside the graph.  Optional per-graph extras: H2D of the next roots from a
+    pinned slot (public end-to-end API) and D2H of the summed loss."""
+
+    def __init__(self, tr: "Trainer", runners, e2e: bool = False):
+        self.tr, self.runners, self.e2e = tr, runners, e2e
+        dev = tr.device
+        B = tr.B
+        self.side = torch.cuda.Stream(dev)
+        if e2e:
+            self.pin_roots = [torch.empty(B, dtype=torch.int64).pin_memory() for _ in range(2)]
+            self.pin_loss = [torch.zeros(1, dtype=torch.float32).pin_memory() for _ in range(2)]
+        self.graphs = []
+        self.launches = 0
+        cur = torch.cuda.current_stream(dev)
+        for x in range(2):
+            run, nxt = runners[x], runners[1 - x]
+            for r in (run, nxt):
+                r.desc.roots = r.roots.data_ptr()
+                r.desc.agg1_ready = 1
+                r.n_roots = B
+            g = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream(dev)
+            cap.wait_stream(cur)
+            before = _lib.launch_count()
+            with torch.cuda.graph(g, stream=cap):
+                self.side.wait_stream(cap)
+                ss = self.side.cuda_stream
+                with torch.cuda.stream(self.side):
+                    if e2e:  # roots of the next step, written by the host into a pinned slot
+                        nxt.roots.copy_(self.pin_roots[1 - x], non_blocking=True)
+                    _lib.call("hg_iter_stage", tr._perm_buf.data_ptr(), tr._states_buf.data_ptr(),
+                              tr.iters, tr._it_dev.data_ptr(), B, 1, 1,
+                              None if e2e else nxt.roots.data_ptr(), nxt.keys.data_ptr(), ss)
+                    nxt.builder.build(tr.graph, nxt.roots.data_ptr(), nxt.keys.data_ptr(), B,
+                                      n_roots=B, stream=ss)
+                    _lib.call("hg_step_prologue", C.byref(nxt.desc), B, 1, ss)
+                cs = cap.cuda_stream
+                _lib.call("hg_train_step", C.byref(run.desc), B, cs)
+                tr.model.sgd(tr.lr, B, stream=cs)
+                if e2e:
+                    self.pin_loss[x].copy_(run.loss[:B].sum().reshape(1), non_blocking=True)
+                cap.wait_stream(self.side)
+            self.launches = _lib.launch_count() - before
+            cur.wait_stream(cap)
+            self.graphs.append(g)
+        self.iters = tr.iters
+
+    def replay(self, x: int) -> None:
+        self.graphs[x].replay()
+
+
 class Trainer:
     """One model on one GPU (S = 1): the reference's micrograph and
-    model-centric strategies coincide here (engine.py:485-507 with N = 1)."""
+    model-centric strategies coincide here (engine.py:485-507 with N = 1).
+    ``graphs=True`` replays the steady-state loop as CUDA graphs (GraphLoop)."""
 
     def __init__(self, graph: Graph, table: FeatureTable, model: ModelState, fanout,
                  batch: int, seed: int, lr: float = 0.1, iterations: int = 0,
-                 run_ahead: bool = True):
+                 run_ahead: bool = True, graphs: bool = True):
         self.graph, self.table, self.model = graph, table, model
         self.fanout = tuple(fanout)
         self.B, self.seed, self.lr, self.iter_cap = int(batch), int(seed), float(lr), iterations
@@ -98,6 +157,11 @@ class Trainer:
             self.ra = RunAhead([self.runner, CellRunner(graph, table, model, self.fanout, self.B,
                                                         self.labels)], self.device)
         self.last_runner = self.runner
+        self.graphs = graphs and run_ahead
+        self._gl = None       # GraphLoop for step()
+        self._gl_e2e = None   # GraphLoop for train_step()
+        self._gnext = None    # iteration the graph loop is positioned at
+        self._eager_steps = 0
 
     # ------------------------------------------------------------ epoch plan
     def begin_epoch(self, epoch: int) -> int:
@@ -108,7 +172,63 @@ class Trainer:
         states = [chain(self.sampler_seed, epoch, it) for it in range(self.iters)]
         self.states = torch.from_numpy(_u64_as_i64(states)).to(self.device)
         self.epoch = epoch
+        if self.graphs:
+            # graph-visible copies at fixed addresses (captured once per trainer)
+            if not hasattr(self, "_perm_buf"):
+                self._perm_buf = torch.empty_like(self.perm)
+                self._states_buf = torch.empty_like(self.states)
+                self._it_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
+            self._perm_buf.copy_(self.perm)
+            self._states_buf.copy_(self.states)
+            self._gnext = None
+        # run-ahead builds read perm/states from side streams: order them after
+        # this epoch's permutation (written on the current stream)
+        cur = torch.cuda.current_stream(self.device)
+        for ra in (getattr(self, "ra", None), getattr(self, "_e2e_ra", None)):
+            if ra is not None:
+                ra.side.wait_stream(cur)
         return self.iters
+
+    # ------------------------------------------------------------ graph loop
+    def _graph_ready(self, attr: str, e2e: bool):
+        gl = getattr(self, attr)
+        if gl is not None and gl.iters != self.iters:
+            gl = None
+        if gl is None:
+            if self._eager_steps < 2:  # library state (attributes, tensor maps) warmed eagerly
+                return None
+            self._drain_run_ahead()
+            gl = GraphLoop(self, self.ra.runners if not e2e else self._e2e_ra.runners, e2e)
+            setattr(self, attr, gl)
+        return gl
+
+    def _drain_run_ahead(self) -> None:
+        cur = torch.cuda.current_stream(self.device)
+        for ra in (self.ra, getattr(self, "_e2e_ra", None)):
+            if ra is not None:
+                cur.wait_stream(ra.side)
+                ra.reset()
+
+    def _graph_restart(self, gl: GraphLoop, it: int, roots=None) -> None:
+        """Position the graph loop at `it`: build it eagerly into runner it%2
+        on the current stream, point the device cursor at it."""
+        self._drain_run_ahead()
+        if gl.e2e:
+            cur = torch.cuda.current_stream(self.device)
+            cur.wait_stream(gl.side)
+        r = gl.runners[it % 2]
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        if roots is None:
+            roots = self.roots_of(it)
+        n = roots.numel()
+        r.roots[:n].copy_(roots, non_blocking=True)
+        r.keys[:1].copy_(self.states[it:it + 1])
+        r.builder.build(self.graph, r.roots.data_ptr(), r.keys.data_ptr(), n, n_roots=n, stream=s)
+        r.desc.roots = r.roots.data_ptr()
+        r.n_roots = n
+        _lib.call("hg_step_prologue", C.byref(r.desc), n, 1, s)
+        r.desc.agg1_ready = 1
+        self._it_dev.fill_(it)
 
     def roots_of(self, it: int) -> torch.Tensor:
         lo = min(it * self.B, self.perm.numel())
@@ -134,6 +254,21 @@ class Trainer:
         With run-ahead, iteration it+1's micrographs are built on a side
         stream while this iteration trains."""
         s = self.stream.cuda_stream
+        gl = self._graph_ready("_gl", False) if self.graphs else None
+        if gl is not None and (it + 1 < self.iters or self._gnext == it):
+            if self._gnext != it:
+                self._graph_restart(gl, it)
+            r = gl.runners[it % 2]
+            if it + 1 < self.iters:
+                gl.replay(it % 2)  # trains `it`, builds it+1 into the other runner
+            else:  # last iteration of the epoch: nothing to build ahead
+                _lib.call("hg_train_step", C.byref(r.desc), r.n_roots, s)
+                self.model.sgd(self.lr, r.n_roots, stream=s)
+            self._gnext = it + 1
+            self.last_runner = r
+            return
+        self._gnext = None
+        self._eager_steps += 1
         if not self.run_ahead:
             r = self.runner
             self._build(it)(r, s)
@@ -166,6 +301,12 @@ class Trainer:
                 self.graph, self.table, self.model, self.fanout, self.B, self.labels)],
                 self.device) if self.run_ahead else None
         e = self._e2e
+        if self.graphs and next_roots_host is not None:
+            gl = self._graph_ready("_gl_e2e", True)
+            if gl is not None:
+                return self._train_step_graph(gl, roots_host, it, next_roots_host)
+        e["gnext"] = None
+        self._eager_steps += 1
 
         def build_for(j, roots_h):
             dev = e["dev"][j % 2]
@@ -205,8 +346,45 @@ class Trainer:
         e["pending"] = (ev, e["slot"])
         return prev
 
+    def _train_step_graph(self, gl: GraphLoop, roots_host, it: int, next_roots_host):
+        """train_step through the e2e GraphLoop: the host copies the next
+        step's roots into a pinned slot and launches one graph; the graph's
+        H2D / D2H copies move the roots in and the summed loss out."""
+        e = self._e2e
+        x = it % 2
+        prev = None
+        if e.get("gnext") != it:
+            prev = self._drain_loss()  # an eager step's pending loss
+            dev = e["dev"][x]
+            n = roots_host.numel()
+            dev[:n].copy_(roots_host, non_blocking=True)
+            self._graph_restart(gl, it, dev[:n])
+            e["gev"] = [None, None]
+        # pinned roots slot 1-x was last read by replay(it-2) (same parity as this one)
+        if e["gev"][x] is not None:
+            e["gev"][x].synchronize()
+        gl.pin_roots[1 - x].numpy()[:next_roots_host.numel()] = next_roots_host.numpy()
+        gl.replay(x)
+        ev = torch.cuda.Event()
+        ev.record()
+        e["gev"][x] = ev
+        e["gnext"] = it + 1
+        self.last_runner = gl.runners[x]
+        # the previous step's loss: wait for replay(it-1) while replay(it) is queued
+        ev_prev = e["gev"][1 - x]
+        if ev_prev is not None:
+            ev_prev.synchronize()
+            prev = float(gl.pin_loss[1 - x].item())
+        e["pending_graph"] = (ev, gl, x)
+        return prev
+
     def _drain_loss(self):
         e = getattr(self, "_e2e", None)
+        if e and e.get("pending_graph") is not None:
+            ev, gl, x = e["pending_graph"]
+            ev.synchronize()
+            e["pending_graph"] = None
+            return float(gl.pin_loss[x].item())
         if not e or e["pending"] is None:
             return None
         ev, slot = e["pending"]
