@@ -781,7 +781,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
       // f32 dz is only needed where a SIMT GEMM consumes it (layer k-1's dX)
       const bool tc_dx = tc && d->in_dim[k - 1] % 64 == 0 && d->Wb[k - 1];
       const bool want_f32 = !tc || (k - 1 >= 2 && !tc_dx);
-      const int grid = std::min(n_roots, num_sms() * 2);
+      const int grid = n_roots;  // one CTA per root: every root's latency chain in flight at once
       count_launch();
       if (sage)
         k_scatter_root<true, T><<<grid, 256, root_smem, s>>>(
