@@ -571,30 +571,59 @@ k_mg_build(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targ
 }
 
 // Exclusive scans of the per-root counts (one CTA).  cols 0..L: need sizes,
-// cols L+1..2L: pair counts of layers 1..L.
+// cols L+1..2L: pair counts of layers 1..L.  Every count is loaded up front
+// (one strided gather in flight per thread and column) so the per-column
+// scans run from registers and shared memory only.
+constexpr int kScanCols = 2 * HG_MAX_LAYERS + 1;
+constexpr int kScanPer = 2;  // roots per thread held in registers per 2048-root tile
+
 __global__ void __launch_bounds__(1024)
 k_mg_scan(const int32_t* __restrict__ ws, int n_roots, MgCarve c, hg_mg_batch out) {
   __shared__ int scan[40];
-  const int L = c.L;
-  for (int col = 0; col <= 2 * L; ++col) {
-    int32_t* dst = col <= L ? out.need_off[col] : out.pair_off[col - L];
-    const int per = (n_roots + blockDim.x - 1) / blockDim.x;
-    const int s = threadIdx.x * per;
-    const int e = min(s + per, n_roots);
-    int sum = 0;
-    for (int i = s; i < e; ++i) sum += ws[(size_t)i * c.ws_root_ints + c.ws_cnt + col];
-    int total;
-    int pos = block_exclusive_scan(sum, scan, &total);
-    for (int i = s; i < e; ++i) {
-      dst[i] = pos;
-      pos += ws[(size_t)i * c.ws_root_ints + c.ws_cnt + col];
+  __shared__ int32_t* dsts[kScanCols];
+  const int L = c.L, ncol = 2 * L + 1;
+  if (threadIdx.x < ncol)
+    dsts[threadIdx.x] = threadIdx.x <= L ? out.need_off[threadIdx.x] : out.pair_off[threadIdx.x - L];
+  __syncthreads();
+  int carry[kScanCols];
+#pragma unroll
+  for (int col = 0; col < kScanCols; ++col) carry[col] = 0;
+  for (int base = 0; base < n_roots; base += (int)blockDim.x * kScanPer) {  // tiles of 2048 roots
+    const int s0 = base + threadIdx.x * kScanPer;
+    int v[kScanCols][kScanPer];
+#pragma unroll
+    for (int col = 0; col < kScanCols; ++col)
+#pragma unroll
+      for (int j = 0; j < kScanPer; ++j)
+        v[col][j] = (col < ncol && s0 + j < n_roots)
+                        ? ws[(size_t)(s0 + j) * c.ws_root_ints + c.ws_cnt + col] : 0;
+#pragma unroll
+    for (int col = 0; col < kScanCols; ++col) {
+      if (col >= ncol) continue;  // uniform across the block
+      int32_t* dst = dsts[col];
+      int sum = 0;
+#pragma unroll
+      for (int j = 0; j < kScanPer; ++j) sum += v[col][j];
+      int total;
+      int pos = carry[col] + block_exclusive_scan(sum, scan, &total);
+#pragma unroll
+      for (int j = 0; j < kScanPer; ++j) {
+        if (s0 + j < n_roots) dst[s0 + j] = pos;
+        pos += v[col][j];
+      }
+      carry[col] += total;
     }
-    if (threadIdx.x == 0) {
-      dst[n_roots] = total;
-      out.totals[col] = total;
-      if (col > L) out.nbr_off[col - L][out.totals[col - L]] = total;
+  }
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int col = 0; col < kScanCols; ++col) {
+      if (col >= ncol) continue;
+      int32_t* dst = dsts[col];
+      dst[n_roots] = carry[col];
+      out.totals[col] = carry[col];
     }
-    __syncthreads();
+    // pair totals close the CSR-by-destination offsets of each layer
+    for (int k = 1; k <= L; ++k) out.nbr_off[k][out.totals[k]] = out.totals[L + k];
   }
 }
 
