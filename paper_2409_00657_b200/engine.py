@@ -267,6 +267,11 @@ class Trainer:
             self._gnext = it + 1
             self.last_runner = r
             return
+        if self._gnext is not None:
+            # leaving the graph loop: its last replay may still be building into a
+            # run-ahead runner -- order the side stream after it
+            self.ra.side.wait_stream(torch.cuda.current_stream(self.device))
+            self.ra.reset()
         self._gnext = None
         self._eager_steps += 1
         if not self.run_ahead:
@@ -305,6 +310,9 @@ class Trainer:
             gl = self._graph_ready("_gl_e2e", True)
             if gl is not None:
                 return self._train_step_graph(gl, roots_host, it, next_roots_host)
+        if e.get("gnext") is not None and self._e2e_ra is not None:
+            self._e2e_ra.side.wait_stream(torch.cuda.current_stream(self.device))
+            self._e2e_ra.reset()
         e["gnext"] = None
         self._eager_steps += 1
 
