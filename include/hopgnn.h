@@ -93,6 +93,13 @@ int hg_epoch_permutation(int64_t n, uint64_t state, int64_t* perm_out, void* ws,
 int hg_iter_stage(const int64_t* perm, const uint64_t* states, int64_t iters, int64_t* it_dev,
                   int32_t batch, int32_t ahead, int32_t advance, int64_t* roots_out,
                   uint64_t* key_out, void* stream);
+/* Ranged variant (multi-GPU: this rank's roots of iteration it are
+ * roots[ranges[2it] .. ranges[2it+1])): copies at most `cap` of them, writes
+ * the count to *n_out (device), stages states[it+ahead], advances the cursor. */
+int hg_iter_stage_ranged(const int64_t* roots, const int64_t* ranges, const uint64_t* states,
+                         int64_t iters, int64_t* it_dev, int32_t cap, int32_t ahead,
+                         int32_t advance, int64_t* roots_out, int32_t* n_out, uint64_t* key_out,
+                         void* stream);
 
 /* Glorot init (model.py:87-90): out f64 or f32 [rows*cols] row-major. */
 int hg_glorot(int32_t rows, int32_t cols, uint64_t state, int32_t dtype, void* out,
@@ -170,6 +177,14 @@ int hg_mg_build(const int64_t* offsets, const int32_t* targets, int64_t n_vertic
                 const int64_t* roots, int32_t n_roots, const uint64_t* iter_state,
                 int32_t roots_per_state, const hg_mg_layout* layout, int32_t* ws,
                 hg_mg_batch* out, int* err_flag, void* stream);
+/* Same with a device-resident root count: n_roots is the capacity (grid),
+ * *n_roots_dev <= n_roots the roots actually built; the rest are empty
+ * micrographs (zero rows).  Keeps launch arguments fixed for CUDA graphs. */
+int hg_mg_build_n(const int64_t* offsets, const int32_t* targets, int64_t n_vertices,
+                  const int64_t* roots, int32_t n_roots, const int32_t* n_roots_dev,
+                  const uint64_t* iter_state, int32_t roots_per_state,
+                  const hg_mg_layout* layout, int32_t* ws, hg_mg_batch* out, int* err_flag,
+                  void* stream);
 
 
 /* ------------------------------------------------------------------------
@@ -270,6 +285,15 @@ int hg_pregather_peer(const int32_t* ids, const int32_t* n_dev, const int32_t* h
                       int32_t* stage_count, int32_t stage_cap, void* staging,
                       unsigned long long* uniq_per_home, unsigned long long* total_remote,
                       int* err, void* stream);
+/* Same, with the per-home counts written to row *it_dev of an [iters x S]
+ * table (uniq_per_home + *it_dev * row_stride): fixed arguments for graphs. */
+int hg_pregather_peer_at(const int32_t* ids, const int32_t* n_dev, const int32_t* home,
+                         int32_t rank, const int32_t* local_row, const void* peers,
+                         int32_t row_bytes, uint32_t* bitmap, int32_t* stage_list,
+                         int32_t* stage_row, int32_t* stage_count, int32_t stage_cap,
+                         void* staging, unsigned long long* uniq_per_home, const int64_t* it_dev,
+                         int32_t row_stride, unsigned long long* total_remote, int* err,
+                         void* stream);
 /* Parameter-independent prologue of a step: the layer-1 gather + aggregate
  * (sets up agg[1]; run ahead of the previous iteration's training). */
 int hg_step_prologue(const hg_step_desc* d, int32_t n_roots, int32_t backward, void* stream);

@@ -86,6 +86,7 @@ SIGNATURES = {
     "hg_epoch_permutation": [I64, U64, V, V, PSZ, V],
     "hg_glorot": [I32, I32, U64, I32, V, V],
     "hg_iter_stage": [V, V, I64, V, I32, I32, I32, V, V, V],
+    "hg_iter_stage_ranged": [V, V, V, I64, V, I32, I32, I32, V, V, V, V],
     "hg_graph_raw_degrees": [C.POINTER(GraphTables), V, V],
     "hg_graph_fill": [C.POINTER(GraphTables), I64, I64, V, V, V],
     "hg_graph_canonicalize": [I64, I64, V, V, V, V, PSZ, V],
@@ -94,6 +95,8 @@ SIGNATURES = {
     "hg_mg_plan_layout": [I32, C.POINTER(I32), C.POINTER(MgLayout)],
     "hg_mg_build": [V, V, I64, V, I32, V, I32, C.POINTER(MgLayout), V, C.POINTER(MgBatch),
                     V, V],
+    "hg_mg_build_n": [V, V, I64, V, I32, V, V, I32, C.POINTER(MgLayout), V, C.POINTER(MgBatch),
+                      V, V],
     "hg_train_step": [C.POINTER(StepDesc), I32, V],
     "hg_forward": [C.POINTER(StepDesc), I32, V],
     "hg_sgd_update": [V, V, V, I64, C.c_float, C.c_float, V],
@@ -111,6 +114,7 @@ SIGNATURES = {
     "hg_allreduce_sgd": [V, V, V, I64, C.c_float, C.c_float, V],
     "hg_shift": [V, C.c_int, C.c_int, C.c_int, V, V, V, V, I64, V],
     "hg_pregather_peer": [V, V, V, I32, V, V, I32, V, V, V, V, I32, V, V, V, V, V],
+    "hg_pregather_peer_at": [V, V, V, I32, V, V, I32, V, V, V, V, I32, V, V, V, I32, V, V, V],
     "hg_step_prologue": [C.POINTER(StepDesc), I32, I32, V],
     "hg_debug_build_phases": [C.POINTER(C.c_longlong), C.c_int],
 }

@@ -254,12 +254,19 @@ k_gemm(const TA* __restrict__ A, int lda, const float* __restrict__ B, int ldb, 
 // warp per root: softmax-CE on the root logits (model.py:253-259); logits are
 // overwritten with dlogits = softmax - onehot(label).
 __global__ void k_softmax_ce(float* __restrict__ logits, int C, const int64_t* __restrict__ roots,
-                             int n_roots, uint64_t label_state, float* __restrict__ loss,
-                             bf16* __restrict__ dl_lowp, int ldp) {
+                             int n_roots, const int32_t* __restrict__ n_dev, uint64_t label_state,
+                             float* __restrict__ loss, bf16* __restrict__ dl_lowp, int ldp) {
   const int r = blockIdx.x * (blockDim.x / 32) + warp_id();
   if (r >= n_roots) return;
   const int lane = lane_id();
   float* x = logits + (int64_t)r * C;
+  if (n_dev && r >= *n_dev) {  // capacity rows past the device root count: no loss, no gradient
+    for (int c = lane; c < C; c += 32) x[c] = 0.f;
+    if (dl_lowp)
+      for (int c = lane; c < ldp; c += 32) dl_lowp[(int64_t)r * ldp + c] = __float2bfloat16_rn(0.f);
+    if (lane == 0) loss[r] = 0.f;
+    return;
+  }
   float mx = -INFINITY;
   for (int c = lane; c < C; c += 32) mx = fmaxf(mx, x[c]);
 #pragma unroll
@@ -303,10 +310,15 @@ __global__ void k_pad_bf16(const float* __restrict__ W, int rows, int cols, bf16
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_head(const T* __restrict__ hL, const float* __restrict__ Wc, int H, int C,
-       const int64_t* __restrict__ roots, int n_roots, uint64_t label_state,
-       float* __restrict__ dlogits, float* __restrict__ loss, float* __restrict__ dz,
-       bf16* __restrict__ dz_lowp, int cap_rows, float* __restrict__ gb, int backward) {
+       const int64_t* __restrict__ roots, int n_cap, const int32_t* __restrict__ n_dev,
+       uint64_t label_state, float* __restrict__ dlogits, float* __restrict__ loss,
+       float* __restrict__ dz, bf16* __restrict__ dz_lowp, int cap_rows, float* __restrict__ gb,
+       int backward) {
   extern __shared__ float sm[];
+  const int n_roots = n_dev ? *n_dev : n_cap;
+  for (int i = n_roots + blockIdx.x * blockDim.x + threadIdx.x; i < n_cap;
+       i += gridDim.x * blockDim.x)
+    loss[i] = 0.f;  // capacity rows past the device root count
   const int pitch = C | 1;
   float* ws = sm;                                   // [H][pitch]
   float* gbs = ws + (size_t)H * pitch;              // [H]
@@ -702,17 +714,18 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
       k_transpose_bf16<<<g, b, 0, s>>>(d->Wc, H, C, (bf16*)d->WcT, nullptr);
       k_pad_bf16<<<64, 256, 0, s>>>(d->Wc, H, C, (bf16*)d->Wcp, Cp);
     }
+    // root rows: n_roots is the capacity, the device count N_L the actual roots
     int st = umma_gemm(d->h[L], H, false, d->WcT, H, false, d->logits, C, n_roots, C, H,
-                       nullptr, nullptr, 0, nullptr, 1, s);
+                       tot + L, nullptr, 0, nullptr, 1, s);
     if (st) return st;
     count_launch();
-    k_softmax_ce<<<(n_roots + 7) / 8, 256, 0, s>>>(d->logits, C, d->roots, n_roots,
+    k_softmax_ce<<<(n_roots + 7) / 8, 256, 0, s>>>(d->logits, C, d->roots, n_roots, tot + L,
                                                    d->label_state, d->loss,
                                                    (bf16*)d->dl_lowp, Cp);
     if (backward) {
       // dz_L = (dlogits @ W_cᵀ) * (h_L > 0); gb_L; bf16 dz_L for the dW GEMM
       st = umma_gemm(d->dl_lowp, Cp, false, d->Wcp, Cp, false, d->dh[L], H, n_roots, H, Cp,
-                     nullptr, nullptr, 0, nullptr, 1, s);
+                     tot + L, nullptr, 0, nullptr, 1, s);
       if (st) return st;
       dim3 g((H + 31) / 32, 16);
       count_launch();
@@ -721,7 +734,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
       // gW_c += h_Lᵀ dlogits (both MN-major, reduction over the roots)
       const int split = std::max(1, std::min(16, n_roots / 256));
       st = umma_gemm(d->h[L], H, true, d->dl_lowp, Cp, true, d->gWc, C, H, C, n_roots,
-                     nullptr, nullptr, 2, nullptr, split, s);
+                     nullptr, tot + L, 2, nullptr, split, s);
       if (st) return st;
     }
   } else {
@@ -734,7 +747,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     const int grid = std::max(1, std::min(num_sms(), (n_roots + 7) / 8));
     count_launch();
     k_head<T><<<grid, 256, smem, s>>>((const T*)d->h[L], d->Wc, H, C, d->roots, n_roots,
-                                      d->label_state, d->logits, d->loss, d->dh[L],
+                                      tot + L, d->label_state, d->logits, d->loss, d->dh[L],
                                       tc ? (bf16*)d->lowp_scratch : nullptr, d->max_rows[L],
                                       d->gb[L], backward ? 1 : 0);
   }
@@ -744,7 +757,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
   // gWc += h_L^T dlogits
   if (!tc_head)
     gemm<T, true, false, EPI_ATOMIC, float, T>(s, (const T*)d->h[L], H, d->logits, C, d->gWc, C,
-                                               nullptr, H, C, nullptr, n_roots, nullptr, nullptr,
+                                               nullptr, H, C, tot + L, n_roots, nullptr, nullptr,
                                                0, split_r);
   for (int k = L; k >= 1; --k) {
     // gW_k += agg_k^T dz_k   (reduction over the N_k rows, split across CTAs)

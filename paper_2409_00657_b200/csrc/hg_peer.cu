@@ -52,8 +52,10 @@ __global__ void k_stage_mark(const int32_t* __restrict__ ids, const int32_t* __r
                              uint32_t* __restrict__ bitmap, int32_t* __restrict__ stage_list,
                              int32_t* __restrict__ stage_row, int32_t* __restrict__ stage_count,
                              int stage_cap, unsigned long long* __restrict__ uniq_per_home,
-                             unsigned long long* __restrict__ total_remote, int* err) {
+                             unsigned long long* __restrict__ total_remote, int* err,
+                             const int64_t* __restrict__ it_dev, int row_stride) {
   const int n = *n_dev;
+  if (uniq_per_home && it_dev) uniq_per_home += *it_dev * row_stride;
   unsigned long long mine = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int v = ids[i];
@@ -112,23 +114,36 @@ k_stage_copy(const int32_t* __restrict__ stage_list, const int32_t* __restrict__
 
 using namespace hg;
 
+extern "C" int hg_pregather_peer_at(const int32_t* ids, const int32_t* n_dev, const int32_t* home,
+                                    int32_t rank, const int32_t* local_row, const void* peers,
+                                    int32_t row_bytes, uint32_t* bitmap, int32_t* stage_list,
+                                    int32_t* stage_row, int32_t* stage_count, int32_t stage_cap,
+                                    void* staging, unsigned long long* uniq_per_home,
+                                    const int64_t* it_dev, int32_t row_stride,
+                                    unsigned long long* total_remote, int* err, void* stream) {
+  if (row_bytes % 16) return hg_fail(HG_ECONFIG, "row bytes must be a multiple of 16");
+  cudaStream_t s = (cudaStream_t)stream;
+  HG_CUDA_TRY(cudaMemsetAsync(stage_count, 0, sizeof(int32_t), s));
+  count_launch(3);
+  k_stage_mark<<<148 * 2, 256, 0, s>>>(ids, n_dev, home, rank, bitmap, stage_list, stage_row,
+                                       stage_count, stage_cap, uniq_per_home, total_remote, err,
+                                       it_dev, row_stride);
+  k_stage_copy<<<148 * 4, 256, 0, s>>>(stage_list, stage_count, stage_cap, home, local_row,
+                                       (const uint8_t* const*)peers, row_bytes, (uint8_t*)staging);
+  k_remote_clear<<<148 * 2, 256, 0, s>>>(ids, n_dev, 0, bitmap);
+  HG_CUDA_TRY(cudaGetLastError());
+  return HG_OK;
+}
+
 extern "C" int hg_pregather_peer(const int32_t* ids, const int32_t* n_dev, const int32_t* home,
                                  int32_t rank, const int32_t* local_row, const void* peers,
                                  int32_t row_bytes, uint32_t* bitmap, int32_t* stage_list,
                                  int32_t* stage_row, int32_t* stage_count, int32_t stage_cap,
                                  void* staging, unsigned long long* uniq_per_home,
                                  unsigned long long* total_remote, int* err, void* stream) {
-  if (row_bytes % 16) return hg_fail(HG_ECONFIG, "row bytes must be a multiple of 16");
-  cudaStream_t s = (cudaStream_t)stream;
-  HG_CUDA_TRY(cudaMemsetAsync(stage_count, 0, sizeof(int32_t), s));
-  count_launch(3);
-  k_stage_mark<<<148 * 2, 256, 0, s>>>(ids, n_dev, home, rank, bitmap, stage_list, stage_row,
-                                       stage_count, stage_cap, uniq_per_home, total_remote, err);
-  k_stage_copy<<<148 * 4, 256, 0, s>>>(stage_list, stage_count, stage_cap, home, local_row,
-                                       (const uint8_t* const*)peers, row_bytes, (uint8_t*)staging);
-  k_remote_clear<<<148 * 2, 256, 0, s>>>(ids, n_dev, 0, bitmap);
-  HG_CUDA_TRY(cudaGetLastError());
-  return HG_OK;
+  return hg_pregather_peer_at(ids, n_dev, home, rank, local_row, peers, row_bytes, bitmap,
+                              stage_list, stage_row, stage_count, stage_cap, staging,
+                              uniq_per_home, nullptr, 0, total_remote, err, stream);
 }
 
 extern "C" int hg_alloc(size_t bytes, void** out) {

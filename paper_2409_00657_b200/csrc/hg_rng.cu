@@ -135,6 +135,42 @@ extern "C" int hg_iter_stage(const int64_t* perm, const uint64_t* states, int64_
   return HG_OK;
 }
 
+__global__ void k_iter_stage_ranged(const int64_t* __restrict__ roots,
+                                    const int64_t* __restrict__ ranges,
+                                    const uint64_t* __restrict__ states, int64_t iters,
+                                    int64_t* it_dev, int cap, int ahead, int advance,
+                                    int64_t* __restrict__ roots_out, int32_t* n_out,
+                                    uint64_t* __restrict__ key_out) {
+  const int64_t it = *it_dev + ahead;
+  if (it < iters) {
+    const int64_t lo = ranges[2 * it];
+    const int n = (int)min((int64_t)cap, ranges[2 * it + 1] - lo);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) roots_out[i] = roots[lo + i];
+    if (threadIdx.x == 0) {
+      *n_out = n;
+      key_out[0] = states[it];
+    }
+  } else if (threadIdx.x == 0) {
+    *n_out = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && advance) *it_dev += advance;
+}
+
+extern "C" int hg_iter_stage_ranged(const int64_t* roots, const int64_t* ranges,
+                                    const uint64_t* states, int64_t iters, int64_t* it_dev,
+                                    int32_t cap, int32_t ahead, int32_t advance,
+                                    int64_t* roots_out, int32_t* n_out, uint64_t* key_out,
+                                    void* stream) {
+  if (cap < 0) return hg_fail(HG_ERANGE, "bad capacity");
+  count_launch();
+  k_iter_stage_ranged<<<1, 1024, 0, (cudaStream_t)stream>>>(roots, ranges, states, iters, it_dev,
+                                                             cap, ahead, advance, roots_out,
+                                                             n_out, key_out);
+  HG_CUDA_TRY(cudaGetLastError());
+  return HG_OK;
+}
+
 extern "C" int hg_glorot(int32_t rows, int32_t cols, uint64_t state, int32_t dtype, void* out,
                          void* stream) {
   const int64_t total = (int64_t)rows * cols;

@@ -425,11 +425,16 @@ __global__ void __launch_bounds__(kBuildThreads, 4)
 k_mg_build(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targets,
            int64_t n_vertices, const int64_t* __restrict__ roots, int n_roots,
            const uint64_t* __restrict__ iter_state, int roots_per_state, MgCarve c,
-           int32_t* __restrict__ ws, int* err) {
+           int32_t* __restrict__ ws, int* err, const int32_t* __restrict__ n_roots_dev) {
   extern __shared__ __align__(16) int sm[];
   const int r = blockIdx.x;
   if (r >= n_roots) return;
   const int L = c.L;
+  if (n_roots_dev && r >= *n_roots_dev) {  // beyond the device count: an empty micrograph
+    int32_t* w = ws + (size_t)r * c.ws_root_ints;
+    if (threadIdx.x <= 2 * L) w[c.ws_cnt + threadIdx.x] = 0;
+    return;
+  }
   int* scan = sm + c.sm_scan;
   __shared__ int warp_ctr[kBuildWarps + 1];
   __shared__ uint64_t tslots[kBuildWarps + 1];
@@ -720,6 +725,15 @@ extern "C" int hg_mg_build(const int64_t* offsets, const int32_t* targets, int64
                            const int64_t* roots, int32_t n_roots, const uint64_t* iter_state,
                            int32_t roots_per_state, const hg_mg_layout* layout, int32_t* ws,
                            hg_mg_batch* out, int* err_flag, void* stream) {
+  return hg_mg_build_n(offsets, targets, n_vertices, roots, n_roots, nullptr, iter_state,
+                       roots_per_state, layout, ws, out, err_flag, stream);
+}
+
+extern "C" int hg_mg_build_n(const int64_t* offsets, const int32_t* targets, int64_t n_vertices,
+                             const int64_t* roots, int32_t n_roots, const int32_t* n_roots_dev,
+                             const uint64_t* iter_state, int32_t roots_per_state,
+                             const hg_mg_layout* layout, int32_t* ws, hg_mg_batch* out,
+                             int* err_flag, void* stream) {
   if (n_roots < 0 || roots_per_state < 0) return hg_fail(HG_ERANGE, "bad root count");
   MgCarve c;
   int st = make_carve(layout->n_layers, layout->fanout, &c);
@@ -732,7 +746,7 @@ extern "C" int hg_mg_build(const int64_t* offsets, const int32_t* targets, int64
   prof_begin(PROF_BUILD, s);
   k_mg_build<<<n_roots, kBuildThreads, c.smem_bytes, s>>>(offsets, targets, n_vertices, roots,
                                                           n_roots, iter_state, roots_per_state,
-                                                          c, ws, err_flag);
+                                                          c, ws, err_flag, n_roots_dev);
   HG_CUDA_TRY(cudaGetLastError());
   k_mg_scan<<<1, 1024, 0, s>>>(ws, n_roots, c, *out);
   HG_CUDA_TRY(cudaGetLastError());

@@ -331,6 +331,74 @@ class PeerFeatures:
         self.opened = []
 
 
+# ---------------------------------------------------------------- graph loop
+
+class DistGraphLoop:
+    """CUDA-graph replay of the multi-GPU fast path (fused mode, initial trace
+    table, NVLink device pre-gather).  Like engine.GraphLoop, two graphs
+    alternate runners; the forked branch stages this rank's roots of the next
+    iteration from a device cursor (hg_iter_stage_ranged: variable count, at
+    most `cap`), builds them (device root count), pre-gathers their remote rows
+    over NVLink (per-iteration ledger row chosen by the cursor) and runs the
+    layer-1 gather; the main branch trains the current runner, copies the
+    summed loss to a pinned slot, and runs the NCCL all-reduce + SGD.  Root
+    count capacity `cap` pads with empty micrographs, which contribute
+    nothing (zero loss rows and gradients)."""
+
+    def __init__(self, tr: "MicrographTrainer", cap: int):
+        self.tr, self.cap = tr, int(cap)
+        dev = tr.device
+        self.runners = tr.runners[:2]
+        self.side = torch.cuda.Stream(dev)
+        self.pin_loss = [torch.zeros(1, dtype=torch.float32).pin_memory() for _ in range(2)]
+        m = tr.model
+        total = tr.S * tr.B
+        self.graphs = []
+        cur = torch.cuda.current_stream(dev)
+        before = _lib.launch_count()
+        for x in range(2):
+            run, nxt = self.runners[x], self.runners[1 - x]
+            g = torch.cuda.CUDAGraph()
+            cap_s = torch.cuda.Stream(dev)
+            cap_s.wait_stream(cur)
+            with torch.cuda.graph(g, stream=cap_s):
+                self.side.wait_stream(cap_s)
+                with torch.cuda.stream(self.side):
+                    self.side_ops(nxt, self.side.cuda_stream)
+                cs = cap_s.cuda_stream
+                _lib.call("hg_train_step", C.byref(run.desc), self.cap, cs)
+                self.pin_loss[x].copy_(run.loss[:self.cap].sum().reshape(1), non_blocking=True)
+                _lib.call("hg_allreduce_sgd", tr._comm, m.flat.data_ptr(), m.grad.data_ptr(),
+                          m.flat.numel(), float(tr.lr), 1.0 / total, cs)
+                cap_s.wait_stream(self.side)
+            cur.wait_stream(cap_s)
+            self.graphs.append(g)
+        self.launches = (_lib.launch_count() - before) // 2
+        self.iters = tr.iters
+
+    def side_ops(self, r: CellRunner, s) -> None:
+        """Stage (cursor -> cursor + 1), build, pre-gather and layer-1 gather of
+        the iteration after the cursor into runner r."""
+        tr = self.tr
+        _lib.call("hg_iter_stage_ranged", tr._g_roots.data_ptr(), tr._g_ranges.data_ptr(),
+                  tr._g_states.data_ptr(), tr.iters, tr._g_it.data_ptr(), self.cap, 1, 1,
+                  r.roots.data_ptr(), r.n_dev.data_ptr(), r.keys.data_ptr(), s)
+        r.builder.build(tr.graph, r.roots.data_ptr(), r.keys.data_ptr(), self.cap,
+                        n_roots=self.cap, stream=s, n_dev=r.n_dev.data_ptr())
+        f = tr.feats
+        t = r.builder.tensors
+        _lib.call("hg_pregather_peer_at", t["need_ids"][0].data_ptr(), t["totals"].data_ptr(),
+                  f.home.data_ptr(), f.rank, f.local_row.data_ptr(), f.peers.data_ptr(),
+                  f.ld * f.staging.element_size(), f.bitmap.data_ptr(), f.stage_list.data_ptr(),
+                  f.stage_row.data_ptr(), f.stage_count.data_ptr(), f.stage_cap,
+                  f.staging.data_ptr(), tr._acct_rows.data_ptr(), tr._g_it.data_ptr(), tr.S,
+                  tr._acct_total.data_ptr(), f.err.data_ptr(), s)
+        _lib.call("hg_step_prologue", C.byref(r.desc), self.cap, 1, s)
+
+    def replay(self, x: int) -> None:
+        self.graphs[x].replay()
+
+
 # ---------------------------------------------------------------- trainer
 
 class MicrographTrainer:
@@ -339,7 +407,7 @@ class MicrographTrainer:
     def __init__(self, graph: Graph, part: PartitionMap, model: ModelState, fanout, batch: int,
                  seed: int, lr: float = 0.1, dtype=torch.bfloat16, mode: str = "fused",
                  iterations: int = 0, group=None, use_tc: bool = True, pregather: bool = True,
-                 strategy: str = "micrograph"):
+                 strategy: str = "micrograph", graphs: bool = True):
         """strategy="micrograph": HopGNN feature-centric training (engine.py:562-623);
         "model-centric": the baseline it is measured against (engine.py:482-507) --
         GPU d trains all of batch d, fetching every remote row its micrographs
@@ -355,6 +423,10 @@ class MicrographTrainer:
             mode = "fused"  # one cell per GPU, nothing to hop
         self.strategy = strategy
         self.pregather = pregather
+        self.graphs = graphs
+        self._dgl = None       # DistGraphLoop
+        self._gnext = None     # iteration the graph loop is positioned at
+        self._eager_fast = 0   # eager fast-path steps taken (library warm-up before capture)
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.S = part.n_servers
@@ -383,6 +455,9 @@ class MicrographTrainer:
             table = FeatureTable(1, model.D, dtype, self.device, model.Dp)  # shape carrier
         self.runners = [CellRunner(graph, table, model, self.fanout, cap_roots,
                                    self.labels, use_tc=use_tc) for _ in range(n_runners)]
+        # load the loss-sum reduction kernel now (lazy module loading costs ~10 ms
+        # on its first launch, which would otherwise land inside a timed step)
+        self.runners[0].loss[:1].sum().item()
         if not pregather:
             for r in self.runners:
                 self.feats.bind(r)
@@ -426,7 +501,99 @@ class MicrographTrainer:
         self.epoch = epoch
         self.iters = iterations_per_epoch(n, self.S, self.B, self.iter_cap)
         self._plan_epoch()
+        if self._graph_eligible():
+            self._graph_epoch_plan()
         return self.iters
+
+    # ------------------------------------------------------------ graph loop
+    def _graph_eligible(self) -> bool:
+        return (self.graphs and self.S > 1 and self.mode == "fused" and not self.pregather
+                and self._comm_ok and self._comm is not None)
+
+    def _graph_epoch_plan(self) -> None:
+        """Device copies of this epoch's root ranges / stream states for the graph
+        loop's cursor, at fixed addresses (captured once)."""
+        S, B, it_n = self.S, self.B, self.iters
+        its = np.arange(it_n, dtype=np.int64)
+        if self.strategy == "model-centric":
+            roots = self.perm
+            lo = (its * S + self.rank) * B
+            ranges = np.stack([lo, lo + B], axis=1)
+            cap = B
+        else:
+            roots = self._my_roots
+            b = np.asarray(self._my_bounds, dtype=np.int64)
+            ranges = np.stack([b[:-1], b[1:]], axis=1)
+            cap = int((ranges[:, 1] - ranges[:, 0]).max()) if it_n else 1
+            cap = min(-(-max(cap, 1) // 64) * 64, self.runners[0].max_roots)
+        states = hash_vec(chain(self.sampler_seed, self.epoch), its).view(np.int64)
+        dev = self.device
+        fresh = (not hasattr(self, "_g_roots") or self._g_roots.numel() != len(roots)
+                 or self._g_ranges.shape[0] != it_n)
+        if fresh:
+            self._g_roots = torch.empty(len(roots), dtype=torch.int64, device=dev)
+            self._g_ranges = torch.empty((it_n, 2), dtype=torch.int64, device=dev)
+            self._g_states = torch.empty(it_n, dtype=torch.int64, device=dev)
+            self._g_it = torch.zeros(1, dtype=torch.int64, device=dev)
+            self._dgl = None
+        self._g_roots.copy_(torch.from_numpy(np.ascontiguousarray(roots)))
+        self._g_ranges.copy_(torch.from_numpy(np.ascontiguousarray(ranges)))
+        self._g_states.copy_(torch.from_numpy(np.ascontiguousarray(states)))
+        if self._dgl is not None and (self._dgl.cap < cap or self._dgl.iters != it_n):
+            self._dgl = None
+        self._g_cap = cap if self._dgl is None else self._dgl.cap
+        self._acct_row_ptr(it_n - 1)
+        self._gnext = None
+
+    def _graph_loop(self):
+        if self._dgl is None:
+            if self._eager_fast < 2 or not hasattr(self, "_ra"):
+                return None
+            self._drain_run_ahead()
+            for r in self.runners[:2]:
+                r.desc.roots = r.roots.data_ptr()
+                r.desc.agg1_ready = 1
+                self.feats.bind_staged(r, self._stage_cap)
+            self._dgl = DistGraphLoop(self, self._g_cap)
+        return self._dgl
+
+    def _drain_run_ahead(self) -> None:
+        if hasattr(self, "_ra"):
+            self._ra.side.wait_stream(torch.cuda.current_stream(self.device))
+            self._ra.reset()
+
+    def _step_graph(self, gl: DistGraphLoop, it: int, want_loss: bool):
+        x = it % 2
+        if self._gnext != it:  # position the loop: build `it` eagerly into runner x
+            self._drain_run_ahead()
+            for r in gl.runners:  # the general cell path may have rebound these
+                r.desc.roots = r.roots.data_ptr()
+                r.desc.agg1_ready = 1
+                self.feats.bind_staged(r, self._stage_cap)
+            # an eager run-ahead build of `it` may already have charged its ledger row
+            self._acct_rows[it].zero_()
+            self._g_it.fill_(it - 1)
+            gl.side_ops(gl.runners[x], torch.cuda.current_stream(self.device).cuda_stream)
+            self._acct_iters = getattr(self, "_acct_iters", set())
+            self._acct_iters.add(it)
+        prev = None
+        # pin slot x was written by the replay two steps back: read it before reuse
+        if self._loss_pending and self._loss_pending[0][1] is gl.pin_loss[x]:
+            prev = self._drain_loss()
+        gl.replay(x)  # trains `it`, builds + pre-gathers it+1, all-reduce + SGD
+        ev = torch.cuda.Event()
+        ev.record()
+        self._loss_pending.append((ev, gl.pin_loss[x]))
+        if want_loss and prev is None and len(self._loss_pending) > 2:
+            prev = self._drain_loss()
+        if not want_loss:
+            prev = None
+        self._acct_iters = getattr(self, "_acct_iters", set())
+        self._acct_iters.add(it + 1)
+        self._fast_iters = getattr(self, "_fast_iters", 0) + 1
+        self.traffic.allreduce_bytes += 2.0 * (self.S - 1) / self.S * self.flat_bytes
+        self._gnext = it + 1
+        return prev
 
     def batches(self, it: int):
         n = len(self.perm)
@@ -548,6 +715,13 @@ class MicrographTrainer:
         of it reads remote rows over NVLink, then all-reduce + SGD in C."""
         S = self.S
         s = torch.cuda.current_stream(self.device).cuda_stream
+        self._eager_fast += 1
+        if self._gnext is not None:
+            if self._gnext == it and self._dgl is not None:
+                # the graph loop already built `it` into runner it%2: train it here
+                return self._train_built(self._dgl.runners[it % 2], it, want_loss)
+            self._drain_run_ahead()
+            self._gnext = None
         if self.pregather:  # staging exchange needs host-known sizes: no run-ahead
             r = self.runners[0]
             self._fast_build(it)(r, s)
@@ -577,7 +751,7 @@ class MicrographTrainer:
                 # values are read two steps late so the host never stalls the queue
                 if len(self._loss_pending) >= 2:
                     prev = self._drain_loss()
-                self._loss_pending.append((ev, self._loss_slot))
+                self._loss_pending.append((ev, self._loss_pin[self._loss_slot]))
         self._fast_iters = getattr(self, "_fast_iters", 0) + 1
         total = S * self.B
         m = self.model
@@ -591,13 +765,36 @@ class MicrographTrainer:
             self.traffic.allreduce_bytes += 2.0 * (S - 1) / S * self.flat_bytes
         return prev
 
+    def _train_built(self, r: CellRunner, it: int, want_loss: bool):
+        """Eagerly train a runner the graph loop built (the epoch's last iteration)."""
+        self._gnext = None
+        self._drain_run_ahead()
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        cap = self._dgl.cap
+        _lib.call("hg_train_step", C.byref(r.desc), cap, s)
+        prev = None
+        if want_loss:
+            self._loss_slot = (self._loss_slot + 1) % 4
+            self._loss_pin[self._loss_slot].copy_(r.loss[:cap].sum().reshape(1), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            if len(self._loss_pending) >= 2:
+                prev = self._drain_loss()
+            self._loss_pending.append((ev, self._loss_pin[self._loss_slot]))
+        m = self.model
+        _lib.call("hg_allreduce_sgd", self._comm, m.flat.data_ptr(), m.grad.data_ptr(),
+                  m.flat.numel(), float(self.lr), 1.0 / (self.S * self.B), s)
+        self._fast_iters = getattr(self, "_fast_iters", 0) + 1
+        self.traffic.allreduce_bytes += 2.0 * (self.S - 1) / self.S * self.flat_bytes
+        return prev
+
     def _drain_loss(self):
         pend = getattr(self, "_loss_pending", None)
         if not pend:
             return None
-        ev, slot = pend.pop(0)
+        ev, buf = pend.pop(0)
         ev.synchronize()
-        return float(self._loss_pin[slot].item())
+        return float(buf.item())
 
     def last_loss(self):
         """Drain every pending step loss; returns the most recent (host sync)."""
@@ -612,6 +809,10 @@ class MicrographTrainer:
         (a host sync) or None when want_loss is False."""
         if (self.mode == "fused" and (not self.table.removed or self.strategy == "model-centric")
                 and self._comm_ok and len(self.perm) >= (it + 1) * self.S * self.B):
+            if self._graph_eligible() and hasattr(self, "_g_roots") and it + 1 < self.iters:
+                gl = self._graph_loop()
+                if gl is not None:
+                    return self._step_graph(gl, it, want_loss)
             return self._step_fast(it, want_loss)
         S, rank = self.S, self.rank
         batches = self.batches(it)

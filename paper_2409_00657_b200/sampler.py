@@ -202,7 +202,7 @@ class MicrographBuilder:
         self.cbatch.totals = t["totals"].data_ptr()
 
     def build(self, g: Graph, roots: torch.Tensor, keys: torch.Tensor, roots_per_state: int,
-              n_roots: int = None, stream=None) -> MicrographBatch:
+              n_roots: int = None, stream=None, n_dev: int = None) -> MicrographBatch:
         """Launch sampling + build.  keys: uint64 (as int64) iteration states, or
         per-root final keys when roots_per_state == 0."""
         n = roots.numel() if n_roots is None else int(n_roots)
@@ -211,6 +211,11 @@ class MicrographBuilder:
         s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
         rp = roots if isinstance(roots, int) else roots.data_ptr()
         kp = keys if isinstance(keys, int) else keys.data_ptr()
+        if n_dev is not None:  # n is the capacity; the device count says how many are real
+            _lib.call("hg_mg_build_n", g.offsets.data_ptr(), g.targets.data_ptr(), g.n_vertices,
+                      rp, n, n_dev, kp, int(roots_per_state), C.byref(self.layout),
+                      self.ws.data_ptr(), C.byref(self.cbatch), self.err.data_ptr(), s)
+            return MicrographBatch(self.L, n, self.tensors)
         _lib.call("hg_mg_build", g.offsets.data_ptr(), g.targets.data_ptr(), g.n_vertices,
                   rp, n, kp, int(roots_per_state),
                   C.byref(self.layout), self.ws.data_ptr(), C.byref(self.cbatch),

@@ -90,6 +90,7 @@ class CellRunner:
         d.WcT, d.Wcp, d.dl_lowp = self.wct.data_ptr(), self.wcp.data_ptr(), self.dl16.data_ptr()
         self.desc = d
         self.n_roots = 0
+        self.n_dev = torch.zeros(1, dtype=torch.int32, device=dev)  # device root count (graphs)
 
     def stage_roots(self, roots, keys, roots_per_state: int) -> None:
         """Copy roots (int64) and iteration states / keys into the fixed buffers."""

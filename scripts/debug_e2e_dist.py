@@ -42,8 +42,11 @@ def loop(K, want):
     return t / K * 1e3, float(np.median(hs)) * 1e3, float(np.max(hs)) * 1e3, (h1 - t0) / K * 1e3
 loop(10, False)
 res = {}
-for name, want in (("noloss", False), ("loss", True), ("noloss2", False), ("loss2", True)):
-    res[name] = [round(x, 4) for x in loop(40, want)]
+res["noloss"] = [round(x, 4) for x in loop(30, False)]
+tr.flush_accounting()
+tr.global_ledger()
+res["loss_after_ledger"] = [round(x, 4) for x in loop(30, True)]
+res["loss2"] = [round(x, 4) for x in loop(30, True)]
 print(rank, json.dumps(res), flush=True)
 dist.barrier()
 dist.destroy_process_group()

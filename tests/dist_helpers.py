@@ -60,7 +60,7 @@ def pregather_worker(rank, world, init_file, result_file):
 
 
 def micrograph_worker(rank, world, init_file, result_file, mode, dtype_name, feat_mode="pg",
-                      strategy="micrograph"):
+                      strategy="micrograph", iters=3):
     """Full multi-GPU micrograph (or model-centric) iterations vs the oracle
     engine (ledger exact, parameters within tolerance)."""
     import json
@@ -73,7 +73,7 @@ def micrograph_worker(rank, world, init_file, result_file, mode, dtype_name, fea
     from paper_2409_00657_b200.distributed import MicrographTrainer
     from paper_2409_00657_b200.graph import Graph, PartitionMap
     from paper_2409_00657_b200.model import init_model
-    seed, arch, fo, D, H, C, B, iters = 3, "sage-mean", (15, 10), 16, 64, 5, 64, 3
+    seed, arch, fo, D, H, C, B = 3, "sage-mean", (15, 10), 16, 64, 5, 64
     off, tgt = build_csr(build_tables(OSpec(n=3000, avg_deg=12.0, beta=0.7, p_in=0.9,
                                             n_blocks=4, d_cap=600, seed=11)))
     home = (keyed(chain(seed, 0x02, 0xA7), np.arange(3000)) % np.uint64(world)).astype(np.int64)
@@ -86,6 +86,7 @@ def micrograph_worker(rank, world, init_file, result_file, mode, dtype_name, fea
     tr.begin_epoch(0)
     losses = [tr.step(it) for it in range(tr.iters)]
     torch.cuda.synchronize()
+    graph_used = tr._dgl is not None
     led = tr.global_ledger()
     params = [p.tolist() for p in model.params()]
     out = {"ok": True, "msg": ""}
@@ -101,6 +102,7 @@ def micrograph_worker(rank, world, init_file, result_file, mode, dtype_name, fea
                                         oled)
         out = _compare(led, oled, model, P, dtype_name)
         out["losses"] = losses
+        out["graph_used"] = graph_used
     with open(f"{result_file}.{rank}", "w") as f:
         json.dump(out, f)
     dist.barrier()

@@ -62,3 +62,19 @@ def test_merge_controller_matches_oracle(feat):
              nprocs=world, join=True)
     res = json.load(open(os.path.join(d, "res.0")))
     assert res["ok"], res["msg"]
+
+
+@pytest.mark.parametrize("strategy", ["micrograph", "model-centric"])
+def test_graph_loop_matches_oracle(strategy):
+    """Enough iterations for the CUDA-graph loop (DistGraphLoop) to engage:
+    device root counts, cursor-staged roots, cursor-indexed ledger rows."""
+    import dist_helpers
+    world = _world()
+    d = tempfile.mkdtemp()
+    mp.spawn(dist_helpers.micrograph_worker,
+             args=(world, os.path.join(d, "init"), os.path.join(d, "res"), "fused", "f32", "peer",
+                   strategy, 7),
+             nprocs=world, join=True)
+    res = json.load(open(os.path.join(d, "res.0")))
+    assert res["ok"], res["msg"]
+    assert res["graph_used"], "graph loop never engaged"
