@@ -431,7 +431,10 @@ def run_distributed(args, cfg):
     if rank == 0:
         for name, site in (("build", _lib.PROF_BUILD), ("agg1", _lib.PROF_AGG1),
                            ("gemm1", _lib.PROF_GEMM1), ("dw1", _lib.PROF_DW1),
-                           ("step", _lib.PROF_STEP), ("sgd", _lib.PROF_SGD)):
+                           ("step", _lib.PROF_STEP), ("sgd", _lib.PROF_SGD),
+                           ("pregather_mark", _lib.PROF_PG_MARK),
+                           ("pregather_copy", _lib.PROF_PG_COPY),
+                           ("pregather_clear", _lib.PROF_PG_CLEAR)):
             t, c = _lib.prof_read(site)
             sites[name] = round(t / max(c, 1), 4)
         _lib.prof_enable(False)

@@ -294,6 +294,22 @@ int hg_pregather_peer_at(const int32_t* ids, const int32_t* n_dev, const int32_t
                          void* staging, unsigned long long* uniq_per_home, const int64_t* it_dev,
                          int32_t row_stride, unsigned long long* total_remote, int* err,
                          void* stream);
+/* Push variant (NVLink, owner-side gather): the requester dedups its remote
+ * vertices into its mailbox list (slot i -> staging row i of its mailbox,
+ * stage_row[v] = i), signals its peers, and every owner copies the rows
+ * homed on it from its local shard into the requesters' staging rows over
+ * NVLink; returns (stream order) once every peer has signalled completion.
+ * All ranks must call it the same number of times.  boxes: device array of
+ * the S mailbox base addresses (own + IPC-mapped peers); layout offsets in
+ * bytes; seq: device int64 sequence counter (starts at 0). */
+int hg_pregather_push(const int32_t* ids, const int32_t* n_dev, const int32_t* home, int32_t rank,
+                      int32_t n_ranks, const int32_t* local_row, const void* shard,
+                      int32_t row_bytes, uint32_t* bitmap, int32_t* stage_row, int32_t stage_cap,
+                      const void* boxes, void* own_box, int64_t o_flags, int64_t o_done,
+                      int64_t o_count, int64_t o_list, int64_t o_staging,
+                      unsigned long long* uniq_per_home, const int64_t* it_dev,
+                      int32_t row_stride, unsigned long long* total_remote, int64_t* seq,
+                      int* err, void* stream);
 /* Parameter-independent prologue of a step: the layer-1 gather + aggregate
  * (sets up agg[1]; run ahead of the previous iteration's training). */
 int hg_step_prologue(const hg_step_desc* d, int32_t n_roots, int32_t backward, void* stream);

@@ -115,6 +115,8 @@ SIGNATURES = {
     "hg_shift": [V, C.c_int, C.c_int, C.c_int, V, V, V, V, I64, V],
     "hg_pregather_peer": [V, V, V, I32, V, V, I32, V, V, V, V, I32, V, V, V, V, V],
     "hg_pregather_peer_at": [V, V, V, I32, V, V, I32, V, V, V, V, I32, V, V, V, I32, V, V, V],
+    "hg_pregather_push": [V, V, V, I32, I32, V, V, I32, V, V, I32, V, V, I64, I64, I64, I64, I64,
+                          V, V, I32, V, V, V, V],
     "hg_step_prologue": [C.POINTER(StepDesc), I32, I32, V],
     "hg_debug_build_phases": [C.POINTER(C.c_longlong), C.c_int],
 }
@@ -186,4 +188,5 @@ def prof_read(site: int):
     return t.value, n.value
 
 
-PROF_BUILD, PROF_AGG1, PROF_GEMM1, PROF_DW1, PROF_STEP, PROF_AGG2, PROF_SGD = range(7)
+(PROF_BUILD, PROF_AGG1, PROF_GEMM1, PROF_DW1, PROF_STEP, PROF_AGG2, PROF_SGD, PROF_PG_MARK,
+ PROF_PG_COPY, PROF_PG_CLEAR) = range(10)

@@ -93,7 +93,8 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* scratch, int* to
 // Launch accounting + optional CUDA-event timing of selected kernel sites
 // (bench.py reads them through hg_prof_read / hg_launch_count).
 enum ProfSite { PROF_BUILD = 0, PROF_AGG1 = 1, PROF_GEMM1 = 2, PROF_DW1 = 3, PROF_STEP = 4,
-                PROF_AGG2 = 5, PROF_SGD = 6, PROF_NSITES = 8 };
+                PROF_AGG2 = 5, PROF_SGD = 6, PROF_PG_MARK = 7, PROF_PG_COPY = 8,
+                PROF_PG_CLEAR = 9, PROF_NSITES = 12 };
 void count_launch(int n = 1);
 void prof_begin(int site, cudaStream_t s);
 void prof_end(int site, cudaStream_t s);

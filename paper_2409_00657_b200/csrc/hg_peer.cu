@@ -48,7 +48,7 @@ __global__ void k_remote_clear(const int32_t* __restrict__ ids, const int32_t* _
 // append them to a staging list and map vertex -> staging row; copy = pull
 // their rows from the owners' HBM with wide, deeply pipelined peer loads.
 __global__ void k_stage_mark(const int32_t* __restrict__ ids, const int32_t* __restrict__ n_dev,
-                             const int32_t* __restrict__ home, int rank,
+                             const int32_t* __restrict__ home, int rank, int n_homes,
                              uint32_t* __restrict__ bitmap, int32_t* __restrict__ stage_list,
                              int32_t* __restrict__ stage_row, int32_t* __restrict__ stage_count,
                              int stage_cap, unsigned long long* __restrict__ uniq_per_home,
@@ -56,27 +56,49 @@ __global__ void k_stage_mark(const int32_t* __restrict__ ids, const int32_t* __r
                              const int64_t* __restrict__ it_dev, int row_stride) {
   const int n = *n_dev;
   if (uniq_per_home && it_dev) uniq_per_home += *it_dev * row_stride;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
   unsigned long long mine = 0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int v = ids[i];
-    const int h = home[v];
-    if (h == rank) continue;
-    ++mine;
-    const uint32_t bit = 1u << (v & 31);
-    const uint32_t old = atomicOr(bitmap + (v >> 5), bit);
-    if (!(old & bit)) {
-      const int slot = atomicAdd(stage_count, 1);
+  // warp-uniform trip count: the counters below are warp-aggregated (one
+  // atomic per warp instead of one per new remote row on a single address)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    int v = 0, h = rank;
+    if (i < n) {
+      v = ids[i];
+      h = home[v];
+    }
+    const bool remote = h != rank;
+    bool fresh = false;
+    if (remote) {
+      ++mine;
+      const uint32_t bit = 1u << (v & 31);
+      fresh = !(atomicOr(bitmap + (v >> 5), bit) & bit);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, fresh);
+    if (!m) continue;
+    int slot0 = 0;
+    if (lane == 0) slot0 = atomicAdd(stage_count, __popc(m));
+    slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+    if (fresh) {
+      const int slot = slot0 + __popc(m & lt);
       if (slot < stage_cap) {
         stage_list[slot] = v;
         stage_row[v] = slot;
       } else {
         raise_flag(err, HG_EINVARIANT);
       }
-      if (uniq_per_home) atomicAdd(uniq_per_home + h, 1ull);
+    }
+    if (uniq_per_home) {
+      for (int q = 0; q < n_homes; ++q) {
+        const unsigned mq = __ballot_sync(0xffffffffu, fresh && h == q);
+        if (lane == 0 && mq) atomicAdd(uniq_per_home + q, (unsigned long long)__popc(mq));
+      }
     }
   }
   for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-  if (total_remote && (threadIdx.x & 31) == 0 && mine) atomicAdd(total_remote, mine);
+  if (total_remote && lane == 0 && mine) atomicAdd(total_remote, mine);
 }
 
 // 16 lanes x 16 B per row (256-byte bf16 rows); 8 rows in flight per warp.
@@ -110,9 +132,130 @@ k_stage_copy(const int32_t* __restrict__ stage_list, const int32_t* __restrict__
   }
 }
 
+// ---------------------------------------------------------------- push pre-gather
+//
+// Random row reads from a peer's 10+ GB shard are bound by the requester's
+// peer-mapping TLB (measured: 9K random 256-B rows 80 GB/s, 36K rows 29 GB/s;
+// sequential 157 GB/s).  The push variant turns them around: each rank
+// publishes its deduplicated request list in its mailbox, the OWNER gathers
+// the rows from its local shard (local TLB) and writes them into the
+// requester's staging rows over NVLink (a small contiguous region).
+// Mailbox (one cudaMalloc per rank, IPC-mapped by every peer):
+//   flags[S] i64 | done[S] i64 | count i32 | list[cap] i32 | staging[cap x row]
+// flags[p] / done[p] = sequence number of p's latest "requests ready" / "my
+// rows written" signal; the sequence advances once per pre-gather on every rank.
+
+struct Mailbox {
+  int64_t o_flags, o_done, o_count, o_list, o_staging;
+};
+
+__device__ __forceinline__ uint8_t* mb_base(const uint64_t* boxes, int p) {
+  return reinterpret_cast<uint8_t*>(boxes[p]);
+}
+
+// wait until every peer's counter (at box[rank] + off + 8*p, written by p) reaches seq
+__device__ bool spin_peers(const uint64_t* boxes, int rank, int S, int64_t off, int64_t seq) {
+  volatile int64_t* mine = reinterpret_cast<volatile int64_t*>(mb_base(boxes, rank) + off);
+  for (long long it = 0; it < (1ll << 26); ++it) {
+    bool all = true;
+    for (int p = 0; p < S; ++p)
+      if (p != rank && mine[p] < seq) all = false;
+    if (all) return true;
+    __nanosleep(64);
+  }
+  return false;
+}
+
+__global__ void k_pg_signal(const uint64_t* __restrict__ boxes, int rank, int S, Mailbox m,
+                            int64_t* seq, int64_t off) {
+  if (threadIdx.x != 0) return;
+  const int64_t v = (off == m.o_flags) ? *seq + 1 : *seq;
+  if (off == m.o_flags) *seq = v;
+  __threadfence_system();
+  for (int p = 0; p < S; ++p) {
+    if (p == rank) continue;
+    volatile int64_t* f = reinterpret_cast<volatile int64_t*>(mb_base(boxes, p) + off);
+    f[rank] = v;
+  }
+  __threadfence_system();
+}
+
+__global__ void k_pg_wait(const uint64_t* __restrict__ boxes, int rank, int S, Mailbox m,
+                          const int64_t* seq, int64_t off, int* err) {
+  if (threadIdx.x == 0 && !spin_peers(boxes, rank, S, off, *seq)) raise_flag(err, HG_EINVARIANT);
+}
+
+// owner side: serve every peer's requests homed here.  Half-warp per row.
+__global__ void __launch_bounds__(256)
+k_pg_serve(const uint64_t* __restrict__ boxes, int rank, int S, Mailbox m, const int64_t* seq,
+           const int32_t* __restrict__ home, const int32_t* __restrict__ local_row,
+           const uint8_t* __restrict__ shard, int row_bytes, int stage_cap, int* err) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) ok = spin_peers(boxes, rank, S, m.o_flags, *seq) ? 1 : 0;
+  __syncthreads();
+  if (!ok) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) raise_flag(err, HG_EINVARIANT);
+    return;
+  }
+  const int vec = row_bytes / 16;
+  const int hw = (blockIdx.x * blockDim.x + threadIdx.x) / 16, hl = threadIdx.x & 15;
+  const int n_hw = gridDim.x * blockDim.x / 16;
+  for (int p = 0; p < S; ++p) {
+    if (p == rank) continue;
+    uint8_t* box = mb_base(boxes, p);
+    const int n = min(*reinterpret_cast<volatile int32_t*>(box + m.o_count), stage_cap);
+    const int32_t* list = reinterpret_cast<const int32_t*>(box + m.o_list);
+    uint8_t* staging = box + m.o_staging;
+    for (int i = hw; i < n; i += n_hw) {
+      const int v = list[i];
+      if (home[v] != rank) continue;
+      const uint4* src = reinterpret_cast<const uint4*>(shard + (int64_t)local_row[v] * row_bytes);
+      uint4* dst = reinterpret_cast<uint4*>(staging + (int64_t)i * row_bytes);
+      for (int c = hl; c < vec; c += 16) dst[c] = src[c];
+    }
+  }
+  __threadfence_system();  // rows land before the "done" signal of the next kernel
+}
+
 }  // namespace hg
 
 using namespace hg;
+
+extern "C" int hg_pregather_push(const int32_t* ids, const int32_t* n_dev, const int32_t* home,
+                                 int32_t rank, int32_t n_ranks, const int32_t* local_row,
+                                 const void* shard, int32_t row_bytes, uint32_t* bitmap,
+                                 int32_t* stage_row, int32_t stage_cap, const void* boxes,
+                                 void* own_box, int64_t o_flags, int64_t o_done, int64_t o_count,
+                                 int64_t o_list, int64_t o_staging,
+                                 unsigned long long* uniq_per_home, const int64_t* it_dev,
+                                 int32_t row_stride, unsigned long long* total_remote,
+                                 int64_t* seq, int* err, void* stream) {
+  if (row_bytes % 16) return hg_fail(HG_ECONFIG, "row bytes must be a multiple of 16");
+  cudaStream_t s = (cudaStream_t)stream;
+  const Mailbox m{o_flags, o_done, o_count, o_list, o_staging};
+  const uint64_t* bx = (const uint64_t*)boxes;
+  uint8_t* own = (uint8_t*)own_box;
+  int32_t* count = (int32_t*)(own + o_count);
+  HG_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t), s));
+  count_launch(6);
+  prof_begin(PROF_PG_MARK, s);
+  k_stage_mark<<<148 * 2, 256, 0, s>>>(ids, n_dev, home, rank, n_ranks, bitmap,
+                                       (int32_t*)(own + o_list), stage_row, count, stage_cap,
+                                       uniq_per_home, total_remote, err, it_dev, row_stride);
+  prof_end(PROF_PG_MARK, s);
+  prof_begin(PROF_PG_COPY, s);
+  k_pg_signal<<<1, 32, 0, s>>>(bx, rank, n_ranks, m, seq, o_flags);          // requests ready
+  k_pg_serve<<<148 * 2, 256, 0, s>>>(bx, rank, n_ranks, m, seq, home, local_row,
+                                     (const uint8_t*)shard, row_bytes, stage_cap, err);
+  k_pg_signal<<<1, 32, 0, s>>>(bx, rank, n_ranks, m, seq, o_done);           // my rows written
+  k_pg_wait<<<1, 32, 0, s>>>(bx, rank, n_ranks, m, seq, o_done, err);        // all rows here
+  prof_end(PROF_PG_COPY, s);
+  prof_begin(PROF_PG_CLEAR, s);
+  k_remote_clear<<<148 * 2, 256, 0, s>>>(ids, n_dev, 0, bitmap);
+  prof_end(PROF_PG_CLEAR, s);
+  HG_CUDA_TRY(cudaGetLastError());
+  return HG_OK;
+}
 
 extern "C" int hg_pregather_peer_at(const int32_t* ids, const int32_t* n_dev, const int32_t* home,
                                     int32_t rank, const int32_t* local_row, const void* peers,
@@ -125,12 +268,18 @@ extern "C" int hg_pregather_peer_at(const int32_t* ids, const int32_t* n_dev, co
   cudaStream_t s = (cudaStream_t)stream;
   HG_CUDA_TRY(cudaMemsetAsync(stage_count, 0, sizeof(int32_t), s));
   count_launch(3);
-  k_stage_mark<<<148 * 2, 256, 0, s>>>(ids, n_dev, home, rank, bitmap, stage_list, stage_row,
-                                       stage_count, stage_cap, uniq_per_home, total_remote, err,
-                                       it_dev, row_stride);
+  prof_begin(PROF_PG_MARK, s);
+  k_stage_mark<<<148 * 2, 256, 0, s>>>(ids, n_dev, home, rank, row_stride > 0 ? row_stride : 64,
+                                       bitmap, stage_list, stage_row, stage_count, stage_cap,
+                                       uniq_per_home, total_remote, err, it_dev, row_stride);
+  prof_end(PROF_PG_MARK, s);
+  prof_begin(PROF_PG_COPY, s);
   k_stage_copy<<<148 * 4, 256, 0, s>>>(stage_list, stage_count, stage_cap, home, local_row,
                                        (const uint8_t* const*)peers, row_bytes, (uint8_t*)staging);
+  prof_end(PROF_PG_COPY, s);
+  prof_begin(PROF_PG_CLEAR, s);
   k_remote_clear<<<148 * 2, 256, 0, s>>>(ids, n_dev, 0, bitmap);
+  prof_end(PROF_PG_CLEAR, s);
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;
 }
@@ -148,7 +297,9 @@ extern "C" int hg_pregather_peer(const int32_t* ids, const int32_t* n_dev, const
 
 extern "C" int hg_alloc(size_t bytes, void** out) {
   *out = nullptr;
-  HG_CUDA_TRY(cudaMalloc(out, bytes < 256 ? 256 : bytes));
+  const size_t b = bytes < 256 ? 256 : bytes;
+  HG_CUDA_TRY(cudaMalloc(out, b));
+  HG_CUDA_TRY(cudaMemset(*out, 0, b));  // mailboxes rely on zeroed counters
   return HG_OK;
 }
 

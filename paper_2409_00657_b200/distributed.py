@@ -28,6 +28,7 @@ categories and messages) so byte counts compare one for one with gnnsim;
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -240,6 +241,7 @@ class PeerFeatures:
         self.dim, self.ld = dim, (dim + 7) // 8 * 8
         self.dtype, self.device = dtype, dev
         self.rank, self.S = rank, part.n_servers
+        self.group = group
         esz = 2 if dtype == torch.bfloat16 else 4
         home = part.home
         local = np.flatnonzero(home == rank).astype(np.int64)
@@ -297,33 +299,71 @@ class PeerFeatures:
         d.rank = self.rank
 
     def bind_staged(self, runner: CellRunner, stage_cap: int) -> None:
-        """Staged mode: remote rows are pre-gathered into local HBM by
-        hg_pregather_peer (bulk NVLink copies), the gather reads HBM only."""
-        if not hasattr(self, "staging"):
+        """Staged mode: remote rows are pre-gathered into local HBM (the staging
+        rows of this rank's mailbox) by hg_pregather_push, the gather reads HBM
+        only.  The first call allocates and exchanges the mailboxes (collective:
+        every rank reaches it at the same step)."""
+        if not hasattr(self, "mbox"):
             dev = self.device
-            self.stage_cap = int(stage_cap)
-            self.staging = torch.empty((self.stage_cap, self.ld), dtype=self.dtype, device=dev)
-            self.stage_list = torch.empty(self.stage_cap, dtype=torch.int32, device=dev)
+            S, row = self.S, self.ld * (2 if self.dtype == torch.bfloat16 else 4)
+            cap = int(stage_cap)
+            up = lambda x: (x + 255) // 256 * 256  # noqa: E731
+            o_flags, o_done = 0, 8 * S
+            o_count = up(16 * S)
+            o_list = up(o_count + 16)
+            o_staging = up(o_list + 4 * cap)
+            total = o_staging + cap * row
+            ptr = C.c_void_p()
+            _lib.call("hg_alloc", total, C.byref(ptr))
+            self.mbox = ptr.value
+            self.mb_off = (o_flags, o_done, o_count, o_list, o_staging)
+            handle = (C.c_char * 64)()
+            _lib.call("hg_ipc_handle", self.mbox, handle)
+            handles = [None] * S
+            if dist.is_initialized() and S > 1:
+                dist.all_gather_object(handles, bytes(handle), group=self.group)
+            else:
+                handles = [bytes(handle)]
+            boxes = []
+            for h, hb in enumerate(handles):
+                if h == self.rank:
+                    boxes.append(self.mbox)
+                    continue
+                p = C.c_void_p()
+                _lib.call("hg_ipc_open", (C.c_char * 64).from_buffer_copy(hb), C.byref(p))
+                self.opened.append(p.value)
+                boxes.append(p.value)
+            self.boxes = torch.tensor(boxes, dtype=torch.int64, device=dev)
+            self.stage_cap = cap
+            self.row_bytes = row
             self.stage_row = torch.zeros(len(self.local_row), dtype=torch.int32, device=dev)
-            self.stage_count = torch.zeros(1, dtype=torch.int32, device=dev)
+            self.seq = torch.zeros(1, dtype=torch.int64, device=dev)
             self.err = torch.zeros(1, dtype=torch.int32, device=dev)
         d = runner.desc
         d.features = self.ptr
         d.feat_row = self.local_row.data_ptr()
         d.feat_peers = None
         d.feat_home = self.home.data_ptr()
-        d.stage_base = self.staging.data_ptr()
+        d.stage_base = self.mbox + self.mb_off[4]
         d.stage_row = self.stage_row.data_ptr()
         d.rank = self.rank
 
-    def pregather(self, runner: CellRunner, uniq_row_ptr: int, total_ptr: int, stream) -> None:
+    def pregather(self, runner: CellRunner, uniq_row_ptr: int, total_ptr: int, stream,
+                  it_dev_ptr=None, empty: bool = False) -> None:
+        """Owner-side push pre-gather of the runner's remote rows (every rank
+        calls it in lock-step).  Ledger counts go to uniq_row_ptr (plus
+        *it_dev * S rows when a device cursor is given)."""
         t = runner.builder.tensors
-        _lib.call("hg_pregather_peer", t["need_ids"][0].data_ptr(), t["totals"].data_ptr(),
-                  self.home.data_ptr(), self.rank, self.local_row.data_ptr(),
-                  self.peers.data_ptr(), self.ld * self.staging.element_size(),
-                  self.bitmap.data_ptr(), self.stage_list.data_ptr(), self.stage_row.data_ptr(),
-                  self.stage_count.data_ptr(), self.stage_cap, self.staging.data_ptr(),
-                  uniq_row_ptr, total_ptr, self.err.data_ptr(), stream)
+        o = self.mb_off
+        if not hasattr(self, "_zero"):
+            self._zero = torch.zeros(1, dtype=torch.int32, device=self.device)
+        n_ptr = self._zero.data_ptr() if empty else t["totals"].data_ptr()
+        _lib.call("hg_pregather_push", t["need_ids"][0].data_ptr(), n_ptr,
+                  self.home.data_ptr(), self.rank, self.S, self.local_row.data_ptr(), self.ptr,
+                  self.row_bytes, self.bitmap.data_ptr(), self.stage_row.data_ptr(),
+                  self.stage_cap, self.boxes.data_ptr(), self.mbox, o[0], o[1], o[2], o[3], o[4],
+                  uniq_row_ptr, it_dev_ptr, self.S, total_ptr, self.seq.data_ptr(),
+                  self.err.data_ptr(), stream)
 
     def close(self):
         for p in self.opened:
@@ -367,9 +407,14 @@ class DistGraphLoop:
                     self.side_ops(nxt, self.side.cuda_stream)
                 cs = cap_s.cuda_stream
                 _lib.call("hg_train_step", C.byref(run.desc), self.cap, cs)
-                self.pin_loss[x].copy_(run.loss[:self.cap].sum().reshape(1), non_blocking=True)
-                _lib.call("hg_allreduce_sgd", tr._comm, m.flat.data_ptr(), m.grad.data_ptr(),
-                          m.flat.numel(), float(tr.lr), 1.0 / total, cs)
+                if not os.environ.get("HG_DGL_NO_LOSS"):  # timing experiment knob
+                    self.pin_loss[x].copy_(run.loss[:self.cap].sum().reshape(1),
+                                           non_blocking=True)
+                if os.environ.get("HG_DGL_NO_ALLREDUCE"):  # timing experiment only
+                    m.sgd(tr.lr, total, stream=cs)
+                else:
+                    _lib.call("hg_allreduce_sgd", tr._comm, m.flat.data_ptr(), m.grad.data_ptr(),
+                              m.flat.numel(), float(tr.lr), 1.0 / total, cs)
                 cap_s.wait_stream(self.side)
             cur.wait_stream(cap_s)
             self.graphs.append(g)
@@ -385,14 +430,8 @@ class DistGraphLoop:
                   r.roots.data_ptr(), r.n_dev.data_ptr(), r.keys.data_ptr(), s)
         r.builder.build(tr.graph, r.roots.data_ptr(), r.keys.data_ptr(), self.cap,
                         n_roots=self.cap, stream=s, n_dev=r.n_dev.data_ptr())
-        f = tr.feats
-        t = r.builder.tensors
-        _lib.call("hg_pregather_peer_at", t["need_ids"][0].data_ptr(), t["totals"].data_ptr(),
-                  f.home.data_ptr(), f.rank, f.local_row.data_ptr(), f.peers.data_ptr(),
-                  f.ld * f.staging.element_size(), f.bitmap.data_ptr(), f.stage_list.data_ptr(),
-                  f.stage_row.data_ptr(), f.stage_count.data_ptr(), f.stage_cap,
-                  f.staging.data_ptr(), tr._acct_rows.data_ptr(), tr._g_it.data_ptr(), tr.S,
-                  tr._acct_total.data_ptr(), f.err.data_ptr(), s)
+        tr.feats.pregather(r, tr._acct_rows.data_ptr(), tr._acct_total.data_ptr(), s,
+                           it_dev_ptr=tr._g_it.data_ptr())
         _lib.call("hg_step_prologue", C.byref(r.desc), self.cap, 1, s)
 
     def replay(self, x: int) -> None:
@@ -684,6 +723,10 @@ class MicrographTrainer:
         def launch(r, s):
             r.n_roots = n
             if not n:
+                if not self.pregather and hasattr(self.feats, "mbox"):
+                    # the push pre-gather is collective: take part with no requests
+                    self.feats.pregather(r, self._acct_rows[it].data_ptr(),
+                                         self._acct_total.data_ptr(), s, empty=True)
                 return
             rp, kp = self._stage_ring(roots, it)
             r.builder.build(self.graph, rp, kp, n, n_roots=n, stream=s)
