@@ -301,10 +301,11 @@ int hg_pregather_peer_at(const int32_t* ids, const int32_t* n_dev, const int32_t
  * NVLink; returns (stream order) once every peer has signalled completion.
  * All ranks must call it the same number of times.  boxes: device array of
  * the S mailbox base addresses (own + IPC-mapped peers); layout offsets in
- * bytes; seq: device int64 sequence counter (starts at 0). */
+ * bytes; stamp: int32[n] zero-initialised dedup stamps (no clearing pass);
+ * seq: device int64 sequence counter (starts at 0). */
 int hg_pregather_push(const int32_t* ids, const int32_t* n_dev, const int32_t* home, int32_t rank,
                       int32_t n_ranks, const int32_t* local_row, const void* shard,
-                      int32_t row_bytes, uint32_t* bitmap, int32_t* stage_row, int32_t stage_cap,
+                      int32_t row_bytes, int32_t* stamp, int32_t* stage_row, int32_t stage_cap,
                       const void* boxes, void* own_box, int64_t o_flags, int64_t o_done,
                       int64_t o_count, int64_t o_list, int64_t o_staging,
                       unsigned long long* uniq_per_home, const int64_t* it_dev,

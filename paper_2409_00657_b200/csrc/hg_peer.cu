@@ -101,6 +101,63 @@ __global__ void k_stage_mark(const int32_t* __restrict__ ids, const int32_t* __r
   if (total_remote && lane == 0 && mine) atomicAdd(total_remote, mine);
 }
 
+// Push-path variant of k_stage_mark: dedup by generation stamps instead of a
+// bitmap (stamp[v] = tag of the last pre-gather that listed v), so no clearing
+// pass is needed afterwards.  tag = the sequence number this call will publish.
+__global__ void k_stage_mark_stamp(const int32_t* __restrict__ ids, const int32_t* __restrict__ n_dev,
+                                   const int32_t* __restrict__ home, int rank, int n_homes,
+                                   int32_t* __restrict__ stamp, const int64_t* __restrict__ seq,
+                                   int32_t* __restrict__ stage_list, int32_t* __restrict__ stage_row,
+                                   int32_t* __restrict__ stage_count, int stage_cap,
+                                   unsigned long long* __restrict__ uniq_per_home,
+                                   unsigned long long* __restrict__ total_remote, int* err,
+                                   const int64_t* __restrict__ it_dev, int row_stride) {
+  const int n = *n_dev;
+  int32_t tag = (int32_t)((*seq + 1) & 0x7fffffff);  // unique per call until 2^31 calls
+  if (tag == 0) tag = 1;
+  if (uniq_per_home && it_dev) uniq_per_home += *it_dev * row_stride;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  unsigned long long mine = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    int v = 0, h = rank;
+    if (i < n) {
+      v = ids[i];
+      h = home[v];
+    }
+    const bool remote = h != rank;
+    bool fresh = false;
+    if (remote) {
+      ++mine;
+      fresh = atomicExch(stamp + v, tag) != tag;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, fresh);
+    if (!m) continue;
+    int slot0 = 0;
+    if (lane == 0) slot0 = atomicAdd(stage_count, __popc(m));
+    slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+    if (fresh) {
+      const int slot = slot0 + __popc(m & lt);
+      if (slot < stage_cap) {
+        stage_list[slot] = v;
+        stage_row[v] = slot;
+      } else {
+        raise_flag(err, HG_EINVARIANT);
+      }
+    }
+    if (uniq_per_home) {
+      for (int q = 0; q < n_homes; ++q) {
+        const unsigned mq = __ballot_sync(0xffffffffu, fresh && h == q);
+        if (lane == 0 && mq) atomicAdd(uniq_per_home + q, (unsigned long long)__popc(mq));
+      }
+    }
+  }
+  for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if (total_remote && lane == 0 && mine) atomicAdd(total_remote, mine);
+}
+
 // 16 lanes x 16 B per row (256-byte bf16 rows); 8 rows in flight per warp.
 __global__ void __launch_bounds__(256)
 k_stage_copy(const int32_t* __restrict__ stage_list, const int32_t* __restrict__ stage_count,
@@ -223,7 +280,7 @@ using namespace hg;
 
 extern "C" int hg_pregather_push(const int32_t* ids, const int32_t* n_dev, const int32_t* home,
                                  int32_t rank, int32_t n_ranks, const int32_t* local_row,
-                                 const void* shard, int32_t row_bytes, uint32_t* bitmap,
+                                 const void* shard, int32_t row_bytes, int32_t* stamp,
                                  int32_t* stage_row, int32_t stage_cap, const void* boxes,
                                  void* own_box, int64_t o_flags, int64_t o_done, int64_t o_count,
                                  int64_t o_list, int64_t o_staging,
@@ -237,11 +294,12 @@ extern "C" int hg_pregather_push(const int32_t* ids, const int32_t* n_dev, const
   uint8_t* own = (uint8_t*)own_box;
   int32_t* count = (int32_t*)(own + o_count);
   HG_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t), s));
-  count_launch(6);
+  count_launch(5);
   prof_begin(PROF_PG_MARK, s);
-  k_stage_mark<<<148 * 2, 256, 0, s>>>(ids, n_dev, home, rank, n_ranks, bitmap,
-                                       (int32_t*)(own + o_list), stage_row, count, stage_cap,
-                                       uniq_per_home, total_remote, err, it_dev, row_stride);
+  k_stage_mark_stamp<<<148 * 2, 256, 0, s>>>(ids, n_dev, home, rank, n_ranks, stamp, seq,
+                                             (int32_t*)(own + o_list), stage_row, count,
+                                             stage_cap, uniq_per_home, total_remote, err, it_dev,
+                                             row_stride);
   prof_end(PROF_PG_MARK, s);
   prof_begin(PROF_PG_COPY, s);
   k_pg_signal<<<1, 32, 0, s>>>(bx, rank, n_ranks, m, seq, o_flags);          // requests ready
@@ -250,9 +308,6 @@ extern "C" int hg_pregather_push(const int32_t* ids, const int32_t* n_dev, const
   k_pg_signal<<<1, 32, 0, s>>>(bx, rank, n_ranks, m, seq, o_done);           // my rows written
   k_pg_wait<<<1, 32, 0, s>>>(bx, rank, n_ranks, m, seq, o_done, err);        // all rows here
   prof_end(PROF_PG_COPY, s);
-  prof_begin(PROF_PG_CLEAR, s);
-  k_remote_clear<<<148 * 2, 256, 0, s>>>(ids, n_dev, 0, bitmap);
-  prof_end(PROF_PG_CLEAR, s);
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;
 }

@@ -338,6 +338,7 @@ class PeerFeatures:
             self.row_bytes = row
             self.stage_row = torch.zeros(len(self.local_row), dtype=torch.int32, device=dev)
             self.seq = torch.zeros(1, dtype=torch.int64, device=dev)
+            self.stamp = torch.zeros(len(self.local_row), dtype=torch.int32, device=dev)
             self.err = torch.zeros(1, dtype=torch.int32, device=dev)
         d = runner.desc
         d.features = self.ptr
@@ -360,7 +361,7 @@ class PeerFeatures:
         n_ptr = self._zero.data_ptr() if empty else t["totals"].data_ptr()
         _lib.call("hg_pregather_push", t["need_ids"][0].data_ptr(), n_ptr,
                   self.home.data_ptr(), self.rank, self.S, self.local_row.data_ptr(), self.ptr,
-                  self.row_bytes, self.bitmap.data_ptr(), self.stage_row.data_ptr(),
+                  self.row_bytes, self.stamp.data_ptr(), self.stage_row.data_ptr(),
                   self.stage_cap, self.boxes.data_ptr(), self.mbox, o[0], o[1], o[2], o[3], o[4],
                   uniq_row_ptr, it_dev_ptr, self.S, total_ptr, self.seq.data_ptr(),
                   self.err.data_ptr(), stream)
