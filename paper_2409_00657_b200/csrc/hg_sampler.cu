@@ -27,6 +27,9 @@
 namespace hg {
 
 constexpr int kBuildThreads = 256;
+#ifndef HG_BUILD_MINB
+#define HG_BUILD_MINB 5  // resident build CTAs per SM (48 regs): leaves room for the training branch
+#endif
 constexpr int kBuildWarps = kBuildThreads / 32;
 constexpr int kBigTask = 256;  // degree above which the whole CTA draws one vertex
 
@@ -421,7 +424,7 @@ __device__ long long g_phase[4096][16];
 #define HG_PHASE(i)
 #endif
 
-__global__ void __launch_bounds__(kBuildThreads, 4)
+__global__ void __launch_bounds__(kBuildThreads, HG_BUILD_MINB)
 k_mg_build(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targets,
            int64_t n_vertices, const int64_t* __restrict__ roots, int n_roots,
            const uint64_t* __restrict__ iter_state, int roots_per_state, MgCarve c,
