@@ -242,6 +242,9 @@ typedef struct {
   /* per-root capacity of need[k] rows (hg_mg_layout.cap_need); 0 = unknown.
    * Enables the per-root fused backward scatter when a root's rows fit smem. */
   int32_t root_rows[HG_MAX_LAYERS + 1];
+  /* 1: the bf16 operand copies (Wlp, Wb, WcT, Wcp) already hold the current
+   * parameters (hg_sgd_refresh ran last) -- the step skips its transposes */
+  int32_t lowp_fresh;
 } hg_step_desc;
 
 /* Peer memory (one process per GPU): device allocations whose CUDA IPC
@@ -330,6 +333,14 @@ int hg_gemm_bf16(const void* A, int64_t lda, int a_mn_major, const void* B, int6
 /* theta -= lr * (g * inv_batch); g = 0; refresh bf16 shadow (model.py:315-324). */
 int hg_sgd_update(float* params, float* grads, void* shadow_bf16, int64_t n, float lr,
                   float inv_batch, void* stream);
+/* SGD (as hg_sgd_update) fused with the refresh of the step's bf16 operand
+ * copies of the parameters (Wlp = Wᵀ, Wb = W, WcT = W_cᵀ, Wcp = W_c padded),
+ * so the next step can run with d->lowp_fresh = 1.  update = 0: refresh only. */
+int hg_sgd_refresh(const hg_step_desc* d, float* params, float* grads, int64_t n, float lr,
+                   float inv_batch, int32_t update, void* stream);
+/* NCCL all-reduce of the gradients + hg_sgd_refresh. */
+int hg_allreduce_sgd_refresh(void* comm, const hg_step_desc* d, float* params, float* grads,
+                             int64_t n, float lr, float inv_batch, void* stream);
 
 #ifdef __cplusplus
 }

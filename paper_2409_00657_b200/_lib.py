@@ -66,7 +66,8 @@ class StepDesc(C.Structure):
                 ("Wb", _P7V), ("feat_peers", C.c_void_p), ("feat_home", C.c_void_p),
                 ("stage_base", C.c_void_p), ("stage_row", C.c_void_p), ("rank", C.c_int32),
                 ("agg1_ready", C.c_int32), ("WcT", C.c_void_p), ("Wcp", C.c_void_p),
-                ("dl_lowp", C.c_void_p), ("root_rows", C.c_int32 * 7)]
+                ("dl_lowp", C.c_void_p), ("root_rows", C.c_int32 * 7),
+                ("lowp_fresh", C.c_int32)]
 
 
 V, I32, I64, U64, SZ = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_size_t
@@ -100,6 +101,8 @@ SIGNATURES = {
     "hg_train_step": [C.POINTER(StepDesc), I32, V],
     "hg_forward": [C.POINTER(StepDesc), I32, V],
     "hg_sgd_update": [V, V, V, I64, C.c_float, C.c_float, V],
+    "hg_sgd_refresh": [C.POINTER(StepDesc), V, V, I64, C.c_float, C.c_float, I32, V],
+    "hg_allreduce_sgd_refresh": [V, C.POINTER(StepDesc), V, V, I64, C.c_float, C.c_float, V],
     "hg_gemm_bf16": [V, I64, C.c_int, V, I64, C.c_int, V, I64, I32, I32, I32, I32, V, I32, V],
     "hg_alloc": [C.c_size_t, C.POINTER(C.c_void_p)],
     "hg_free": [V],

@@ -585,6 +585,51 @@ __global__ void k_zero_rows(float* __restrict__ x, const int32_t* __restrict__ n
   }
 }
 
+// Where each parameter's bf16 operand copies live (the step's layout).
+struct LowpMap {
+  int L, H, C, Cp;
+  int64_t off[HG_MAX_LAYERS + 1];  // flat offset of W_k
+  int in[HG_MAX_LAYERS + 1];
+  bf16* Wlp[HG_MAX_LAYERS + 1];    // [H x in_k]  (Wᵀ, K-major B of the forward GEMM)
+  bf16* Wb[HG_MAX_LAYERS + 1];     // [in_k x H]  (W, K-major B of the dX GEMM) or null
+  int64_t off_c;                   // flat offset of W_c [H x C]
+  bf16* WcT;                       // [C x H]
+  bf16* Wcp;                       // [H x Cp]
+};
+
+// SGD + gradient reset, then the parameter's bf16 copies (one pass over the
+// flat buffer instead of three transposes and a pad per step).
+__global__ void k_sgd_refresh(float* __restrict__ p, float* __restrict__ g, int64_t n, float lr,
+                              float inv_batch, int update, LowpMap m) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v = p[i];
+    if (update) {
+      v -= lr * (g[i] * inv_batch);
+      p[i] = v;
+      g[i] = 0.f;
+    }
+    const bf16 b = __float2bfloat16_rn(v);
+    if (i >= m.off_c) {
+      const int64_t j = i - m.off_c;
+      if (j < (int64_t)m.H * m.C) {
+        const int r = (int)(j / m.C), c = (int)(j % m.C);
+        m.WcT[(int64_t)c * m.H + r] = b;
+        m.Wcp[(int64_t)r * m.Cp + c] = b;
+      }
+      continue;
+    }
+    for (int k = 1; k <= m.L; ++k) {
+      const int64_t j = i - m.off[k];
+      if (j < 0 || j >= (int64_t)m.in[k] * m.H) continue;
+      const int r = (int)(j / m.H), c = (int)(j % m.H);
+      m.Wlp[k][(int64_t)c * m.in[k] + r] = b;
+      if (m.Wb[k]) m.Wb[k][j] = b;
+      break;
+    }
+  }
+}
+
 __global__ void k_sgd(float* __restrict__ p, float* __restrict__ g, bf16* __restrict__ shadow,
                       int64_t n, float lr, float inv_batch) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -680,7 +725,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
   scatter_root_attrs<T>();
   // ---- forward
   prof_begin(PROF_STEP, s);
-  if (tc) {
+  if (tc && !d->lowp_fresh) {
     for (int k = 1; k <= L; ++k) {
       dim3 g((H + 31) / 32, (d->in_dim[k] + 31) / 32), b(32, 8);
       count_launch();
@@ -708,7 +753,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
   if (tc_head) {
     // logits = h_L @ W_c on tcgen05 (B = W_cᵀ bf16, K-major); softmax-CE writes
     // dlogits (f32 in place + bf16 padded copy for the backward GEMMs)
-    {
+    if (!d->lowp_fresh) {
       dim3 g((C + 31) / 32, (H + 31) / 32), b(32, 8);
       count_launch(2);
       k_transpose_bf16<<<g, b, 0, s>>>(d->Wc, H, C, (bf16*)d->WcT, nullptr);
@@ -870,6 +915,35 @@ extern "C" int hg_forward(const hg_step_desc* d, int32_t n_roots, void* stream) 
   cudaStream_t s = (cudaStream_t)stream;
   st = d->act_dtype == 0 ? run_step<float>(d, n_roots, s, false) : run_step<bf16>(d, n_roots, s, false);
   if (st) return st;
+  HG_CUDA_TRY(cudaGetLastError());
+  return HG_OK;
+}
+
+extern "C" int hg_sgd_refresh(const hg_step_desc* d, float* params, float* grads, int64_t n,
+                              float lr, float inv_batch, int32_t update, void* stream) {
+  if (n <= 0) return HG_OK;
+  if (!d->WcT || !d->Wcp) return hg_fail(HG_ECONFIG, "hg_sgd_refresh needs the bf16 head operands");
+  LowpMap m{};
+  m.L = d->n_layers;
+  m.H = d->hidden;
+  m.C = d->n_classes;
+  m.Cp = (m.C + 63) / 64 * 64;
+  for (int k = 1; k <= m.L; ++k) {
+    m.off[k] = d->W[k] - params;
+    m.in[k] = d->in_dim[k];
+    m.Wlp[k] = (bf16*)d->Wlp[k];
+    m.Wb[k] = k >= 2 ? (bf16*)d->Wb[k] : nullptr;
+    if (m.off[k] < 0 || m.off[k] + (int64_t)m.in[k] * m.H > n)
+      return hg_fail(HG_ECONFIG, "layer %d weights outside the flat parameter buffer", k);
+  }
+  m.off_c = d->Wc - params;
+  m.WcT = (bf16*)d->WcT;
+  m.Wcp = (bf16*)d->Wcp;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  count_launch();
+  prof_begin(PROF_SGD, (cudaStream_t)stream);
+  k_sgd_refresh<<<grid, 256, 0, (cudaStream_t)stream>>>(params, grads, n, lr, inv_batch, update, m);
+  prof_end(PROF_SGD, (cudaStream_t)stream);
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;
 }

@@ -50,6 +50,18 @@ extern "C" int hg_allreduce_sgd(void* comm, float* params, float* grads, int64_t
   return hg_sgd_update(params, grads, nullptr, n, lr, inv_batch, stream);
 }
 
+extern "C" int hg_sgd_refresh(const hg_step_desc* d, float* params, float* grads, int64_t n,
+                              float lr, float inv_batch, int32_t update, void* stream);
+
+extern "C" int hg_allreduce_sgd_refresh(void* comm, const hg_step_desc* d, float* params,
+                                        float* grads, int64_t n, float lr, float inv_batch,
+                                        void* stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (comm) HG_NCCL_TRY(ncclAllReduce(grads, grads, (size_t)n, ncclFloat32, ncclSum,
+                                      (ncclComm_t)comm, s));
+  return hg_sgd_refresh(d, params, grads, n, lr, inv_batch, 1, stream);
+}
+
 extern "C" int hg_shift(void* comm, int rank, int nranks, int delta, const float* send0,
                         const float* send1, float* recv0, float* recv1, int64_t n, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
@@ -69,6 +81,10 @@ extern "C" int hg_nccl_unique_id(void*) { return hg_fail(HG_ENCCL, "built withou
 extern "C" int hg_nccl_init(const void*, int, int, void**) { return hg_fail(HG_ENCCL, "built without NCCL"); }
 extern "C" int hg_nccl_destroy(void*) { return HG_OK; }
 extern "C" int hg_allreduce_sgd(void*, float*, float*, int64_t, float, float, void*) {
+  return hg_fail(HG_ENCCL, "built without NCCL");
+}
+extern "C" int hg_allreduce_sgd_refresh(void*, const hg_step_desc*, float*, float*, int64_t, float,
+                                        float, void*) {
   return hg_fail(HG_ENCCL, "built without NCCL");
 }
 extern "C" int hg_shift(void*, int, int, int, const float*, const float*, float*, float*, int64_t,

@@ -407,12 +407,18 @@ class DistGraphLoop:
                 with torch.cuda.stream(self.side):
                     self.side_ops(nxt, self.side.cuda_stream)
                 cs = cap_s.cuda_stream
+                run.desc.lowp_fresh = 1 if run.tc else 0
                 _lib.call("hg_train_step", C.byref(run.desc), self.cap, cs)
+                run.desc.lowp_fresh = 0
                 if not os.environ.get("HG_DGL_NO_LOSS"):  # timing experiment knob
                     self.pin_loss[x].copy_(run.loss[:self.cap].sum().reshape(1),
                                            non_blocking=True)
                 if os.environ.get("HG_DGL_NO_ALLREDUCE"):  # timing experiment only
                     m.sgd(tr.lr, total, stream=cs)
+                elif run.tc:  # SGD refreshes the bf16 operands: steps skip their transposes
+                    _lib.call("hg_allreduce_sgd_refresh", tr._comm, C.byref(run.desc),
+                              m.flat.data_ptr(), m.grad.data_ptr(), m.flat.numel(),
+                              float(tr.lr), 1.0 / total, cs)
                 else:
                     _lib.call("hg_allreduce_sgd", tr._comm, m.flat.data_ptr(), m.grad.data_ptr(),
                               m.flat.numel(), float(tr.lr), 1.0 / total, cs)
@@ -613,7 +619,12 @@ class MicrographTrainer:
             # an eager run-ahead build of `it` may already have charged its ledger row
             self._acct_rows[it].zero_()
             self._g_it.fill_(it - 1)
-            gl.side_ops(gl.runners[x], torch.cuda.current_stream(self.device).cuda_stream)
+            cs = torch.cuda.current_stream(self.device).cuda_stream
+            gl.side_ops(gl.runners[x], cs)
+            if gl.runners[x].tc:  # replays start from bf16 operands matching the parameters
+                m = self.model
+                _lib.call("hg_sgd_refresh", C.byref(gl.runners[x].desc), m.flat.data_ptr(),
+                          m.grad.data_ptr(), m.flat.numel(), 0.0, 1.0, 0, cs)
             self._acct_iters = getattr(self, "_acct_iters", set())
             self._acct_iters.add(it)
         prev = None

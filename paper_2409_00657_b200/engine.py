@@ -121,8 +121,16 @@ class GraphLoop:
                                       n_roots=B, stream=ss)
                     _lib.call("hg_step_prologue", C.byref(nxt.desc), B, 1, ss)
                 cs = cap.cuda_stream
-                _lib.call("hg_train_step", C.byref(run.desc), B, cs)
-                tr.model.sgd(tr.lr, B, stream=cs)
+                m = tr.model
+                if run.tc:  # SGD refreshes the bf16 operands: the step skips its transposes
+                    run.desc.lowp_fresh = 1
+                    _lib.call("hg_train_step", C.byref(run.desc), B, cs)
+                    _lib.call("hg_sgd_refresh", C.byref(run.desc), m.flat.data_ptr(),
+                              m.grad.data_ptr(), m.flat.numel(), float(tr.lr), 1.0 / B, 1, cs)
+                    run.desc.lowp_fresh = 0
+                else:
+                    _lib.call("hg_train_step", C.byref(run.desc), B, cs)
+                    m.sgd(tr.lr, B, stream=cs)
                 if e2e:
                     self.pin_loss[x].copy_(run.loss[:B].sum().reshape(1), non_blocking=True)
                 cap.wait_stream(self.side)
@@ -228,6 +236,10 @@ class Trainer:
         r.n_roots = n
         _lib.call("hg_step_prologue", C.byref(r.desc), n, 1, s)
         r.desc.agg1_ready = 1
+        if r.tc:  # the replays' steps use the bf16 operands as the previous SGD left them
+            m = self.model
+            _lib.call("hg_sgd_refresh", C.byref(r.desc), m.flat.data_ptr(), m.grad.data_ptr(),
+                      m.flat.numel(), 0.0, 1.0, 0, s)
         self._it_dev.fill_(it)
 
     def roots_of(self, it: int) -> torch.Tensor:

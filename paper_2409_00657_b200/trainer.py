@@ -59,6 +59,8 @@ class CellRunner:
             d.in_dim[k] = model.in_dim[k]
         d.split_k = split_k or max(1, min(64, self.max_rows[1] // 2048))
         d.use_tc = int(use_tc)
+        # the step's tensor-core path (mirrors run_step's condition)
+        self.tc = act == torch.bfloat16 and use_tc and H % 64 == 0 and H <= 256
         d.features = table.table.data_ptr()
         d.feat_row = table.row_of.data_ptr() if table.row_of is not None else None
         d.roots = self.roots.data_ptr()
@@ -80,12 +82,19 @@ class CellRunner:
         d.logits = self.logits.data_ptr()
         d.loss = self.loss.data_ptr()
         d.lowp_scratch = self.lowp.data_ptr()
-        self.wb16 = torch.empty(model.flat.numel(), dtype=torch.bfloat16, device=dev)
+        # bf16 operand copies of the parameters: one set per model, shared by
+        # every runner (steps are serialised on the training stream), so a
+        # fused SGD + refresh (hg_sgd_refresh) keeps all of them current
+        if not hasattr(model, "_lowp"):
+            Cp_ = (model.C + 63) // 64 * 64
+            model._lowp = {
+                "wb16": torch.empty(model.flat.numel(), dtype=torch.bfloat16, device=dev),
+                "wct": torch.empty((model.C, H), dtype=torch.bfloat16, device=dev),
+                "wcp": torch.zeros((H, Cp_), dtype=torch.bfloat16, device=dev)}
+        self.wb16, self.wct, self.wcp = (model._lowp[k] for k in ("wb16", "wct", "wcp"))
         for k in range(1, L + 1):
             d.Wb[k] = self.wb16.data_ptr() + 2 * int(model.offsets[k - 1])
         Cp = (model.C + 63) // 64 * 64
-        self.wct = torch.empty((model.C, H), dtype=torch.bfloat16, device=dev)
-        self.wcp = torch.zeros((H, Cp), dtype=torch.bfloat16, device=dev)
         self.dl16 = torch.zeros((max_roots, Cp), dtype=torch.bfloat16, device=dev)
         d.WcT, d.Wcp, d.dl_lowp = self.wct.data_ptr(), self.wcp.data_ptr(), self.dl16.data_ptr()
         self.desc = d
