@@ -247,13 +247,8 @@ __global__ void __launch_bounds__(256)
 k_pg_serve(const uint64_t* __restrict__ boxes, int rank, int S, Mailbox m, const int64_t* seq,
            const int32_t* __restrict__ home, const int32_t* __restrict__ local_row,
            const uint8_t* __restrict__ shard, int row_bytes, int stage_cap, int* err) {
-  __shared__ int ok;
-  if (threadIdx.x == 0) ok = spin_peers(boxes, rank, S, m.o_flags, *seq) ? 1 : 0;
-  __syncthreads();
-  if (!ok) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) raise_flag(err, HG_EINVARIANT);
-    return;
-  }
+  // the requests are ready: k_pg_wait (one CTA) polled the peers' signals, so
+  // these CTAs never occupy SM slots while spinning
   const int vec = row_bytes / 16;
   const int hw = (blockIdx.x * blockDim.x + threadIdx.x) / 16, hl = threadIdx.x & 15;
   const int n_hw = gridDim.x * blockDim.x / 16;
@@ -294,7 +289,7 @@ extern "C" int hg_pregather_push(const int32_t* ids, const int32_t* n_dev, const
   uint8_t* own = (uint8_t*)own_box;
   int32_t* count = (int32_t*)(own + o_count);
   HG_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t), s));
-  count_launch(5);
+  count_launch(6);
   prof_begin(PROF_PG_MARK, s);
   k_stage_mark_stamp<<<148 * 2, 256, 0, s>>>(ids, n_dev, home, rank, n_ranks, stamp, seq,
                                              (int32_t*)(own + o_list), stage_row, count,
@@ -303,6 +298,7 @@ extern "C" int hg_pregather_push(const int32_t* ids, const int32_t* n_dev, const
   prof_end(PROF_PG_MARK, s);
   prof_begin(PROF_PG_COPY, s);
   k_pg_signal<<<1, 32, 0, s>>>(bx, rank, n_ranks, m, seq, o_flags);          // requests ready
+  k_pg_wait<<<1, 32, 0, s>>>(bx, rank, n_ranks, m, seq, o_flags, err);       // peers' requests
   k_pg_serve<<<148 * 2, 256, 0, s>>>(bx, rank, n_ranks, m, seq, home, local_row,
                                      (const uint8_t*)shard, row_bytes, stage_cap, err);
   k_pg_signal<<<1, 32, 0, s>>>(bx, rank, n_ranks, m, seq, o_done);           // my rows written

@@ -376,69 +376,86 @@ class PeerFeatures:
 
 class DistGraphLoop:
     """CUDA-graph replay of the multi-GPU fast path (fused mode, initial trace
-    table, NVLink device pre-gather).  Like engine.GraphLoop, two graphs
-    alternate runners; the forked branch stages this rank's roots of the next
-    iteration from a device cursor (hg_iter_stage_ranged: variable count, at
-    most `cap`), builds them (device root count), pre-gathers their remote rows
-    over NVLink (per-iteration ledger row chosen by the cursor) and runs the
-    layer-1 gather; the main branch trains the current runner, copies the
-    summed loss to a pinned slot, and runs the NCCL all-reduce + SGD.  Root
-    count capacity `cap` pads with empty micrographs, which contribute
-    nothing (zero loss rows and gradients)."""
+    table, NVLink push pre-gather) as a three-stage pipeline over three
+    runners.  Replay x (iteration it, x = it % 3) runs three branches:
+
+      build  : stage this rank's roots of it+2 from the device cursor
+               (hg_iter_stage_ranged: variable count, at most `cap`) and
+               build their micrographs (device root count) into runner x+2;
+      gather : pre-gather the remote rows of it+1 (built by the previous
+               replay) over NVLink into runner x+1's staging (ledger row from
+               a second cursor) and run its layer-1 gather;
+      train  : train runner x, copy the summed loss to a pinned slot, NCCL
+               all-reduce + SGD (+ bf16 operand refresh).
+
+    so sampling, the cross-GPU exchange and training of three consecutive
+    iterations overlap.  Root count capacity `cap` pads with empty
+    micrographs, which contribute nothing (zero loss rows and gradients)."""
 
     def __init__(self, tr: "MicrographTrainer", cap: int):
         self.tr, self.cap = tr, int(cap)
         dev = tr.device
-        self.runners = tr.runners[:2]
-        self.side = torch.cuda.Stream(dev)
-        self.pin_loss = [torch.zeros(1, dtype=torch.float32).pin_memory() for _ in range(2)]
+        self.runners = tr.runners[:3]
+        self.side_build = torch.cuda.Stream(dev)
+        self.side_gather = torch.cuda.Stream(dev)
+        self.pin_loss = [torch.zeros(1, dtype=torch.float32).pin_memory() for _ in range(3)]
+        self._dummy = torch.zeros(2, dtype=torch.int64, device=dev)
         m = tr.model
         total = tr.S * tr.B
         self.graphs = []
         cur = torch.cuda.current_stream(dev)
         before = _lib.launch_count()
-        for x in range(2):
-            run, nxt = self.runners[x], self.runners[1 - x]
+        for x in range(3):
+            run, nxt, nxt2 = (self.runners[(x + j) % 3] for j in range(3))
             g = torch.cuda.CUDAGraph()
             cap_s = torch.cuda.Stream(dev)
             cap_s.wait_stream(cur)
             with torch.cuda.graph(g, stream=cap_s):
-                self.side.wait_stream(cap_s)
-                with torch.cuda.stream(self.side):
-                    self.side_ops(nxt, self.side.cuda_stream)
+                self.side_build.wait_stream(cap_s)
+                self.side_gather.wait_stream(cap_s)
+                with torch.cuda.stream(self.side_build):
+                    self.build_ops(nxt2, self.side_build.cuda_stream)
+                with torch.cuda.stream(self.side_gather):
+                    self.gather_ops(nxt, self.side_gather.cuda_stream)
                 cs = cap_s.cuda_stream
                 run.desc.lowp_fresh = 1 if run.tc else 0
                 _lib.call("hg_train_step", C.byref(run.desc), self.cap, cs)
                 run.desc.lowp_fresh = 0
-                if not os.environ.get("HG_DGL_NO_LOSS"):  # timing experiment knob
-                    self.pin_loss[x].copy_(run.loss[:self.cap].sum().reshape(1),
-                                           non_blocking=True)
-                if os.environ.get("HG_DGL_NO_ALLREDUCE"):  # timing experiment only
-                    m.sgd(tr.lr, total, stream=cs)
-                elif run.tc:  # SGD refreshes the bf16 operands: steps skip their transposes
+                self.pin_loss[x].copy_(run.loss[:self.cap].sum().reshape(1), non_blocking=True)
+                if run.tc:  # SGD refreshes the bf16 operands: steps skip their transposes
                     _lib.call("hg_allreduce_sgd_refresh", tr._comm, C.byref(run.desc),
                               m.flat.data_ptr(), m.grad.data_ptr(), m.flat.numel(),
                               float(tr.lr), 1.0 / total, cs)
                 else:
                     _lib.call("hg_allreduce_sgd", tr._comm, m.flat.data_ptr(), m.grad.data_ptr(),
                               m.flat.numel(), float(tr.lr), 1.0 / total, cs)
-                cap_s.wait_stream(self.side)
+                cap_s.wait_stream(self.side_build)
+                cap_s.wait_stream(self.side_gather)
             cur.wait_stream(cap_s)
             self.graphs.append(g)
-        self.launches = (_lib.launch_count() - before) // 2
+        self.launches = (_lib.launch_count() - before) // 3
         self.iters = tr.iters
 
-    def side_ops(self, r: CellRunner, s) -> None:
-        """Stage (cursor -> cursor + 1), build, pre-gather and layer-1 gather of
-        the iteration after the cursor into runner r."""
+    def build_ops(self, r: CellRunner, s) -> None:
+        """Build cursor -> cursor + 1: stage and build that iteration into r."""
         tr = self.tr
         _lib.call("hg_iter_stage_ranged", tr._g_roots.data_ptr(), tr._g_ranges.data_ptr(),
                   tr._g_states.data_ptr(), tr.iters, tr._g_it.data_ptr(), self.cap, 1, 1,
                   r.roots.data_ptr(), r.n_dev.data_ptr(), r.keys.data_ptr(), s)
         r.builder.build(tr.graph, r.roots.data_ptr(), r.keys.data_ptr(), self.cap,
                         n_roots=self.cap, stream=s, n_dev=r.n_dev.data_ptr())
+
+    def gather_ops(self, r: CellRunner, s) -> None:
+        """Gather cursor -> cursor + 1: pre-gather (ledger row = that iteration)
+        and the layer-1 gather of runner r, already built."""
+        tr = self.tr
+        # advance the gather cursor (cap 0: nothing staged)
+        _lib.call("hg_iter_stage_ranged", tr._g_roots.data_ptr(), tr._g_ranges.data_ptr(),
+                  tr._g_states.data_ptr(), tr.iters, tr._g_pg.data_ptr(), 0, 1, 1,
+                  self._dummy.data_ptr(), self._dummy.data_ptr(),
+                  self._dummy.data_ptr() + 8, s)
         tr.feats.pregather(r, tr._acct_rows.data_ptr(), tr._acct_total.data_ptr(), s,
-                           it_dev_ptr=tr._g_it.data_ptr())
+                           it_dev_ptr=tr._g_pg.data_ptr())
         _lib.call("hg_step_prologue", C.byref(r.desc), self.cap, 1, s)
 
     def replay(self, x: int) -> None:
@@ -581,6 +598,7 @@ class MicrographTrainer:
             self._g_ranges = torch.empty((it_n, 2), dtype=torch.int64, device=dev)
             self._g_states = torch.empty(it_n, dtype=torch.int64, device=dev)
             self._g_it = torch.zeros(1, dtype=torch.int64, device=dev)
+            self._g_pg = torch.zeros(1, dtype=torch.int64, device=dev)
             self._dgl = None
         self._g_roots.copy_(torch.from_numpy(np.ascontiguousarray(roots)))
         self._g_ranges.copy_(torch.from_numpy(np.ascontiguousarray(ranges)))
@@ -596,7 +614,11 @@ class MicrographTrainer:
             if self._eager_fast < 2 or not hasattr(self, "_ra"):
                 return None
             self._drain_run_ahead()
-            for r in self.runners[:2]:
+            while len(self.runners) < 3:  # a third runner for the three-stage pipeline
+                self.runners.append(CellRunner(self.graph, self.runners[0].table, self.model,
+                                               self.fanout, self.runners[0].max_roots,
+                                               self.labels))
+            for r in self.runners[:3]:
                 r.desc.roots = r.roots.data_ptr()
                 r.desc.agg1_ready = 1
                 self.feats.bind_staged(r, self._stage_cap)
@@ -609,8 +631,10 @@ class MicrographTrainer:
             self._ra.reset()
 
     def _step_graph(self, gl: DistGraphLoop, it: int, want_loss: bool):
-        x = it % 2
-        if self._gnext != it:  # position the loop: build `it` eagerly into runner x
+        x = it % 3
+        if self._gnext != it:
+            # position the pipeline: `it` built + pre-gathered + layer-1 gathered
+            # into runner x, it+1 built into runner x+1 (eagerly, on this stream)
             self._drain_run_ahead()
             for r in gl.runners:  # the general cell path may have rebound these
                 r.desc.roots = r.roots.data_ptr()
@@ -618,9 +642,12 @@ class MicrographTrainer:
                 self.feats.bind_staged(r, self._stage_cap)
             # an eager run-ahead build of `it` may already have charged its ledger row
             self._acct_rows[it].zero_()
-            self._g_it.fill_(it - 1)
             cs = torch.cuda.current_stream(self.device).cuda_stream
-            gl.side_ops(gl.runners[x], cs)
+            self._g_it.fill_(it - 1)
+            self._g_pg.fill_(it - 1)
+            gl.build_ops(gl.runners[x], cs)
+            gl.gather_ops(gl.runners[x], cs)
+            gl.build_ops(gl.runners[(x + 1) % 3], cs)
             if gl.runners[x].tc:  # replays start from bf16 operands matching the parameters
                 m = self.model
                 _lib.call("hg_sgd_refresh", C.byref(gl.runners[x].desc), m.flat.data_ptr(),
@@ -628,10 +655,10 @@ class MicrographTrainer:
             self._acct_iters = getattr(self, "_acct_iters", set())
             self._acct_iters.add(it)
         prev = None
-        # pin slot x was written by the replay two steps back: read it before reuse
-        if self._loss_pending and self._loss_pending[0][1] is gl.pin_loss[x]:
+        # pin slot x was written by the replay three steps back: read it before reuse
+        while self._loss_pending and any(b is gl.pin_loss[x] for _, b in self._loss_pending):
             prev = self._drain_loss()
-        gl.replay(x)  # trains `it`, builds + pre-gathers it+1, all-reduce + SGD
+        gl.replay(x)  # trains `it`, pre-gathers it+1, builds it+2, all-reduce + SGD
         ev = torch.cuda.Event()
         ev.record()
         self._loss_pending.append((ev, gl.pin_loss[x]))
@@ -773,8 +800,8 @@ class MicrographTrainer:
         self._eager_fast += 1
         if self._gnext is not None:
             if self._gnext == it and self._dgl is not None:
-                # the graph loop already built `it` into runner it%2: train it here
-                return self._train_built(self._dgl.runners[it % 2], it, want_loss)
+                # the graph loop already built `it` into runner it%3: train it here
+                return self._train_built(self._dgl.runners[it % 3], it, want_loss)
             self._drain_run_ahead()
             self._gnext = None
         if self.pregather:  # staging exchange needs host-known sizes: no run-ahead
