@@ -101,6 +101,10 @@ int hg_iter_stage_ranged(const int64_t* roots, const int64_t* ranges, const uint
                          int32_t advance, int64_t* roots_out, int32_t* n_out, uint64_t* key_out,
                          void* stream);
 
+/* mix64 throughput probe (blocks x 256 threads x per_thread hashes): the
+ * measured integer ceiling the sampler's hashes/s are reported against. */
+int hg_bench_mix64(int32_t blocks, int64_t per_thread, uint64_t* sink, void* stream);
+
 /* Glorot init (model.py:87-90): out f64 or f32 [rows*cols] row-major. */
 int hg_glorot(int32_t rows, int32_t cols, uint64_t state, int32_t dtype, void* out,
               void* stream);

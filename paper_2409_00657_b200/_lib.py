@@ -87,6 +87,7 @@ SIGNATURES = {
     "hg_epoch_permutation": [I64, U64, V, V, PSZ, V],
     "hg_glorot": [I32, I32, U64, I32, V, V],
     "hg_iter_stage": [V, V, I64, V, I32, I32, I32, V, V, V],
+    "hg_bench_mix64": [I32, I64, V, V],
     "hg_iter_stage_ranged": [V, V, V, I64, V, I32, I32, I32, V, V, V, V],
     "hg_graph_raw_degrees": [C.POINTER(GraphTables), V, V],
     "hg_graph_fill": [C.POINTER(GraphTables), I64, I64, V, V, V],

@@ -171,6 +171,27 @@ extern "C" int hg_iter_stage_ranged(const int64_t* roots, const int64_t* ranges,
   return HG_OK;
 }
 
+// Throughput ceiling of the sampler's hash (the "integer-ALU roofline" of
+// k_mg_build): every thread runs `per_thread` dependent-free
+// mix64 evaluations (4 independent chains) and folds them into a sink.
+__global__ void k_mix64_peak(int64_t per_thread, uint64_t* sink) {
+  uint64_t a = threadIdx.x, b = blockIdx.x, c = a ^ 0x1234, d = b ^ 0x9876;
+  for (int64_t i = 0; i < per_thread; i += 4) {
+    a = mix64(a ^ (uint64_t)i);
+    b = mix64(b ^ (uint64_t)i);
+    c = mix64(c ^ (uint64_t)i);
+    d = mix64(d ^ (uint64_t)i);
+  }
+  if ((a ^ b ^ c ^ d) == 0x5eed) sink[0] = a;  // keeps the chains live
+}
+
+extern "C" int hg_bench_mix64(int32_t blocks, int64_t per_thread, uint64_t* sink, void* stream) {
+  count_launch();
+  k_mix64_peak<<<blocks, 256, 0, (cudaStream_t)stream>>>(per_thread, sink);
+  HG_CUDA_TRY(cudaGetLastError());
+  return HG_OK;
+}
+
 extern "C" int hg_glorot(int32_t rows, int32_t cols, uint64_t state, int32_t dtype, void* out,
                          void* stream) {
   const int64_t total = (int64_t)rows * cols;
