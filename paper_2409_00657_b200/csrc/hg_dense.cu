@@ -107,8 +107,17 @@ template <typename T, bool SAGE>
 __global__ void __launch_bounds__(256)
 k_aggregate(RowSrc<T> rs, const int32_t* __restrict__ self_pos,
             const int32_t* __restrict__ nbr_off, const int32_t* __restrict__ nbr_idx,
-            const int32_t* __restrict__ n_rows_dev, int W, T* __restrict__ out, int out_ld) {
+            const int32_t* __restrict__ n_rows_dev, int W, T* __restrict__ out, int out_ld,
+            int pad_cap) {
   constexpr int VEC = Vec<T>::N;
+  if (pad_cap && blockIdx.x == gridDim.x - 1) {
+    // the tensor-core dW GEMM reduces over rows up to the next multiple of 64:
+    // keep those padding rows zero (folded in here instead of its own launch)
+    const int n = *n_rows_dev;
+    const int pad = min(pad_cap, (n + 63) / 64 * 64);
+    for (int64_t i = threadIdx.x; i < (int64_t)(pad - n) * out_ld; i += blockDim.x)
+      out[(int64_t)n * out_ld + i] = from_f<T>(0.f);
+  }
   const int nvec = W / VEC;                        // vectors per row
   const int G = nvec >= 32 ? 32 : (nvec >= 16 ? 16 : (nvec >= 8 ? 8 : (nvec >= 4 ? 4 : (nvec >= 2 ? 2 : 1))));
   const int groups_per_block = blockDim.x / G;
@@ -685,19 +694,16 @@ static void launch_aggregate(const hg_step_desc* d, int k, cudaStream_t s, bool 
   RowSrc<T> rs{src, Wd, ids0, k == 1 ? d->feat_row : nullptr,
                k == 1 ? (const T* const*)d->feat_peers : nullptr, d->feat_home,
                (const T*)d->stage_base, k == 1 ? d->stage_row : nullptr, d->rank};
+  const int pad_cap = pad && sizeof(T) == 2 ? d->max_rows[k] : 0;
   if (d->arch == 1)
     k_aggregate<T, true><<<nb, 256, 0, s>>>(rs, d->mg.self_pos[k], d->mg.nbr_off[k],
                                             d->mg.nbr_idx[k], tot + k, Wd, (T*)d->agg[k],
-                                            d->in_dim[k]);
+                                            d->in_dim[k], pad_cap);
   else
     k_aggregate<T, false><<<nb, 256, 0, s>>>(rs, d->mg.self_pos[k], d->mg.nbr_off[k],
                                              d->mg.nbr_idx[k], tot + k, Wd, (T*)d->agg[k],
-                                             d->in_dim[k]);
+                                             d->in_dim[k], pad_cap);
   prof_end(k == 1 ? PROF_AGG1 : PROF_AGG2, s);
-  if (pad && sizeof(T) == 2) {
-    count_launch();
-    k_zero_pad_rows<<<4, 256, 0, s>>>((bf16*)d->agg[k], tot + k, d->in_dim[k], d->max_rows[k]);
-  }
 }
 
 constexpr size_t kScatterSmem = 96 * 1024;
