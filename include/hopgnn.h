@@ -166,6 +166,11 @@ typedef struct {
   int32_t* nbr_idx[HG_MAX_LAYERS + 1];   /* k>=1: need[k-1] row of each pair's source  */
   int32_t* pair_off[HG_MAX_LAYERS + 1];  /* k>=1: [R+1] first pair of each root         */
   int32_t* totals;                       /* [2L+2]: N_0..N_L, P_1..P_L, err             */
+  /* layer 1 by vertex id (the feature gather skips the need[0] indirection):
+   * nbr_vid1[j] = need_ids[0][nbr_idx[1][j]], self_vid1[a] = need_ids[1][a]
+   * row; NULL = not produced */
+  int32_t* nbr_vid1;
+  int32_t* self_vid1;
 } hg_mg_batch;
 
 /* Fill capacities / smem / workspace for a fanout list; returns HG_ECONFIG if

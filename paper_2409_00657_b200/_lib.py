@@ -34,7 +34,8 @@ _P7 = C.c_void_p * (MAX_LAYERS + 1)
 
 class MgBatch(C.Structure):
     _fields_ = [("need_ids", _P7), ("need_off", _P7), ("in_layer", _P7), ("self_pos", _P7),
-                ("nbr_off", _P7), ("nbr_idx", _P7), ("pair_off", _P7), ("totals", C.c_void_p)]
+                ("nbr_off", _P7), ("nbr_idx", _P7), ("pair_off", _P7), ("totals", C.c_void_p),
+                ("nbr_vid1", C.c_void_p), ("self_vid1", C.c_void_p)]
 
 
 class GraphTables(C.Structure):

@@ -90,9 +90,14 @@ struct RowSrc {
   const T* stage;             // staged mode: remote rows pre-gathered into HBM
   const int32_t* stage_row;
   int rank;
+  bool by_vid;                // index arrays hold vertex ids (layer 1 vid lists)
   __device__ __forceinline__ const T* row(int i) const {
+    if (by_vid) return vrow(i);
     if (!need_ids0) return src + (int64_t)i * ld;
-    const int v = need_ids0[i];
+    return vrow(need_ids0[i]);
+  }
+  // row of vertex v (layer 1 with vertex-id pair lists)
+  __device__ __forceinline__ const T* vrow(int v) const {
     if (stage_row) {
       if (home[v] != rank) return stage + (int64_t)stage_row[v] * ld;
       return src + (int64_t)feat_row[v] * ld;
@@ -691,18 +696,20 @@ static void launch_aggregate(const hg_step_desc* d, int k, cudaStream_t s, bool 
   const int32_t* ids0 = k == 1 ? d->mg.need_ids[0] : nullptr;
   prof_begin(k == 1 ? PROF_AGG1 : PROF_AGG2, s);
   count_launch();
+  // layer 1: pair lists by vertex id (one dependent load fewer per source row)
+  const bool vid = k == 1 && d->mg.nbr_vid1 && d->mg.self_vid1;
   RowSrc<T> rs{src, Wd, ids0, k == 1 ? d->feat_row : nullptr,
                k == 1 ? (const T* const*)d->feat_peers : nullptr, d->feat_home,
-               (const T*)d->stage_base, k == 1 ? d->stage_row : nullptr, d->rank};
+               (const T*)d->stage_base, k == 1 ? d->stage_row : nullptr, d->rank, vid};
+  const int32_t* selfv = vid ? d->mg.self_vid1 : d->mg.self_pos[k];
+  const int32_t* nbrv = vid ? d->mg.nbr_vid1 : d->mg.nbr_idx[k];
   const int pad_cap = pad && sizeof(T) == 2 ? d->max_rows[k] : 0;
   if (d->arch == 1)
-    k_aggregate<T, true><<<nb, 256, 0, s>>>(rs, d->mg.self_pos[k], d->mg.nbr_off[k],
-                                            d->mg.nbr_idx[k], tot + k, Wd, (T*)d->agg[k],
-                                            d->in_dim[k], pad_cap);
+    k_aggregate<T, true><<<nb, 256, 0, s>>>(rs, selfv, d->mg.nbr_off[k], nbrv, tot + k, Wd,
+                                            (T*)d->agg[k], d->in_dim[k], pad_cap);
   else
-    k_aggregate<T, false><<<nb, 256, 0, s>>>(rs, d->mg.self_pos[k], d->mg.nbr_off[k],
-                                             d->mg.nbr_idx[k], tot + k, Wd, (T*)d->agg[k],
-                                             d->in_dim[k], pad_cap);
+    k_aggregate<T, false><<<nb, 256, 0, s>>>(rs, selfv, d->mg.nbr_off[k], nbrv, tot + k, Wd,
+                                             (T*)d->agg[k], d->in_dim[k], pad_cap);
   prof_end(k == 1 ? PROF_AGG1 : PROF_AGG2, s);
 }
 

@@ -654,10 +654,14 @@ k_mg_finalize(const int32_t* __restrict__ ws, int n_roots, MgCarve c, hg_mg_batc
     for (int a = threadIdx.x; a < nk; a += blockDim.x) {
       out.self_pos[k][base + a] = prev_base + w[c.ws_self[k] + a];
       out.nbr_off[k][base + a] = pbase + w[c.ws_rowoff[k] + a];
+      if (k == 1 && out.self_vid1) out.self_vid1[base + a] = w[c.ws_need[1] + a];
     }
     const int pk = w[c.ws_cnt + L + k];
-    for (int t = threadIdx.x; t < pk; t += blockDim.x)
-      out.nbr_idx[k][pbase + t] = prev_base + w[c.ws_nbr[k] + t];
+    for (int t = threadIdx.x; t < pk; t += blockDim.x) {
+      const int q = w[c.ws_nbr[k] + t];
+      out.nbr_idx[k][pbase + t] = prev_base + q;
+      if (k == 1 && out.nbr_vid1) out.nbr_vid1[pbase + t] = w[c.ws_need[0] + q];
+    }
   }
 }
 

@@ -190,6 +190,8 @@ class MicrographBuilder:
                 t["nbr_idx"][k] = torch.empty(max(R * lay.cap_lay[k - 1], 1), **i32)
                 t["pair_off"][k] = torch.zeros(R + 1, **i32)
         t["totals"] = torch.zeros(2 * L + 2, **i32)
+        t["nbr_vid1"] = torch.empty(max(R * lay.cap_lay[0], 1), **i32)
+        t["self_vid1"] = torch.empty(max(R * lay.cap_need[1], 1), **i32)
         self.tensors = t
         self.err = torch.zeros(1, **i32)
         self.cbatch = _lib.MgBatch()
@@ -200,6 +202,8 @@ class MicrographBuilder:
                 x = t[name][k]
                 arr[k] = x.data_ptr() if x is not None else None
         self.cbatch.totals = t["totals"].data_ptr()
+        self.cbatch.nbr_vid1 = t["nbr_vid1"].data_ptr()
+        self.cbatch.self_vid1 = t["self_vid1"].data_ptr()
 
     def build(self, g: Graph, roots: torch.Tensor, keys: torch.Tensor, roots_per_state: int,
               n_roots: int = None, stream=None, n_dev: int = None) -> MicrographBatch:
