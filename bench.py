@@ -182,7 +182,7 @@ def gather_bytes(sizes_per_step, cfg, e_f=2, e_a=2):
     return tot
 
 
-def sampler_roofline(runner, g, cfg, build_site, dev):
+def sampler_roofline(runner, g, cfg, build_site, dev, group=1):
     """Hashes/s of the micrograph build against a measured mix64 ceiling
     (hashes = sum over frontier vertices with degree > fanout of
     their degree; one mix64 per hashed slot)."""
@@ -211,7 +211,7 @@ def sampler_roofline(runner, g, cfg, build_site, dev):
     e1.record()
     torch.cuda.synchronize()
     peak = 5 * blocks * 256 * per / (e0.elapsed_time(e1) / 1e3)
-    build_s = build_site[0] / max(build_site[1], 1) / 1e3
+    build_s = build_site[0] / max(build_site[1], 1) / 1e3 / group  # per batch
     achieved = hashes / build_s if build_s > 0 else None
     return {"bound": "int-alu (mix64)", "kernel": "k_mg_build (+ scan, finalize)",
             "hashes_per_batch": hashes, "achieved": round(achieved / 1e9, 2) if achieved else None,
@@ -260,46 +260,70 @@ def _run_ours(args, cfg, dev):
     model = init_model(cfg["arch"], cfg["dim"], cfg["hidden"], len(cfg["fanout"]),
                        cfg["classes"], chain(cfg["seed"], 0x07), dev)
     B = cfg["batch"]
-    tr = Trainer(g, table, model, cfg["fanout"], B, cfg["seed"])
+    G = max(1, int(args.group))
+    tr = Trainer(g, table, model, cfg["fanout"], B, cfg["seed"], group=G)
     iters = tr.begin_epoch(0)
     torch.cuda.synchronize()
     setup_s = time.time() - t0
     K, W = args.steps, args.warmup
-    if 2 * W + 3 * K + 1 > iters:
+    if G > 1:  # warm-up covers two eager steps and one replay of each group graph
+        W = max(W, 2 + 2 * G)
+    if 2 * W + 3 * K + 2 * G + 1 > iters:
         raise SystemExit("epoch too short for the requested steps")
     for i in range(W):
-        tr.step(i)
+        tr.step(i, stop=W)
     torch.cuda.synchronize()
     tr.check()
     L = len(cfg["fanout"])
     totals = torch.zeros((K, 2 * L + 2), dtype=torch.int32, device=dev)
     _lib.launch_count(reset=True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # timed region: the steady-state loop, replayed as CUDA graphs (GraphLoop)
+    replays = 0
+    # timed region: the steady-state loop, replayed as CUDA graphs (GraphLoop /
+    # GroupLoop); iterations that do not fill a whole group run eagerly
     with Clocks(0) as clk:
         ev0.record()
         h0 = time.perf_counter()
         for i in range(K):
-            tr.step(W + i)
-            totals[i].copy_(tr.last_runner.builder.tensors["totals"], non_blocking=True)
+            tr.step(W + i, stop=W + K)
+            lg = getattr(tr, "last_group", None)
+            if G > 1 and lg is not None and lg[0] == W + i:
+                replays += 1
+                for b, r in enumerate(lg[1]):
+                    totals[i + b].copy_(r.builder.tensors["totals"], non_blocking=True)
+            elif G == 1 or lg is None or not lg[0] <= W + i < lg[0] + G:
+                totals[i].copy_(tr.last_runner.builder.tensors["totals"], non_blocking=True)
         host_ms = (time.perf_counter() - h0) * 1000.0 / K
         ev1.record()
         torch.cuda.synchronize()
-    graph_on = tr._gl is not None
-    launches = K * tr._gl.launches + _lib.launch_count() if graph_on else _lib.launch_count()
+    if G > 1:
+        graph_on = tr._gg is not None
+        per_graph = tr._gg.launches if graph_on else None
+        launches = replays * per_graph + _lib.launch_count() if graph_on else _lib.launch_count()
+    else:
+        graph_on = tr._gl is not None
+        per_graph = tr._gl.launches if graph_on else None
+        launches = K * per_graph + _lib.launch_count() if graph_on else _lib.launch_count()
     ms = ev0.elapsed_time(ev1)
     tr.check()
     tot = totals.cpu().numpy()
     sizes = [(int(r[0]), int(r[1]), int(r[L + 1])) for r in tot]
     value = K * B / (ms / 1000.0)
     # per-kernel timing: graph replays hide individual launches from CUDA events,
-    # so the same loop runs eagerly for K more steps with event sites on
+    # so the same loop body runs eagerly (with groups: one grouped build, one
+    # grouped gather, G steps per group) for K more iterations with event sites on
     tr.graphs = False
     _lib.prof_enable(True)
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     p0.record()
-    for i in range(K):
-        tr.step(W + K + i)
+    if G > 1 and tr._gg is not None:
+        n_prof = max(1, K // G) * G
+        for j in range(n_prof // G):
+            tr._gg.run_eager(W + K + j * G)
+    else:
+        n_prof = K
+        for i in range(K):
+            tr.step(W + K + i)
     p1.record()
     torch.cuda.synchronize()
     eager_ms = p0.elapsed_time(p1)
@@ -312,27 +336,49 @@ def _run_ours(args, cfg, dev):
                                                       ("sgd", _lib.PROF_SGD))}
     _lib.prof_enable(False)
     tr.graphs = True
-    sampler_roof = sampler_roofline(tr.last_runner, g, cfg, sites["build"], dev)
+    tr.check()
+    sampler_roof = sampler_roofline(tr.last_runner, g, cfg, sites["build"], dev, G)
     # end-to-end through the public API: pinned host roots in, loss out, every step
-    E0 = W + 2 * K  # e2e iterations: W untimed warm-up, then K timed
-    perm_host = tr.perm[E0 * B:(E0 + W + K + 1) * B].cpu().pin_memory()
+    E0 = W + 2 * K + 2 * G  # e2e iterations: W untimed warm-up, then K timed
+    perm_host = tr.perm[E0 * B:(E0 + W + K + 2 * G + 1) * B].cpu().pin_memory()
 
-    def host_roots(j):
-        return perm_host[j * B:(j + 1) * B]
+    def host_roots(j, n=1):
+        return perm_host[j * B:(j + n) * B]
 
-    for j in range(W):
-        tr.train_step(host_roots(j), E0 + j, host_roots(j + 1))
-    tr.last_loss()
-    torch.cuda.synchronize()
-    e0 = time.perf_counter()
-    for j in range(W, W + K):
-        tr.train_step(host_roots(j), E0 + j, host_roots(j + 1) if j + 1 < W + K else None)
-    tr.last_loss()  # the final step's loss reaches the host inside the timed region
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - e0
+    if G > 1:
+        # train_group: G iterations per call (the loader hands out G batches)
+        Wg = W // G
+        for j in range(Wg):
+            tr.train_group(host_roots(j * G, G), E0 + j * G, host_roots((j + 1) * G, G))
+        tr.last_group_loss()
+        torch.cuda.synchronize()
+        j0 = Wg * G
+        ng = K // G
+        e0 = time.perf_counter()
+        for j in range(ng):
+            a = j0 + j * G
+            nxt = host_roots(a + G, G) if (j + 1 < ng) else None
+            tr.train_group(host_roots(a, G), E0 + a, nxt)
+        tr.last_group_loss()
+        for j in range(j0 + ng * G, j0 + K):  # the remainder, one public step each
+            tr.train_step(host_roots(j), E0 + j, host_roots(j + 1) if j + 1 < j0 + K else None)
+        tr.last_loss()  # the final losses reach the host inside the timed region
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - e0
+    else:
+        for j in range(W):
+            tr.train_step(host_roots(j), E0 + j, host_roots(j + 1))
+        tr.last_loss()
+        torch.cuda.synchronize()
+        e0 = time.perf_counter()
+        for j in range(W, W + K):
+            tr.train_step(host_roots(j), E0 + j, host_roots(j + 1) if j + 1 < W + K else None)
+        tr.last_loss()  # the final step's loss reaches the host inside the timed region
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - e0
     e2e = K * B / e2e_s
     hbm, tflops, peak_kind = peaks()
-    bytes_per_launch = gather_bytes(sizes, cfg) / K
+    bytes_per_launch = gather_bytes(sizes, cfg) / K * (G if G > 1 else 1)
     agg_avg_s = agg_ms / max(agg_n, 1) / 1000.0
     achieved = bytes_per_launch / agg_avg_s / 1e9
     traffic = None
@@ -347,7 +393,8 @@ def _run_ours(args, cfg, dev):
         "n_gpus": 1, "steps": K, "warmup": W, "ms_per_step": round(ms / K, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (GPU-generated graph, keyed features/labels/weights)",
-        "config": {"workload": cfg["workload"], "global_batch": B, "fanout": list(cfg["fanout"]),
+        "config": {"workload": cfg["workload"], "global_batch": B, "run_ahead_group": G,
+                   "fanout": list(cfg["fanout"]),
                    "hidden": cfg["hidden"], "n_vertices": g.n_vertices, "n_edges": g.n_targets,
                    "parallelism": "single GPU (S=1: micrograph == model-centric)",
                    "l2": "inputs larger than L2 (CSR 6.4 GB, features 28 GB)"},
@@ -360,14 +407,18 @@ def _run_ours(args, cfg, dev):
                      "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "peak_source": peak_kind,
                      "bytes_per_launch": int(bytes_per_launch),
+                     "iterations_per_launch": G,
                      "avg_launch_us": round(agg_avg_s * 1e6, 2)},
         "roofline_sampler": sampler_roof,
-        "kernel_ms_per_step": {k: round(v[0] / max(v[1], 1), 4) for k, v in sites.items()},
-        "loop": {"cuda_graphs": graph_on,
-                 "launches_per_graph": tr._gl.launches if graph_on else None,
-                 "eager_ms_per_step": round(eager_ms / K, 4),
-                 "note": "value/ms_per_step: graph replays; kernel_ms_per_step and roofline: "
-                         "the same loop run eagerly for K more steps with CUDA-event sites"},
+        "kernel_ms_per_launch": {k: round(v[0] / max(v[1], 1), 4) for k, v in sites.items()},
+        "loop": {"cuda_graphs": graph_on, "group": G,
+                 "launches_per_graph": per_graph,
+                 "eager_ms_per_step": round(eager_ms / n_prof, 4),
+                 "note": "value/ms_per_step: graph replays (a replay trains a group of G "
+                         "iterations; build and layer-1 gather launch once per group); "
+                         "kernel_ms_per_launch and roofline: the same loop body run eagerly "
+                         "with CUDA-event sites (build / agg1 per group launch, the others "
+                         "per iteration)"},
         "batch_sizes_mean": {"N0": float(np.mean([s[0] for s in sizes])),
                              "N1": float(np.mean([s[1] for s in sizes])),
                              "P0": float(np.mean([s[2] for s in sizes]))},
@@ -612,6 +663,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="papers", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--group", type=int, default=1,
+                    help="iterations per graph replay at N=1 (one build + one gather launch "
+                         "per group; 1 = the per-iteration loop)")
     ap.add_argument("--no-model-centric", action="store_true",
                     help="N>1: skip timing the model-centric strategy on the same GPUs")
     ap.add_argument("--cpu-budget", type=float, default=15.0)

@@ -40,6 +40,7 @@ typedef enum {
 } hg_status;
 
 #define HG_MAX_LAYERS 6
+#define HG_MAX_GROUP 8   /* batches per grouped build / gather launch */
 
 const char* hg_last_error(void);
 int hg_version(void);
@@ -93,6 +94,12 @@ int hg_epoch_permutation(int64_t n, uint64_t state, int64_t* perm_out, void* ws,
 int hg_iter_stage(const int64_t* perm, const uint64_t* states, int64_t iters, int64_t* it_dev,
                   int32_t batch, int32_t ahead, int32_t advance, int64_t* roots_out,
                   uint64_t* key_out, void* stream);
+/* Group variant: iterations it+ahead .. it+ahead+n_batches-1 (those < iters):
+ * roots of each (contiguous in perm) into roots_out[b * batch ..], their
+ * states into key_out[b]; then advances the cursor by `advance`. */
+int hg_iter_stage_group(const int64_t* perm, const uint64_t* states, int64_t iters,
+                        int64_t* it_dev, int32_t batch, int32_t n_batches, int32_t ahead,
+                        int32_t advance, int64_t* roots_out, uint64_t* key_out, void* stream);
 /* Ranged variant (multi-GPU: this rank's roots of iteration it are
  * roots[ranges[2it] .. ranges[2it+1])): copies at most `cap` of them, writes
  * the count to *n_out (device), stages states[it+ahead], advances the cursor. */
@@ -194,6 +201,20 @@ int hg_mg_build_n(const int64_t* offsets, const int32_t* targets, int64_t n_vert
                   const uint64_t* iter_state, int32_t roots_per_state,
                   const hg_mg_layout* layout, int32_t* ws, hg_mg_batch* out, int* err_flag,
                   void* stream);
+/* Run-ahead over several iterations in one launch: n_batches (<= HG_MAX_GROUP)
+ * batches of n_roots roots each, roots[b * n_roots + i]; batch b's stream keys
+ * follow the hg_mg_build rule over the whole group (roots_per_state = n_roots
+ * with iter_state[b] = chain(sampler_seed, epoch, it0 + b)); outs[b] receives
+ * a complete batch (own numbering and totals), exactly what hg_mg_build would
+ * write for that batch alone.  n_roots_dev: NULL or int32[n_batches] device
+ * counts (capacity n_roots each).  ws holds n_batches * n_roots roots.  The
+ * gain over n_batches separate builds is occupancy: one 1024-root batch is
+ * ~1.4 waves of build CTAs, a group keeps every SM busy through the tail. */
+int hg_mg_build_group(const int64_t* offsets, const int32_t* targets, int64_t n_vertices,
+                      const int64_t* roots, int32_t n_roots, int32_t n_batches,
+                      const int32_t* n_roots_dev, const uint64_t* iter_state,
+                      int32_t roots_per_state, const hg_mg_layout* layout, int32_t* ws,
+                      const hg_mg_batch* outs, int* err_flag, void* stream);
 
 
 /* ------------------------------------------------------------------------
@@ -326,6 +347,10 @@ int hg_pregather_push(const int32_t* ids, const int32_t* n_dev, const int32_t* h
 /* Parameter-independent prologue of a step: the layer-1 gather + aggregate
  * (sets up agg[1]; run ahead of the previous iteration's training). */
 int hg_step_prologue(const hg_step_desc* d, int32_t n_roots, int32_t backward, void* stream);
+/* The same for n (<= HG_MAX_GROUP) steps that share one feature source (same
+ * table / staging / peers): ONE gather launch over all their layer-1 rows. */
+int hg_step_prologue_group(const hg_step_desc* const* descs, int32_t n, int32_t backward,
+                           void* stream);
 
 /* Forward + backward of the batch in d->mg for n_roots roots; gradients are
  * ADDED into gW/gb/gWc (the reference GradAccumulator, model.py:144-164). */

@@ -14,6 +14,7 @@ from .errors import ConfigError, InvariantViolation
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libhopgnn.so")
 MAX_LAYERS = 6
+MAX_GROUP = 8   # HG_MAX_GROUP
 
 _lib = None
 
@@ -88,6 +89,7 @@ SIGNATURES = {
     "hg_epoch_permutation": [I64, U64, V, V, PSZ, V],
     "hg_glorot": [I32, I32, U64, I32, V, V],
     "hg_iter_stage": [V, V, I64, V, I32, I32, I32, V, V, V],
+    "hg_iter_stage_group": [V, V, I64, V, I32, I32, I32, I32, V, V, V],
     "hg_bench_mix64": [I32, I64, V, V],
     "hg_iter_stage_ranged": [V, V, V, I64, V, I32, I32, I32, V, V, V, V],
     "hg_graph_raw_degrees": [C.POINTER(GraphTables), V, V],
@@ -100,6 +102,8 @@ SIGNATURES = {
                     V, V],
     "hg_mg_build_n": [V, V, I64, V, I32, V, V, I32, C.POINTER(MgLayout), V, C.POINTER(MgBatch),
                       V, V],
+    "hg_mg_build_group": [V, V, I64, V, I32, I32, V, V, I32, C.POINTER(MgLayout), V,
+                          C.POINTER(MgBatch), V, V],
     "hg_train_step": [C.POINTER(StepDesc), I32, V],
     "hg_forward": [C.POINTER(StepDesc), I32, V],
     "hg_sgd_update": [V, V, V, I64, C.c_float, C.c_float, V],
@@ -123,6 +127,7 @@ SIGNATURES = {
     "hg_pregather_push": [V, V, V, I32, I32, V, V, I32, V, V, I32, V, V, I64, I64, I64, I64, I64,
                           V, V, I32, V, V, V, V],
     "hg_step_prologue": [C.POINTER(StepDesc), I32, I32, V],
+    "hg_step_prologue_group": [C.POINTER(C.POINTER(StepDesc)), I32, I32, V],
     "hg_debug_build_phases": [C.POINTER(C.c_longlong), C.c_int],
 }
 

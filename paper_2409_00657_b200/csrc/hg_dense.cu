@@ -108,13 +108,36 @@ struct RowSrc {
   }
 };
 
+// One warp per destination row.  The row's column span is covered by G lanes
+// (16-byte vectors, G = min(32, vectors per row)); the warp's P = 32/G lane
+// groups ("phases") take interleaved neighbours, so a row's whole neighbour
+// list is in flight at once: lane l loads neighbour index j0+l (one coalesced
+// read), every phase issues up to U predicated 16-byte row loads before
+// consuming any, and the phases' partial sums meet through shuffles.  The
+// dependent chain per row is (self_pos, nbr_off) -> (nbr_idx, self row) ->
+// neighbour rows -> store, which is what bounds a ~100K-row, 30 MB gather.
+// Segments of one launch: blockIdx.y selects a batch (a group of run-ahead
+// iterations shares the feature source and is gathered in one launch).
+template <typename T>
+struct AggSegs {
+  const int32_t* self_pos[HG_MAX_GROUP];
+  const int32_t* nbr_off[HG_MAX_GROUP];
+  const int32_t* nbr_idx[HG_MAX_GROUP];
+  const int32_t* n_rows[HG_MAX_GROUP];
+  T* out[HG_MAX_GROUP];
+};
+
 template <typename T, bool SAGE>
-__global__ void __launch_bounds__(256)
-k_aggregate(RowSrc<T> rs, const int32_t* __restrict__ self_pos,
-            const int32_t* __restrict__ nbr_off, const int32_t* __restrict__ nbr_idx,
-            const int32_t* __restrict__ n_rows_dev, int W, T* __restrict__ out, int out_ld,
-            int pad_cap) {
+__global__ void __launch_bounds__(256, 4)
+k_aggregate(RowSrc<T> rs, AggSegs<T> segs, int W, int out_ld, int pad_cap) {
+  const int32_t* __restrict__ self_pos = segs.self_pos[blockIdx.y];
+  const int32_t* __restrict__ nbr_off = segs.nbr_off[blockIdx.y];
+  const int32_t* __restrict__ nbr_idx = segs.nbr_idx[blockIdx.y];
+  const int32_t* __restrict__ n_rows_dev = segs.n_rows[blockIdx.y];
+  T* __restrict__ out = segs.out[blockIdx.y];
   constexpr int VEC = Vec<T>::N;
+  constexpr int U = 6;   // 64 registers at 4 CTAs/SM; U = 8 spills
+  constexpr unsigned FULL = 0xffffffffu;
   if (pad_cap && blockIdx.x == gridDim.x - 1) {
     // the tensor-core dW GEMM reduces over rows up to the next multiple of 64:
     // keep those padding rows zero (folded in here instead of its own launch)
@@ -125,47 +148,78 @@ k_aggregate(RowSrc<T> rs, const int32_t* __restrict__ self_pos,
   }
   const int nvec = W / VEC;                        // vectors per row
   const int G = nvec >= 32 ? 32 : (nvec >= 16 ? 16 : (nvec >= 8 ? 8 : (nvec >= 4 ? 4 : (nvec >= 2 ? 2 : 1))));
-  const int groups_per_block = blockDim.x / G;
-  const int grp = threadIdx.x / G, gl = threadIdx.x % G;
+  const int P = 32 / G;
+  const int lane = threadIdx.x & 31, ph = lane / G, gl = lane % G;
+  const int warps = blockDim.x >> 5;
   const int n_rows = *n_rows_dev;
-  for (int a = blockIdx.x * groups_per_block + grp; a < n_rows; a += gridDim.x * groups_per_block) {
-    const T* sp = rs.row(self_pos[a]);
+  for (int a = blockIdx.x * warps + (threadIdx.x >> 5); a < n_rows; a += gridDim.x * warps) {
     const int j0 = nbr_off[a], j1 = nbr_off[a + 1];
     const int deg = j1 - j0;
-    for (int cv = gl; cv < nvec; cv += G) {
+    const int sidx = self_pos[a];
+    const int cnt0 = min(32, deg);
+    int idx0 = lane < cnt0 ? nbr_idx[j0 + lane] : 0;
+    const T* sp = rs.row(sidx);
+    T* o = out + (int64_t)a * out_ld;
+    for (int c0 = 0; c0 < nvec; c0 += G) {
+      const int cv = c0 + gl;
+      const bool act = cv < nvec;
       const int col = cv * VEC;
       float self[VEC], acc[VEC];
-      load_vec(sp + col, self);
 #pragma unroll
-      for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
-      int j = j0;
-      for (; j + 4 <= j1; j += 4) {
-        const T* r[4];
+      for (int i = 0; i < VEC; ++i) { acc[i] = 0.f; self[i] = 0.f; }
+      if (act && ph == 0) load_vec(sp + col, self);
+      for (int jb = j0; jb < j1; jb += 32) {
+        const int cnt = min(32, j1 - jb);
+        const int idx = jb == j0 ? idx0 : (lane < cnt ? nbr_idx[jb + lane] : 0);
+        const int per = (cnt - ph + P - 1) / P;     // neighbours of this phase in the chunk
+        const int rounds = (cnt + P - 1) / P;        // warp-uniform
+        for (int t0 = 0; t0 < rounds; t0 += U) {
+          uint4 x[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) r[u] = rs.row(nbr_idx[j + u]);
-        float x[4][VEC];
+          for (int t = 0; t < U; ++t) {
+            const int u = ph + P * (t0 + t);
+            const int v = __shfl_sync(FULL, idx, u & 31);
+            if (act && t0 + t < per) x[t] = __ldg(reinterpret_cast<const uint4*>(rs.row(v) + col));
+            else x[t] = make_uint4(0, 0, 0, 0);
+          }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) load_vec(r[u] + col, x[u]);
+          for (int t = 0; t < U; ++t) {
+            float f[VEC];
+            if constexpr (sizeof(T) == 4) {
+              f[0] = __uint_as_float(x[t].x); f[1] = __uint_as_float(x[t].y);
+              f[2] = __uint_as_float(x[t].z); f[3] = __uint_as_float(x[t].w);
+            } else {
+              const uint32_t w[4] = {x[t].x, x[t].y, x[t].z, x[t].w};
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+              for (int i = 0; i < 4; ++i) {
+                f[2 * i] = __uint_as_float(w[i] << 16);
+                f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+              }
+            }
 #pragma unroll
-          for (int i = 0; i < VEC; ++i) acc[i] += x[u][i];
+            for (int i = 0; i < VEC; ++i) acc[i] += f[i];
+          }
+        }
       }
-      for (; j < j1; ++j) {
-        float x[VEC];
-        load_vec(rs.row(nbr_idx[j]) + col, x);
+      // phases meet: every lane ends with the full neighbour sum of its columns
+      for (int off = G; off < 32; off <<= 1)
 #pragma unroll
-        for (int i = 0; i < VEC; ++i) acc[i] += x[i];
-      }
-      T* o = out + (int64_t)a * out_ld;
+        for (int i = 0; i < VEC; ++i) acc[i] += __shfl_xor_sync(FULL, acc[i], off);
+      if (P > 1)
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) self[i] = __shfl_sync(FULL, self[i], gl);
+      if (!act) continue;
       if constexpr (SAGE) {
-        float nb[VEC];
+        // phase 0 writes the self half, phase 1 (or 0 when P == 1) the mean half
         const float inv = deg > 0 ? 1.0f / (float)deg : 0.f;
+        if (ph == 0) store_vec(o + col, self);
+        if (ph == (P > 1 ? 1 : 0)) {
+          float nb[VEC];
 #pragma unroll
-        for (int i = 0; i < VEC; ++i) nb[i] = deg > 0 ? acc[i] * inv : self[i];
-        store_vec(o + col, self);
-        store_vec(o + W + col, nb);
-      } else {
+          for (int i = 0; i < VEC; ++i) nb[i] = deg > 0 ? acc[i] * inv : self[i];
+          store_vec(o + W + col, nb);
+        }
+      } else if (ph == 0) {
         const float inv = 1.0f / (float)(deg + 1);
 #pragma unroll
         for (int i = 0; i < VEC; ++i) acc[i] = (acc[i] + self[i]) * inv;
@@ -687,30 +741,53 @@ static void gemm(cudaStream_t s, const TA* A, int lda, const float* B, int ldb, 
 // remote rows or peer tables).  pad: zero the rows up to the next 64 for the
 // tensor-core weight-gradient reduction.
 template <typename T>
-static void launch_aggregate(const hg_step_desc* d, int k, cudaStream_t s, bool pad) {
-  const int H = d->hidden;
-  const int32_t* tot = d->mg.totals;
-  const int nb = num_sms() * 4;
-  const int Wd = k == 1 ? d->feat_ld : H;
+static RowSrc<T> row_src(const hg_step_desc* d, int k) {
   const T* src = k == 1 ? (const T*)d->features : (const T*)d->h[k - 1];
-  const int32_t* ids0 = k == 1 ? d->mg.need_ids[0] : nullptr;
-  prof_begin(k == 1 ? PROF_AGG1 : PROF_AGG2, s);
-  count_launch();
+  const int Wd = k == 1 ? d->feat_ld : d->hidden;
   // layer 1: pair lists by vertex id (one dependent load fewer per source row)
   const bool vid = k == 1 && d->mg.nbr_vid1 && d->mg.self_vid1;
-  RowSrc<T> rs{src, Wd, ids0, k == 1 ? d->feat_row : nullptr,
-               k == 1 ? (const T* const*)d->feat_peers : nullptr, d->feat_home,
-               (const T*)d->stage_base, k == 1 ? d->stage_row : nullptr, d->rank, vid};
-  const int32_t* selfv = vid ? d->mg.self_vid1 : d->mg.self_pos[k];
-  const int32_t* nbrv = vid ? d->mg.nbr_vid1 : d->mg.nbr_idx[k];
+  return RowSrc<T>{src, Wd, k == 1 ? d->mg.need_ids[0] : nullptr, k == 1 ? d->feat_row : nullptr,
+                   k == 1 ? (const T* const*)d->feat_peers : nullptr, d->feat_home,
+                   (const T*)d->stage_base, k == 1 ? d->stage_row : nullptr, d->rank, vid};
+}
+
+// Layer-k gather + aggregate for n steps sharing one row source (k == 1
+// reads features: local table, staged remote rows or peer tables; n > 1 only
+// for layer 1 of run-ahead groups).  pad: zero the rows up to the next 64 for
+// the tensor-core weight-gradient reduction.
+template <typename T>
+static void launch_aggregate_n(const hg_step_desc* const* ds, int n, int k, cudaStream_t s,
+                               bool pad) {
+  const hg_step_desc* d = ds[0];
+  const int H = d->hidden;
+  const int Wd = k == 1 ? d->feat_ld : H;
+  AggSegs<T> segs{};
+  int cap = 1;
+  for (int b = 0; b < n; ++b) {
+    const hg_step_desc* e = ds[b];
+    const bool vid = k == 1 && e->mg.nbr_vid1 && e->mg.self_vid1;
+    segs.self_pos[b] = vid ? e->mg.self_vid1 : e->mg.self_pos[k];
+    segs.nbr_off[b] = e->mg.nbr_off[k];
+    segs.nbr_idx[b] = vid ? e->mg.nbr_vid1 : e->mg.nbr_idx[k];
+    segs.n_rows[b] = e->mg.totals + k;
+    segs.out[b] = (T*)e->agg[k];
+    cap = std::max(cap, e->max_rows[k]);
+  }
+  // one warp per row over the capacity: blocks past the device row count exit
+  dim3 grid(std::max(1, std::min((cap + 7) / 8, num_sms() * 32)), n);
   const int pad_cap = pad && sizeof(T) == 2 ? d->max_rows[k] : 0;
+  prof_begin(k == 1 ? PROF_AGG1 : PROF_AGG2, s);
+  count_launch();
   if (d->arch == 1)
-    k_aggregate<T, true><<<nb, 256, 0, s>>>(rs, selfv, d->mg.nbr_off[k], nbrv, tot + k, Wd,
-                                            (T*)d->agg[k], d->in_dim[k], pad_cap);
+    k_aggregate<T, true><<<grid, 256, 0, s>>>(row_src<T>(d, k), segs, Wd, d->in_dim[k], pad_cap);
   else
-    k_aggregate<T, false><<<nb, 256, 0, s>>>(rs, selfv, d->mg.nbr_off[k], nbrv, tot + k, Wd,
-                                             (T*)d->agg[k], d->in_dim[k], pad_cap);
+    k_aggregate<T, false><<<grid, 256, 0, s>>>(row_src<T>(d, k), segs, Wd, d->in_dim[k], pad_cap);
   prof_end(k == 1 ? PROF_AGG1 : PROF_AGG2, s);
+}
+
+template <typename T>
+static void launch_aggregate(const hg_step_desc* d, int k, cudaStream_t s, bool pad) {
+  launch_aggregate_n<T>(&d, 1, k, s, pad);
 }
 
 constexpr size_t kScatterSmem = 96 * 1024;
@@ -912,12 +989,27 @@ extern "C" int hg_train_step(const hg_step_desc* d, int32_t n_roots, void* strea
 
 extern "C" int hg_step_prologue(const hg_step_desc* d, int32_t n_roots, int32_t backward,
                                 void* stream) {
-  int st = validate(d, n_roots);
-  if (st) return st;
+  return hg_step_prologue_group(&d, 1, backward, stream);
+}
+
+extern "C" int hg_step_prologue_group(const hg_step_desc* const* ds, int32_t n, int32_t backward,
+                                      void* stream) {
+  if (n < 1 || n > HG_MAX_GROUP) return hg_fail(HG_ERANGE, "bad group size %d", n);
+  const hg_step_desc* d = ds[0];
+  for (int b = 0; b < n; ++b) {
+    int st = validate(ds[b], ds[b]->max_roots);
+    if (st) return st;
+    const hg_step_desc* e = ds[b];
+    if (e->features != d->features || e->feat_row != d->feat_row || e->feat_ld != d->feat_ld ||
+        e->stage_base != d->stage_base || e->stage_row != d->stage_row ||
+        e->feat_peers != d->feat_peers || e->act_dtype != d->act_dtype || e->arch != d->arch ||
+        e->in_dim[1] != d->in_dim[1] || e->max_rows[1] != d->max_rows[1])
+      return hg_fail(HG_ECONFIG, "grouped prologue: steps must share the feature source");
+  }
   cudaStream_t s = (cudaStream_t)stream;
   const bool tc = d->act_dtype == 1 && d->use_tc && d->hidden % 64 == 0 && d->hidden <= 256;
-  if (d->act_dtype == 0) launch_aggregate<float>(d, 1, s, false);
-  else launch_aggregate<bf16>(d, 1, s, tc && backward);
+  if (d->act_dtype == 0) launch_aggregate_n<float>(ds, n, 1, s, false);
+  else launch_aggregate_n<bf16>(ds, n, 1, s, tc && backward);
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;
 }

@@ -112,13 +112,18 @@ extern "C" int hg_epoch_permutation(int64_t n, uint64_t state, int64_t* perm_out
 }
 
 __global__ void k_iter_stage(const int64_t* __restrict__ perm, const uint64_t* __restrict__ states,
-                             int64_t iters, int64_t* it_dev, int batch, int ahead, int advance,
-                             int64_t* __restrict__ roots_out, uint64_t* __restrict__ key_out) {
-  const int64_t it = *it_dev + ahead;
-  if (it < iters) {
+                             int64_t iters, int64_t* it_dev, int batch, int n_batches, int ahead,
+                             int advance, int64_t* __restrict__ roots_out,
+                             uint64_t* __restrict__ key_out) {
+  const int64_t it0 = *it_dev + ahead;
+  // iterations it0 .. it0 + n_batches - 1 (those inside the epoch); their roots
+  // are contiguous in the permutation
+  const int64_t nb = min((int64_t)n_batches, iters - it0);
+  if (nb > 0) {
     if (roots_out)
-      for (int i = threadIdx.x; i < batch; i += blockDim.x) roots_out[i] = perm[it * batch + i];
-    if (threadIdx.x == 0) key_out[0] = states[it];
+      for (int64_t i = threadIdx.x; i < nb * batch; i += blockDim.x)
+        roots_out[i] = perm[it0 * batch + i];
+    if (threadIdx.x < nb) key_out[threadIdx.x] = states[it0 + threadIdx.x];
   }
   __syncthreads();  // every thread has read *it_dev before it moves
   if (threadIdx.x == 0 && advance) *it_dev += advance;
@@ -127,10 +132,19 @@ __global__ void k_iter_stage(const int64_t* __restrict__ perm, const uint64_t* _
 extern "C" int hg_iter_stage(const int64_t* perm, const uint64_t* states, int64_t iters,
                              int64_t* it_dev, int32_t batch, int32_t ahead, int32_t advance,
                              int64_t* roots_out, uint64_t* key_out, void* stream) {
+  return hg_iter_stage_group(perm, states, iters, it_dev, batch, 1, ahead, advance, roots_out,
+                             key_out, stream);
+}
+
+extern "C" int hg_iter_stage_group(const int64_t* perm, const uint64_t* states, int64_t iters,
+                                   int64_t* it_dev, int32_t batch, int32_t n_batches,
+                                   int32_t ahead, int32_t advance, int64_t* roots_out,
+                                   uint64_t* key_out, void* stream) {
   if (batch < 0) return hg_fail(HG_ERANGE, "bad batch");
+  if (n_batches < 1 || n_batches > 1024) return hg_fail(HG_ERANGE, "bad batch count");
   count_launch();
-  k_iter_stage<<<1, 1024, 0, (cudaStream_t)stream>>>(perm, states, iters, it_dev, batch, ahead,
-                                                      advance, roots_out, key_out);
+  k_iter_stage<<<1, 1024, 0, (cudaStream_t)stream>>>(perm, states, iters, it_dev, batch, n_batches,
+                                                      ahead, advance, roots_out, key_out);
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;
 }

@@ -33,6 +33,12 @@ constexpr int kBuildThreads = 256;
 constexpr int kBuildWarps = kBuildThreads / 32;
 constexpr int kBigTask = 256;  // degree above which the whole CTA draws one vertex
 
+// Output descriptors of a group of batches built by one launch (run-ahead over
+// several iterations): batch b's roots are [b * n_roots, (b + 1) * n_roots).
+struct MgOuts {
+  hg_mg_batch b[HG_MAX_GROUP];
+};
+
 struct MgCarve {
   int L;
   int fanout[HG_MAX_LAYERS];
@@ -428,12 +434,14 @@ __global__ void __launch_bounds__(kBuildThreads, HG_BUILD_MINB)
 k_mg_build(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targets,
            int64_t n_vertices, const int64_t* __restrict__ roots, int n_roots,
            const uint64_t* __restrict__ iter_state, int roots_per_state, MgCarve c,
-           int32_t* __restrict__ ws, int* err, const int32_t* __restrict__ n_roots_dev) {
+           int32_t* __restrict__ ws, int* err, const int32_t* __restrict__ n_roots_dev,
+           int per_batch) {
   extern __shared__ __align__(16) int sm[];
   const int r = blockIdx.x;
   if (r >= n_roots) return;
   const int L = c.L;
-  if (n_roots_dev && r >= *n_roots_dev) {  // beyond the device count: an empty micrograph
+  // beyond the device count of its batch: an empty micrograph
+  if (n_roots_dev && r % per_batch >= n_roots_dev[r / per_batch]) {
     int32_t* w = ws + (size_t)r * c.ws_root_ints;
     if (threadIdx.x <= 2 * L) w[c.ws_cnt + threadIdx.x] = 0;
     return;
@@ -586,7 +594,10 @@ constexpr int kScanCols = 2 * HG_MAX_LAYERS + 1;
 constexpr int kScanPer = 2;  // roots per thread held in registers per 2048-root tile
 
 __global__ void __launch_bounds__(1024)
-k_mg_scan(const int32_t* __restrict__ ws, int n_roots, MgCarve c, hg_mg_batch out) {
+k_mg_scan(const int32_t* __restrict__ ws, int n_roots, MgCarve c, MgOuts outs) {
+  // CTA b scans batch b: roots [b * n_roots, (b + 1) * n_roots) of the workspace
+  const hg_mg_batch& out = outs.b[blockIdx.x];
+  ws += (size_t)blockIdx.x * n_roots * c.ws_root_ints;
   __shared__ int scan[40];
   __shared__ int32_t* dsts[kScanCols];
   const int L = c.L, ncol = 2 * L + 1;
@@ -636,11 +647,12 @@ k_mg_scan(const int32_t* __restrict__ ws, int n_roots, MgCarve c, hg_mg_batch ou
 }
 
 __global__ void __launch_bounds__(128)
-k_mg_finalize(const int32_t* __restrict__ ws, int n_roots, MgCarve c, hg_mg_batch out) {
-  const int r = blockIdx.x;
-  if (r >= n_roots) return;
+k_mg_finalize(const int32_t* __restrict__ ws, int n_roots, MgCarve c, MgOuts outs) {
+  // CTA per root of the whole group; root r belongs to batch r / n_roots
+  const int r = blockIdx.x % n_roots;
+  const hg_mg_batch& out = outs.b[blockIdx.x / n_roots];
   const int L = c.L;
-  const int32_t* w = ws + (size_t)r * c.ws_root_ints;
+  const int32_t* w = ws + (size_t)blockIdx.x * c.ws_root_ints;
   for (int k = 0; k <= L; ++k) {
     const int base = out.need_off[k][r];
     const int nk = w[c.ws_cnt + k];
@@ -736,31 +748,55 @@ extern "C" int hg_mg_build(const int64_t* offsets, const int32_t* targets, int64
                        roots_per_state, layout, ws, out, err_flag, stream);
 }
 
-extern "C" int hg_mg_build_n(const int64_t* offsets, const int32_t* targets, int64_t n_vertices,
-                             const int64_t* roots, int32_t n_roots, const int32_t* n_roots_dev,
-                             const uint64_t* iter_state, int32_t roots_per_state,
-                             const hg_mg_layout* layout, int32_t* ws, hg_mg_batch* out,
-                             int* err_flag, void* stream) {
+static int build_group(const int64_t* offsets, const int32_t* targets, int64_t n_vertices,
+                       const int64_t* roots, int32_t n_roots, int32_t n_batches,
+                       const int32_t* n_roots_dev, const uint64_t* iter_state,
+                       int32_t roots_per_state, const hg_mg_layout* layout, int32_t* ws,
+                       const hg_mg_batch* outs, int* err_flag, void* stream) {
   if (n_roots < 0 || roots_per_state < 0) return hg_fail(HG_ERANGE, "bad root count");
+  if (n_batches < 1 || n_batches > HG_MAX_GROUP) return hg_fail(HG_ERANGE, "bad batch count %d", n_batches);
+  if ((int64_t)n_roots * n_batches > INT32_MAX) return hg_fail(HG_ERANGE, "group too large");
   MgCarve c;
   int st = make_carve(layout->n_layers, layout->fanout, &c);
   if (st) return st;
   cudaStream_t s = (cudaStream_t)stream;
   if (n_roots == 0) return HG_OK;
+  MgOuts o{};
+  for (int b = 0; b < n_batches; ++b) o.b[b] = outs[b];
   HG_CUDA_TRY(cudaFuncSetAttribute(k_mg_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    c.smem_bytes));
+  const int total = n_roots * n_batches;
   count_launch(3);
   prof_begin(PROF_BUILD, s);
-  k_mg_build<<<n_roots, kBuildThreads, c.smem_bytes, s>>>(offsets, targets, n_vertices, roots,
-                                                          n_roots, iter_state, roots_per_state,
-                                                          c, ws, err_flag, n_roots_dev);
+  k_mg_build<<<total, kBuildThreads, c.smem_bytes, s>>>(offsets, targets, n_vertices, roots, total,
+                                                        iter_state, roots_per_state, c, ws,
+                                                        err_flag, n_roots_dev, n_roots);
   HG_CUDA_TRY(cudaGetLastError());
-  k_mg_scan<<<1, 1024, 0, s>>>(ws, n_roots, c, *out);
+  k_mg_scan<<<n_batches, 1024, 0, s>>>(ws, n_roots, c, o);
   HG_CUDA_TRY(cudaGetLastError());
-  k_mg_finalize<<<n_roots, 128, 0, s>>>(ws, n_roots, c, *out);
+  k_mg_finalize<<<total, 128, 0, s>>>(ws, n_roots, c, o);
   prof_end(PROF_BUILD, s);
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;
+}
+
+extern "C" int hg_mg_build_n(const int64_t* offsets, const int32_t* targets, int64_t n_vertices,
+                             const int64_t* roots, int32_t n_roots, const int32_t* n_roots_dev,
+                             const uint64_t* iter_state, int32_t roots_per_state,
+                             const hg_mg_layout* layout, int32_t* ws, hg_mg_batch* out,
+                             int* err_flag, void* stream) {
+  return build_group(offsets, targets, n_vertices, roots, n_roots, 1, n_roots_dev, iter_state,
+                     roots_per_state, layout, ws, out, err_flag, stream);
+}
+
+extern "C" int hg_mg_build_group(const int64_t* offsets, const int32_t* targets,
+                                 int64_t n_vertices, const int64_t* roots, int32_t n_roots,
+                                 int32_t n_batches, const int32_t* n_roots_dev,
+                                 const uint64_t* iter_state, int32_t roots_per_state,
+                                 const hg_mg_layout* layout, int32_t* ws,
+                                 const hg_mg_batch* outs, int* err_flag, void* stream) {
+  return build_group(offsets, targets, n_vertices, roots, n_roots, n_batches, n_roots_dev,
+                     iter_state, roots_per_state, layout, ws, outs, err_flag, stream);
 }
 
 extern "C" int hg_sample_frontier(const int64_t* offsets, const int32_t* targets,

@@ -26,6 +26,7 @@ from .featstore import FeatureTable
 from .graph import Graph
 from .model import LabelOracle, ModelState
 from .rng import chain
+from .sampler import GroupBuilder
 from .trainer import CellRunner
 
 SEED_GRAPH, SEED_PARTITION, SEED_FEATURES, SEED_LABELS = 0x01, 0x02, 0x03, 0x04
@@ -143,6 +144,136 @@ class GraphLoop:
         self.graphs[x].replay()
 
 
+class GroupLoop:
+    """CUDA-graph replay of the run-ahead loop over groups of G iterations
+    (S = 1).  Two sets of G runners alternate: graph x trains set x's G
+    iterations in order (train step + fused SGD/refresh each) while a forked
+    branch stages the next G iterations from the device cursor, builds all
+    their micrographs in ONE launch (hg_mg_build_group) and gathers their
+    layer-1 features in ONE launch (hg_step_prologue_group) into set 1-x.
+    Training semantics are those of the one-iteration loop (sampling never
+    reads the parameters); what changes is launch shape: a 1024-root build is
+    ~1.4 waves of build CTAs and a 100K-row gather is too short to reach HBM
+    bandwidth, a G-iteration group keeps every SM busy through both tails.
+    Optional e2e extras: the next group's roots arrive through a pinned host
+    slot, and the group's per-iteration summed losses go back to pinned host
+    memory."""
+
+    def __init__(self, tr: "Trainer", sets, e2e: bool = False):
+        self.tr, self.sets, self.e2e = tr, sets, e2e
+        self.G = G = len(sets[0])
+        dev, B = tr.device, tr.B
+        self.gb = [GroupBuilder([r.builder for r in st]) for st in sets]
+        for x in range(2):
+            for b, r in enumerate(sets[x]):
+                r.desc.roots = self.gb[x].roots_ptr(b)
+                r.desc.agg1_ready = 1
+                r.n_roots = B
+        self.descp = [(C.POINTER(_lib.StepDesc) * G)(*[C.pointer(r.desc) for r in st])
+                      for st in sets]
+        self.side = torch.cuda.Stream(dev)
+        if e2e:
+            self.pin_roots = [torch.empty(G * B, dtype=torch.int64).pin_memory() for _ in range(2)]
+            self.pin_loss = [torch.zeros(G, dtype=torch.float32).pin_memory() for _ in range(2)]
+        self.graphs = []
+        self.launches = 0
+        self.x = 0
+        cur = torch.cuda.current_stream(dev)
+        m = tr.model
+        for x in range(2):
+            nxt = self.gb[1 - x]
+            g = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream(dev)
+            cap.wait_stream(cur)
+            before = _lib.launch_count()
+            with torch.cuda.graph(g, stream=cap):
+                self.side.wait_stream(cap)
+                ss = self.side.cuda_stream
+                with torch.cuda.stream(self.side):
+                    if e2e:  # roots of the next group, written by the host into a pinned slot
+                        nxt.roots.copy_(self.pin_roots[1 - x], non_blocking=True)
+                    _lib.call("hg_iter_stage_group", tr._perm_buf.data_ptr(),
+                              tr._states_buf.data_ptr(), tr.iters, tr._it_dev.data_ptr(), B, G,
+                              G, G, None if e2e else nxt.roots.data_ptr(), nxt.keys.data_ptr(), ss)
+                    nxt.build(tr.graph, stream=ss)
+                    _lib.call("hg_step_prologue_group", self.descp[1 - x], G, 1, ss)
+                cs = cap.cuda_stream
+                for r in sets[x]:
+                    if r.tc:  # SGD refreshes the bf16 operands: steps skip their transposes
+                        r.desc.lowp_fresh = 1
+                        _lib.call("hg_train_step", C.byref(r.desc), B, cs)
+                        _lib.call("hg_sgd_refresh", C.byref(r.desc), m.flat.data_ptr(),
+                                  m.grad.data_ptr(), m.flat.numel(), float(tr.lr), 1.0 / B, 1, cs)
+                        r.desc.lowp_fresh = 0
+                    else:
+                        _lib.call("hg_train_step", C.byref(r.desc), B, cs)
+                        m.sgd(tr.lr, B, stream=cs)
+                if e2e:
+                    self.pin_loss[x].copy_(torch.stack([r.loss[:B].sum() for r in sets[x]]),
+                                           non_blocking=True)
+                cap.wait_stream(self.side)
+            self.launches = _lib.launch_count() - before
+            cur.wait_stream(cap)
+            self.graphs.append(g)
+        self.iters = tr.iters
+
+    def restart(self, it: int, roots=None) -> None:
+        """Position the loop at iteration `it` (it + G <= iters): build the
+        group [it, it+G) into set 0 on the current stream, point the device
+        cursor at it.  roots: device int64[G*B] (e2e), else the epoch plan."""
+        tr = self.tr
+        tr._drain_run_ahead()
+        cur = torch.cuda.current_stream(tr.device)
+        cur.wait_stream(self.side)
+        s = cur.cuda_stream
+        gb = self.gb[0]
+        tr._it_dev.fill_(it)
+        _lib.call("hg_iter_stage_group", tr._perm_buf.data_ptr(), tr._states_buf.data_ptr(),
+                  tr.iters, tr._it_dev.data_ptr(), tr.B, self.G, 0, 0,
+                  None if roots is not None else gb.roots.data_ptr(), gb.keys.data_ptr(), s)
+        if roots is not None:
+            gb.roots.copy_(roots, non_blocking=True)
+        gb.build(tr.graph, stream=s)
+        _lib.call("hg_step_prologue_group", self.descp[0], self.G, 1, s)
+        r = self.sets[0][0]
+        if r.tc:  # the replays' steps use the bf16 operands as the previous SGD left them
+            m = tr.model
+            _lib.call("hg_sgd_refresh", C.byref(r.desc), m.flat.data_ptr(), m.grad.data_ptr(),
+                      m.flat.numel(), 0.0, 1.0, 0, s)
+        self.x = 0
+
+    def run_eager(self, it: int) -> None:
+        """The body of one replay for iterations it..it+G-1 launched eagerly on
+        the current stream (build group -> gather group -> G steps): the
+        profiling pass, where per-kernel CUDA-event sites need real launches.
+        Leaves the loop unpositioned."""
+        tr = self.tr
+        cur = torch.cuda.current_stream(tr.device)
+        cur.wait_stream(self.side)
+        s = cur.cuda_stream
+        gb = self.gb[0]
+        B, G = tr.B, self.G
+        gb.roots.copy_(tr.perm[it * B:(it + G) * B])
+        gb.keys.copy_(tr.states[it:it + G])
+        gb.build(tr.graph, stream=s)
+        _lib.call("hg_step_prologue_group", self.descp[0], G, 1, s)
+        m = tr.model
+        for r in self.sets[0]:
+            _lib.call("hg_train_step", C.byref(r.desc), B, s)
+            m.sgd(tr.lr, B, stream=s)
+
+    def replay(self) -> int:
+        """Train the positioned group; returns the parity replayed."""
+        x = self.x
+        self.graphs[x].replay()
+        self.x ^= 1
+        return x
+
+    def check(self) -> None:
+        for gb in self.gb:
+            gb.check()
+
+
 class Trainer:
     """One model on one GPU (S = 1): the reference's micrograph and
     model-centric strategies coincide here (engine.py:485-507 with N = 1).
@@ -150,7 +281,7 @@ class Trainer:
 
     def __init__(self, graph: Graph, table: FeatureTable, model: ModelState, fanout,
                  batch: int, seed: int, lr: float = 0.1, iterations: int = 0,
-                 run_ahead: bool = True, graphs: bool = True):
+                 run_ahead: bool = True, graphs: bool = True, group: int = 1):
         self.graph, self.table, self.model = graph, table, model
         self.fanout = tuple(fanout)
         self.B, self.seed, self.lr, self.iter_cap = int(batch), int(seed), float(lr), iterations
@@ -170,6 +301,13 @@ class Trainer:
         self._gl_e2e = None   # GraphLoop for train_step()
         self._gnext = None    # iteration the graph loop is positioned at
         self._eager_steps = 0
+        # run-ahead group size of the graph loop (GroupLoop when > 1)
+        if not 1 <= int(group) <= _lib.MAX_GROUP:
+            raise ValueError(f"group must be 1..{_lib.MAX_GROUP}")
+        self.G = int(group)
+        self._gg = None       # GroupLoop for step()
+        self._gg_e2e = None   # GroupLoop for train_group()
+        self._gdone = None    # iterations < _gdone are already enqueued by a group replay
 
     # ------------------------------------------------------------ epoch plan
     def begin_epoch(self, epoch: int) -> int:
@@ -189,6 +327,7 @@ class Trainer:
             self._perm_buf.copy_(self.perm)
             self._states_buf.copy_(self.states)
             self._gnext = None
+            self._gdone = None
         # run-ahead builds read perm/states from side streams: order them after
         # this epoch's permutation (written on the current stream)
         cur = torch.cuda.current_stream(self.device)
@@ -207,6 +346,21 @@ class Trainer:
                 return None
             self._drain_run_ahead()
             gl = GraphLoop(self, self.ra.runners if not e2e else self._e2e_ra.runners, e2e)
+            setattr(self, attr, gl)
+        return gl
+
+    def _group_ready(self, attr: str, e2e: bool):
+        gl = getattr(self, attr)
+        if gl is not None and gl.iters != self.iters:
+            gl = None
+        if gl is None:
+            if self._eager_steps < 2:  # library state (attributes, tensor maps) warmed eagerly
+                return None
+            self._drain_run_ahead()
+            mk = lambda: CellRunner(self.graph, self.table, self.model, self.fanout, self.B,
+                                    self.labels)
+            sets = [[mk() for _ in range(self.G)] for _ in range(2)]
+            gl = GroupLoop(self, sets, e2e)
             setattr(self, attr, gl)
         return gl
 
@@ -261,12 +415,29 @@ class Trainer:
                 r.desc.agg1_ready = 1
         return launch
 
-    def step(self, it: int) -> None:
+    def step(self, it: int, stop: int = None) -> None:
         """One iteration with inputs already resident in HBM (no host sync).
         With run-ahead, iteration it+1's micrographs are built on a side
-        stream while this iteration trains."""
+        stream while this iteration trains.  With group G > 1 a call at a
+        group start enqueues iterations it..it+G-1 (one graph replay) when
+        all of them are below `stop` (default: the epoch end); the calls for
+        it+1..it+G-1 then return at once.  Other iterations run eagerly."""
         s = self.stream.cuda_stream
-        gl = self._graph_ready("_gl", False) if self.graphs else None
+        if self.G > 1 and self.graphs:
+            if self._gdone is not None and it < self._gdone and it >= self._gdone - self.G:
+                return  # enqueued by the last group replay
+            lim = self.iters if stop is None else min(int(stop), self.iters)
+            gg = self._group_ready("_gg", False) if it + self.G <= lim else None
+            if gg is not None:
+                if self._gnext != it:
+                    gg.restart(it)
+                x = gg.replay()
+                self._gnext = self._gdone = it + self.G
+                self.last_runner = gg.sets[x][-1]
+                self.last_group = (it, gg.sets[x])
+                return
+            self._gnext = self._gdone = None
+        gl = self._graph_ready("_gl", False) if self.graphs and self.G == 1 else None
         if gl is not None and (it + 1 < self.iters or self._gnext == it):
             if self._gnext != it:
                 self._graph_restart(gl, it)
@@ -318,7 +489,7 @@ class Trainer:
                 self.graph, self.table, self.model, self.fanout, self.B, self.labels)],
                 self.device) if self.run_ahead else None
         e = self._e2e
-        if self.graphs and next_roots_host is not None:
+        if self.graphs and self.G == 1 and next_roots_host is not None:
             gl = self._graph_ready("_gl_e2e", True)
             if gl is not None:
                 return self._train_step_graph(gl, roots_host, it, next_roots_host)
@@ -398,6 +569,77 @@ class Trainer:
         e["pending_graph"] = (ev, gl, x)
         return prev
 
+    def train_group(self, roots_host: torch.Tensor, it: int, next_roots_host=None):
+        """Public end-to-end API over a group of G iterations (the data loader
+        hands out G batches at a time): roots_host = pinned int64[G*B], the
+        roots of iterations it..it+G-1; next_roots_host = the next group's
+        (lets its micrographs be built ahead).  Every group's per-iteration
+        summed losses come back to the host; the readback is pipelined one
+        group: the call returns the PREVIOUS group's G losses (None on the
+        first call) and ``last_group_loss()`` drains the final one."""
+        G, B = self.G, self.B
+        if roots_host.numel() != G * B:
+            raise ValueError(f"train_group takes G*B = {G * B} roots")
+        if not hasattr(self, "_e2g"):
+            self._e2g = {"dev": torch.empty(G * B, dtype=torch.int64, device=self.device),
+                         "gnext": None, "gev": [None, None], "pending": None}
+        e = self._e2g
+        gl = None
+        if G > 1 and self.graphs and next_roots_host is not None and it + 2 * G <= self.iters:
+            gl = self._group_ready("_gg_e2e", True)
+        if gl is None:  # eager: G public steps, losses held until the next call
+            prev = self._drain_group()
+            e["gnext"] = None
+            out = []
+            for b in range(G):
+                nxt = (roots_host[(b + 1) * B:(b + 2) * B] if b + 1 < G else
+                       (next_roots_host[:B] if next_roots_host is not None else None))
+                r = self.train_step(roots_host[b * B:(b + 1) * B], it + b, nxt)
+                if b > 0:
+                    out.append(r)
+            out.append(self.last_loss())
+            e["pending"] = ("held", out)
+            return prev
+        x = gl.x
+        prev = None
+        if e["gnext"] != it:
+            prev = self._drain_group()
+            self._drain_loss()
+            e["dev"].copy_(roots_host, non_blocking=True)
+            gl.restart(it, e["dev"])
+            e["gev"] = [None, None]
+        # pinned roots slot 1-x was last read by the replay of parity x
+        if e["gev"][x] is not None:
+            e["gev"][x].synchronize()
+        gl.pin_roots[1 - x].numpy()[:] = next_roots_host.numpy()
+        gl.replay()
+        ev = torch.cuda.Event()
+        ev.record()
+        e["gev"][x] = ev
+        e["gnext"] = it + G
+        self.last_runner = gl.sets[x][-1]
+        ev_prev = e["gev"][1 - x]
+        if ev_prev is not None and prev is None:
+            ev_prev.synchronize()
+            prev = gl.pin_loss[1 - x].tolist()
+        e["pending"] = ("graph", ev, gl, x)
+        return prev
+
+    def _drain_group(self):
+        e = getattr(self, "_e2g", None)
+        if not e or e["pending"] is None:
+            return None
+        p, e["pending"] = e["pending"], None
+        if p[0] == "held":
+            return p[1]
+        _, ev, gl, x = p
+        ev.synchronize()
+        return gl.pin_loss[x].tolist()
+
+    def last_group_loss(self):
+        """The G losses of the most recent train_group (host sync)."""
+        return self._drain_group()
+
     def _drain_loss(self):
         e = getattr(self, "_e2e", None)
         if e and e.get("pending_graph") is not None:
@@ -417,6 +659,9 @@ class Trainer:
         return self._drain_loss()
 
     def check(self) -> None:
+        for gg in (self._gg, self._gg_e2e):
+            if gg is not None:
+                gg.check()
         self.runner.check()
         if self.run_ahead:
             for r in self.ra.runners:

@@ -19,6 +19,8 @@ from . import _lib
 from .graph import Graph, PartitionMap
 from .rng import chain
 
+MAX_GROUP = _lib.MAX_GROUP
+
 NODE_WISE = "node-wise"
 LAYER_WISE = "layer-wise"
 
@@ -227,6 +229,46 @@ class MicrographBuilder:
         return MicrographBatch(self.L, n, self.tensors)
 
     def check(self, what="hg_mg_build"):
+        code = int(self.err.item())
+        if code:
+            self.err.zero_()
+        _lib.flag_status(code, what)
+
+
+class GroupBuilder:
+    """Run-ahead over several iterations in ONE build launch
+    (hg_mg_build_group): batch b of the group is written into builders[b]'s
+    own output buffers, exactly as builders[b].build would have written it.
+    Owns the group's contiguous roots [K*R], iteration states [K] and
+    workspace (fixed addresses: graph-capturable)."""
+
+    def __init__(self, builders):
+        if not 1 <= len(builders) <= MAX_GROUP:
+            raise ValueError(f"group of {len(builders)} batches (1..{MAX_GROUP})")
+        self.builders = list(builders)
+        b0 = self.builders[0]
+        if any(b.fanout != b0.fanout or b.max_roots != b0.max_roots for b in self.builders):
+            raise ValueError("grouped builders must share fanout and capacity")
+        self.K, self.R, self.layout, self.device = len(builders), b0.max_roots, b0.layout, b0.device
+        i32 = dict(dtype=torch.int32, device=self.device)
+        self.ws = torch.empty(self.K * self.R * self.layout.ws_root_ints, **i32)
+        self.roots = torch.zeros(self.K * self.R, dtype=torch.int64, device=self.device)
+        self.keys = torch.zeros(self.K, dtype=torch.int64, device=self.device)
+        self.err = torch.zeros(1, **i32)
+        self.outs = (_lib.MgBatch * self.K)(*[b.cbatch for b in self.builders])
+
+    def roots_ptr(self, b: int) -> int:
+        return self.roots.data_ptr() + 8 * b * self.R
+
+    def build(self, g: Graph, stream=None, n_dev: int = None) -> None:
+        """Build all K batches from self.roots / self.keys (R roots each;
+        batch b keyed by iteration state keys[b])."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        _lib.call("hg_mg_build_group", g.offsets.data_ptr(), g.targets.data_ptr(), g.n_vertices,
+                  self.roots.data_ptr(), self.R, self.K, n_dev, self.keys.data_ptr(), self.R,
+                  C.byref(self.layout), self.ws.data_ptr(), self.outs, self.err.data_ptr(), s)
+
+    def check(self, what="hg_mg_build_group"):
         code = int(self.err.item())
         if code:
             self.err.zero_()

@@ -13,7 +13,8 @@ cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "papers"]
 g = generate(GraphSpec(n=cfg["n"], avg_deg=cfg["avg_deg"], beta=cfg["beta"], p_in=cfg["p_in"],
                        n_blocks=cfg["n_blocks"], d_cap=cfg["d_cap"], seed=cfg["seed"]))
 perm = epoch_permutation(0, 0, g.n_vertices)
-B = cfg["batch"]
+import os
+B = int(os.environ.get("HG_B", cfg["batch"]))
 b = MicrographBuilder(cfg["fanout"], B)
 states = torch.tensor(np.array([chain(chain(0, 6), 0, it) for it in range(64)], dtype=np.uint64).view(np.int64), device="cuda")
 for it in range(5):
