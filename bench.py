@@ -340,7 +340,7 @@ def _run_ours(args, cfg, dev):
     sampler_roof = sampler_roofline(tr.last_runner, g, cfg, sites["build"], dev, G)
     # end-to-end through the public API: pinned host roots in, loss out, every step
     E0 = W + 2 * K + 2 * G  # e2e iterations: W untimed warm-up, then K timed
-    perm_host = tr.perm[E0 * B:(E0 + W + K + 2 * G + 1) * B].cpu().pin_memory()
+    perm_host = tr.perm[E0 * B:(E0 + W + K + 2 * G + 3) * B].cpu().pin_memory()
 
     def host_roots(j, n=1):
         return perm_host[j * B:(j + n) * B]
@@ -351,8 +351,12 @@ def _run_ours(args, cfg, dev):
         for j in range(Wg):
             tr.train_group(host_roots(j * G, G), E0 + j * G, host_roots((j + 1) * G, G))
         tr.last_group_loss()
+        # the remainder steps below go through train_step: warm its state too
+        tr.train_step(host_roots(Wg * G), E0 + Wg * G, host_roots(Wg * G + 1))
+        tr.train_step(host_roots(Wg * G + 1), E0 + Wg * G + 1, None)
+        tr.last_loss()
         torch.cuda.synchronize()
-        j0 = Wg * G
+        j0 = Wg * G + 2
         ng = K // G
         e0 = time.perf_counter()
         for j in range(ng):
@@ -663,7 +667,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="papers", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--group", type=int, default=1,
+    ap.add_argument("--group", type=int, default=8,
                     help="iterations per graph replay at N=1 (one build + one gather launch "
                          "per group; 1 = the per-iteration loop)")
     ap.add_argument("--no-model-centric", action="store_true",

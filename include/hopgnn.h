@@ -209,12 +209,15 @@ int hg_mg_build_n(const int64_t* offsets, const int32_t* targets, int64_t n_vert
  * write for that batch alone.  n_roots_dev: NULL or int32[n_batches] device
  * counts (capacity n_roots each).  ws holds n_batches * n_roots roots.  The
  * gain over n_batches separate builds is occupancy: one 1024-root batch is
- * ~1.4 waves of build CTAs, a group keeps every SM busy through the tail. */
+ * ~1.4 waves of build CTAs, a group keeps every SM busy through the tail.
+ * ctas_per_sm > 0: a persistent grid of that many build CTAs per SM strides
+ * over the roots (leaves registers / smem on every SM for kernels running
+ * concurrently, e.g. the training branch of the graph loop); 0 = CTA/root. */
 int hg_mg_build_group(const int64_t* offsets, const int32_t* targets, int64_t n_vertices,
                       const int64_t* roots, int32_t n_roots, int32_t n_batches,
                       const int32_t* n_roots_dev, const uint64_t* iter_state,
                       int32_t roots_per_state, const hg_mg_layout* layout, int32_t* ws,
-                      const hg_mg_batch* outs, int* err_flag, void* stream);
+                      const hg_mg_batch* outs, int* err_flag, int32_t ctas_per_sm, void* stream);
 
 
 /* ------------------------------------------------------------------------

@@ -103,7 +103,7 @@ SIGNATURES = {
     "hg_mg_build_n": [V, V, I64, V, I32, V, V, I32, C.POINTER(MgLayout), V, C.POINTER(MgBatch),
                       V, V],
     "hg_mg_build_group": [V, V, I64, V, I32, I32, V, V, I32, C.POINTER(MgLayout), V,
-                          C.POINTER(MgBatch), V, V],
+                          C.POINTER(MgBatch), V, I32, V],
     "hg_train_step": [C.POINTER(StepDesc), I32, V],
     "hg_forward": [C.POINTER(StepDesc), I32, V],
     "hg_sgd_update": [V, V, V, I64, C.c_float, C.c_float, V],

@@ -35,6 +35,7 @@ extern "C" int hg_device_sync(void* stream) {
 
 // ---------------------------------------------------------------- accounting
 #include <atomic>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -50,6 +51,14 @@ struct SiteEvents {
 static SiteEvents g_sites[PROF_NSITES];
 
 void count_launch(int n) { g_launches += n; }
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HG_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 void prof_begin(int site, cudaStream_t s) {
   if (!g_prof_on) return;

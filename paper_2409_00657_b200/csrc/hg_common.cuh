@@ -99,6 +99,37 @@ void count_launch(int n = 1);
 void prof_begin(int site, cudaStream_t s);
 void prof_end(int site, cudaStream_t s);
 
+// Programmatic dependent launch (PDL).  The training chain is ~13 small
+// kernels whose launch + CTA setup would otherwise sit between every pair:
+// each chain kernel is launched with programmatic stream serialization (also
+// recorded as programmatic edges under graph capture), signals its dependent
+// at entry (pdl_trigger: the next grid may be scheduled once every CTA of
+// this one is resident) and calls pdl_wait() -- which returns when the
+// predecessor grid has completed and its writes are visible -- before it
+// reads anything a predecessor wrote.  Both are no-ops without the launch
+// attribute.  HG_PDL=0 disables the attribute (A/B switch).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 }  // namespace hg
 
 #define HG_CUDA_TRY(expr)                                              \

@@ -108,14 +108,6 @@ struct RowSrc {
   }
 };
 
-// One warp per destination row.  The row's column span is covered by G lanes
-// (16-byte vectors, G = min(32, vectors per row)); the warp's P = 32/G lane
-// groups ("phases") take interleaved neighbours, so a row's whole neighbour
-// list is in flight at once: lane l loads neighbour index j0+l (one coalesced
-// read), every phase issues up to U predicated 16-byte row loads before
-// consuming any, and the phases' partial sums meet through shuffles.  The
-// dependent chain per row is (self_pos, nbr_off) -> (nbr_idx, self row) ->
-// neighbour rows -> store, which is what bounds a ~100K-row, 30 MB gather.
 // Segments of one launch: blockIdx.y selects a batch (a group of run-ahead
 // iterations shares the feature source and is gathered in one launch).
 template <typename T>
@@ -127,16 +119,33 @@ struct AggSegs {
   T* out[HG_MAX_GROUP];
 };
 
+#ifndef HG_AGG_U
+#define HG_AGG_U 10     // neighbour loads in flight per lane (layer-1 fanout 10 in one round)
+#endif
+#ifndef HG_AGG_MINB
+#define HG_AGG_MINB 3   // CTAs/SM the register budget is sized for (U = 10 -> ~80 registers)
+#endif
+
+// One group of G lanes per destination row (G = min(32, 16-byte vectors per
+// row)), so a warp carries 32/G rows at once.  A row's neighbour indices are
+// read by its lanes in one coalesced load and broadcast by shuffles; each
+// lane then issues up to U predicated 16-byte row loads before consuming
+// any, so a row's whole neighbour list (fanout <= U) is one DRAM round trip.
+// The dependent chain per row is (self_pos, nbr_off) -> (nbr_idx, self row)
+// -> neighbour rows -> store; with ~2 rows x U loads in flight per warp the
+// ~100K-row gather of a batch keeps >100 KB in flight per SM.
 template <typename T, bool SAGE>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, HG_AGG_MINB)
 k_aggregate(RowSrc<T> rs, AggSegs<T> segs, int W, int out_ld, int pad_cap) {
+  pdl_trigger();
+  pdl_wait();
   const int32_t* __restrict__ self_pos = segs.self_pos[blockIdx.y];
   const int32_t* __restrict__ nbr_off = segs.nbr_off[blockIdx.y];
   const int32_t* __restrict__ nbr_idx = segs.nbr_idx[blockIdx.y];
   const int32_t* __restrict__ n_rows_dev = segs.n_rows[blockIdx.y];
   T* __restrict__ out = segs.out[blockIdx.y];
   constexpr int VEC = Vec<T>::N;
-  constexpr int U = 6;   // 64 registers at 4 CTAs/SM; U = 8 spills
+  constexpr int U = HG_AGG_U;
   constexpr unsigned FULL = 0xffffffffu;
   if (pad_cap && blockIdx.x == gridDim.x - 1) {
     // the tensor-core dW GEMM reduces over rows up to the next multiple of 64:
@@ -148,78 +157,70 @@ k_aggregate(RowSrc<T> rs, AggSegs<T> segs, int W, int out_ld, int pad_cap) {
   }
   const int nvec = W / VEC;                        // vectors per row
   const int G = nvec >= 32 ? 32 : (nvec >= 16 ? 16 : (nvec >= 8 ? 8 : (nvec >= 4 ? 4 : (nvec >= 2 ? 2 : 1))));
-  const int P = 32 / G;
-  const int lane = threadIdx.x & 31, ph = lane / G, gl = lane % G;
+  const int P = 32 / G;                            // rows per warp
+  const int lane = threadIdx.x & 31, gi = lane / G, gl = lane % G;
   const int warps = blockDim.x >> 5;
   const int n_rows = *n_rows_dev;
-  for (int a = blockIdx.x * warps + (threadIdx.x >> 5); a < n_rows; a += gridDim.x * warps) {
-    const int j0 = nbr_off[a], j1 = nbr_off[a + 1];
-    const int deg = j1 - j0;
-    const int sidx = self_pos[a];
-    const int cnt0 = min(32, deg);
-    int idx0 = lane < cnt0 ? nbr_idx[j0 + lane] : 0;
-    const T* sp = rs.row(sidx);
+  for (int a0 = (blockIdx.x * warps + (threadIdx.x >> 5)) * P; a0 < n_rows;
+       a0 += gridDim.x * warps * P) {
+    const int a = a0 + gi;
+    const bool row_ok = a < n_rows;
+    int j0 = 0, deg = 0, sidx = 0;
+    if (row_ok) {
+      j0 = nbr_off[a];
+      deg = nbr_off[a + 1] - j0;
+      sidx = self_pos[a];
+    }
+    int idx0 = gl < min(G, deg) ? nbr_idx[j0 + gl] : 0;
+    const T* sp = rs.row(row_ok ? sidx : 0);
+    // warp-uniform trip counts (groups of one warp hold different rows)
+    const int max_deg = __reduce_max_sync(FULL, deg);
     T* o = out + (int64_t)a * out_ld;
     for (int c0 = 0; c0 < nvec; c0 += G) {
       const int cv = c0 + gl;
-      const bool act = cv < nvec;
+      const bool act = row_ok && cv < nvec;
       const int col = cv * VEC;
       float self[VEC], acc[VEC];
 #pragma unroll
-      for (int i = 0; i < VEC; ++i) { acc[i] = 0.f; self[i] = 0.f; }
-      if (act && ph == 0) load_vec(sp + col, self);
-      for (int jb = j0; jb < j1; jb += 32) {
-        const int cnt = min(32, j1 - jb);
-        const int idx = jb == j0 ? idx0 : (lane < cnt ? nbr_idx[jb + lane] : 0);
-        const int per = (cnt - ph + P - 1) / P;     // neighbours of this phase in the chunk
-        const int rounds = (cnt + P - 1) / P;        // warp-uniform
+      for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
+      if (act) load_vec(sp + col, self);
+      for (int jb = 0; jb < max_deg; jb += G) {       // neighbour chunks of G indices
+        const int idx = jb == 0 ? idx0 : (gl < deg - jb ? nbr_idx[j0 + jb + gl] : 0);
+        const int cnt = min(G, deg - jb);              // this group's neighbours in the chunk
+        const int rounds = min(G, max_deg - jb);       // warp-uniform
         for (int t0 = 0; t0 < rounds; t0 += U) {
           uint4 x[U];
 #pragma unroll
           for (int t = 0; t < U; ++t) {
-            const int u = ph + P * (t0 + t);
-            const int v = __shfl_sync(FULL, idx, u & 31);
-            if (act && t0 + t < per) x[t] = __ldg(reinterpret_cast<const uint4*>(rs.row(v) + col));
+            const int v = __shfl_sync(FULL, idx, (gi * G + ((t0 + t) & (G - 1))) & 31);
+            if (act && t0 + t < cnt) x[t] = __ldg(reinterpret_cast<const uint4*>(rs.row(v) + col));
             else x[t] = make_uint4(0, 0, 0, 0);
           }
 #pragma unroll
           for (int t = 0; t < U; ++t) {
-            float f[VEC];
             if constexpr (sizeof(T) == 4) {
-              f[0] = __uint_as_float(x[t].x); f[1] = __uint_as_float(x[t].y);
-              f[2] = __uint_as_float(x[t].z); f[3] = __uint_as_float(x[t].w);
+              acc[0] += __uint_as_float(x[t].x); acc[1] += __uint_as_float(x[t].y);
+              acc[2] += __uint_as_float(x[t].z); acc[3] += __uint_as_float(x[t].w);
             } else {
               const uint32_t w[4] = {x[t].x, x[t].y, x[t].z, x[t].w};
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
-                f[2 * i] = __uint_as_float(w[i] << 16);
-                f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+                acc[2 * i] += __uint_as_float(w[i] << 16);
+                acc[2 * i + 1] += __uint_as_float(w[i] & 0xFFFF0000u);
               }
             }
-#pragma unroll
-            for (int i = 0; i < VEC; ++i) acc[i] += f[i];
           }
         }
       }
-      // phases meet: every lane ends with the full neighbour sum of its columns
-      for (int off = G; off < 32; off <<= 1)
-#pragma unroll
-        for (int i = 0; i < VEC; ++i) acc[i] += __shfl_xor_sync(FULL, acc[i], off);
-      if (P > 1)
-#pragma unroll
-        for (int i = 0; i < VEC; ++i) self[i] = __shfl_sync(FULL, self[i], gl);
       if (!act) continue;
       if constexpr (SAGE) {
-        // phase 0 writes the self half, phase 1 (or 0 when P == 1) the mean half
+        float nb[VEC];
         const float inv = deg > 0 ? 1.0f / (float)deg : 0.f;
-        if (ph == 0) store_vec(o + col, self);
-        if (ph == (P > 1 ? 1 : 0)) {
-          float nb[VEC];
 #pragma unroll
-          for (int i = 0; i < VEC; ++i) nb[i] = deg > 0 ? acc[i] * inv : self[i];
-          store_vec(o + W + col, nb);
-        }
-      } else if (ph == 0) {
+        for (int i = 0; i < VEC; ++i) nb[i] = deg > 0 ? acc[i] * inv : self[i];
+        store_vec(o + col, self);
+        store_vec(o + W + col, nb);
+      } else {
         const float inv = 1.0f / (float)(deg + 1);
 #pragma unroll
         for (int i = 0; i < VEC; ++i) acc[i] = (acc[i] + self[i]) * inv;
@@ -324,6 +325,8 @@ k_gemm(const TA* __restrict__ A, int lda, const float* __restrict__ B, int ldb, 
 __global__ void k_softmax_ce(float* __restrict__ logits, int C, const int64_t* __restrict__ roots,
                              int n_roots, const int32_t* __restrict__ n_dev, uint64_t label_state,
                              float* __restrict__ loss, bf16* __restrict__ dl_lowp, int ldp) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x * (blockDim.x / 32) + warp_id();
   if (r >= n_roots) return;
   const int lane = lane_id();
@@ -502,6 +505,8 @@ k_scatter_root(const float* __restrict__ dagg, int ld, const int32_t* __restrict
                int n_roots, int H, const T* __restrict__ h, float* __restrict__ dh_out,
                bf16* __restrict__ lowp, float* __restrict__ gb,
                const int32_t* __restrict__ n_rows_dev, int cap_rows) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ float acc[];  // [root_rows x H]
   // each thread owns columns c and c + blockDim.x (H <= 2 * blockDim.x)
   float colsum0 = 0.f, colsum1 = 0.f;
@@ -556,6 +561,8 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 k_mask_colsum(float* __restrict__ dh, const T* __restrict__ h, const int32_t* __restrict__ n_rows_dev,
               int H, float* __restrict__ gb, bf16* __restrict__ lowp, int cap_rows) {
+  pdl_trigger();
+  pdl_wait();
   const int n_rows = *n_rows_dev;
   const int c = blockIdx.x * 32 + (threadIdx.x & 31);
   const int r0 = blockIdx.y * 8 + (threadIdx.x >> 5);
@@ -669,6 +676,8 @@ struct LowpMap {
 // flat buffer instead of three transposes and a pad per step).
 __global__ void k_sgd_refresh(float* __restrict__ p, float* __restrict__ g, int64_t n, float lr,
                               float inv_batch, int update, LowpMap m) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float v = p[i];
@@ -700,6 +709,8 @@ __global__ void k_sgd_refresh(float* __restrict__ p, float* __restrict__ g, int6
 
 __global__ void k_sgd(float* __restrict__ p, float* __restrict__ g, bf16* __restrict__ shadow,
                       int64_t n, float lr, float inv_batch) {
+  pdl_trigger();
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const float step = g[i] * inv_batch;
@@ -773,15 +784,18 @@ static void launch_aggregate_n(const hg_step_desc* const* ds, int n, int k, cuda
     segs.out[b] = (T*)e->agg[k];
     cap = std::max(cap, e->max_rows[k]);
   }
-  // one warp per row over the capacity: blocks past the device row count exit
-  dim3 grid(std::max(1, std::min((cap + 7) / 8, num_sms() * 32)), n);
+  // rows per CTA: 8 warps x (32 / lanes per row); blocks past the device row count exit
+  const int nvec = Wd / (16 / (int)sizeof(T));
+  const int lanes = nvec >= 32 ? 32 : nvec >= 16 ? 16 : nvec >= 8 ? 8 : nvec >= 4 ? 4 : nvec >= 2 ? 2 : 1;
+  const int rows_per_cta = 8 * (32 / lanes);
+  dim3 grid(std::max(1, std::min((cap + rows_per_cta - 1) / rows_per_cta, num_sms() * 32)), n);
   const int pad_cap = pad && sizeof(T) == 2 ? d->max_rows[k] : 0;
   prof_begin(k == 1 ? PROF_AGG1 : PROF_AGG2, s);
   count_launch();
   if (d->arch == 1)
-    k_aggregate<T, true><<<grid, 256, 0, s>>>(row_src<T>(d, k), segs, Wd, d->in_dim[k], pad_cap);
+    launch_pdl(k_aggregate<T, true>, dim3(grid), dim3(256), 0, s, row_src<T>(d, k), segs, Wd, d->in_dim[k], pad_cap);
   else
-    k_aggregate<T, false><<<grid, 256, 0, s>>>(row_src<T>(d, k), segs, Wd, d->in_dim[k], pad_cap);
+    launch_pdl(k_aggregate<T, false>, dim3(grid), dim3(256), 0, s, row_src<T>(d, k), segs, Wd, d->in_dim[k], pad_cap);
   prof_end(k == 1 ? PROF_AGG1 : PROF_AGG2, s);
 }
 
@@ -854,7 +868,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
                        tot + L, nullptr, 0, nullptr, 1, s);
     if (st) return st;
     count_launch();
-    k_softmax_ce<<<(n_roots + 7) / 8, 256, 0, s>>>(d->logits, C, d->roots, n_roots, tot + L,
+    launch_pdl(k_softmax_ce, dim3((n_roots + 7) / 8), dim3(256), 0, s, d->logits, C, d->roots, n_roots, tot + L,
                                                    d->label_state, d->loss,
                                                    (bf16*)d->dl_lowp, Cp);
     if (backward) {
@@ -864,7 +878,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
       if (st) return st;
       dim3 g((H + 31) / 32, 16);
       count_launch();
-      k_mask_colsum<T><<<g, 256, 0, s>>>(d->dh[L], (const T*)d->h[L], tot + L, H, d->gb[L],
+      launch_pdl(k_mask_colsum<T>, dim3(g), dim3(256), 0, s, d->dh[L], (const T*)d->h[L], tot + L, H, d->gb[L],
                                          (bf16*)d->lowp_scratch, d->max_rows[L]);
       // gW_c += h_Lᵀ dlogits (both MN-major, reduction over the roots)
       const int split = std::max(1, std::min(16, n_roots / 256));
@@ -932,13 +946,13 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
       const int grid = n_roots;  // one CTA per root: every root's latency chain in flight at once
       count_launch();
       if (sage)
-        k_scatter_root<true, T><<<grid, 256, root_smem, s>>>(
+        launch_pdl(k_scatter_root<true, T>, dim3(grid), dim3(256), root_smem, s, 
             d->dagg, d->in_dim[k], d->mg.need_off[k - 1], d->mg.need_off[k], d->mg.self_pos[k],
             d->mg.nbr_off[k], d->mg.nbr_idx[k], n_roots, H, (const T*)d->h[k - 1],
             want_f32 ? d->dh[k - 1] : nullptr, tc ? (bf16*)d->lowp_scratch : nullptr,
             d->gb[k - 1], tot + (k - 1), d->max_rows[k - 1]);
       else
-        k_scatter_root<false, T><<<grid, 256, root_smem, s>>>(
+        launch_pdl(k_scatter_root<false, T>, dim3(grid), dim3(256), root_smem, s, 
             d->dagg, d->in_dim[k], d->mg.need_off[k - 1], d->mg.need_off[k], d->mg.self_pos[k],
             d->mg.nbr_off[k], d->mg.nbr_idx[k], n_roots, H, (const T*)d->h[k - 1],
             want_f32 ? d->dh[k - 1] : nullptr, tc ? (bf16*)d->lowp_scratch : nullptr,
@@ -957,7 +971,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
                                             d->mg.nbr_off[k], d->mg.nbr_idx[k], tot + k, H,
                                             d->dh[k - 1]);
     dim3 g((H + 31) / 32, 64);
-    k_mask_colsum<T><<<g, 256, 0, s>>>(d->dh[k - 1], (const T*)d->h[k - 1], tot + (k - 1), H,
+    launch_pdl(k_mask_colsum<T>, dim3(g), dim3(256), 0, s, d->dh[k - 1], (const T*)d->h[k - 1], tot + (k - 1), H,
                                        d->gb[k - 1], tc ? (bf16*)d->lowp_scratch : nullptr,
                                        d->max_rows[k - 1]);
   }
@@ -1047,7 +1061,7 @@ extern "C" int hg_sgd_refresh(const hg_step_desc* d, float* params, float* grads
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
   count_launch();
   prof_begin(PROF_SGD, (cudaStream_t)stream);
-  k_sgd_refresh<<<grid, 256, 0, (cudaStream_t)stream>>>(params, grads, n, lr, inv_batch, update, m);
+  launch_pdl(k_sgd_refresh, dim3(grid), dim3(256), 0, (cudaStream_t)stream, params, grads, n, lr, inv_batch, update, m);
   prof_end(PROF_SGD, (cudaStream_t)stream);
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;
@@ -1059,7 +1073,7 @@ extern "C" int hg_sgd_update(float* params, float* grads, void* shadow_bf16, int
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
   count_launch();
   prof_begin(PROF_SGD, (cudaStream_t)stream);
-  k_sgd<<<grid, 256, 0, (cudaStream_t)stream>>>(params, grads, (bf16*)shadow_bf16, n, lr, inv_batch);
+  launch_pdl(k_sgd, dim3(grid), dim3(256), 0, (cudaStream_t)stream, params, grads, (bf16*)shadow_bf16, n, lr, inv_batch);
   prof_end(PROF_SGD, (cudaStream_t)stream);
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;

@@ -17,7 +17,9 @@
 // of the hub's adjacency.  Vertices with degree <= 256 are handled by one
 // warp; larger hubs by the whole CTA.  A rare under/overflow of the survivor
 // buffer bisects the threshold and retries, so the result is always exact.
+#include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cstdio>
 
 #include <cub/device/device_scan.cuh>
@@ -430,15 +432,13 @@ __device__ long long g_phase[4096][16];
 #define HG_PHASE(i)
 #endif
 
-__global__ void __launch_bounds__(kBuildThreads, HG_BUILD_MINB)
-k_mg_build(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targets,
-           int64_t n_vertices, const int64_t* __restrict__ roots, int n_roots,
-           const uint64_t* __restrict__ iter_state, int roots_per_state, MgCarve c,
-           int32_t* __restrict__ ws, int* err, const int32_t* __restrict__ n_roots_dev,
-           int per_batch) {
+// One root's micrograph (CTA-wide); r indexes roots / iter_state / ws.
+__device__ __forceinline__ void build_root(
+    const int r, const int64_t* __restrict__ offsets, const int32_t* __restrict__ targets,
+    int64_t n_vertices, const int64_t* __restrict__ roots, const uint64_t* __restrict__ iter_state,
+    int roots_per_state, const MgCarve& c, int32_t* __restrict__ ws, int* err,
+    const int32_t* __restrict__ n_roots_dev, int per_batch) {
   extern __shared__ __align__(16) int sm[];
-  const int r = blockIdx.x;
-  if (r >= n_roots) return;
   const int L = c.L;
   // beyond the device count of its batch: an empty micrograph
   if (n_roots_dev && r % per_batch >= n_roots_dev[r / per_batch]) {
@@ -584,6 +584,22 @@ k_mg_build(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targ
     for (int k = 1; k <= L; ++k) w[c.ws_cnt + L + k] = ntot[L - k + 1];
   }
   HG_PHASE(14);
+}
+
+// CTA per root, or (gridDim.x < n_roots) a persistent grid striding over the
+// roots: capping the resident build CTAs per SM leaves registers for the
+// training kernels that run beside the build in the graph loop.
+__global__ void __launch_bounds__(kBuildThreads, HG_BUILD_MINB)
+k_mg_build(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targets,
+           int64_t n_vertices, const int64_t* __restrict__ roots, int n_roots,
+           const uint64_t* __restrict__ iter_state, int roots_per_state, MgCarve c,
+           int32_t* __restrict__ ws, int* err, const int32_t* __restrict__ n_roots_dev,
+           int per_batch) {
+  for (int r = blockIdx.x; r < n_roots; r += gridDim.x) {
+    build_root(r, offsets, targets, n_vertices, roots, iter_state, roots_per_state, c, ws, err,
+               n_roots_dev, per_batch);
+    __syncthreads();  // shared tiles are reused by the next root
+  }
 }
 
 // Exclusive scans of the per-root counts (one CTA).  cols 0..L: need sizes,
@@ -752,7 +768,7 @@ static int build_group(const int64_t* offsets, const int32_t* targets, int64_t n
                        const int64_t* roots, int32_t n_roots, int32_t n_batches,
                        const int32_t* n_roots_dev, const uint64_t* iter_state,
                        int32_t roots_per_state, const hg_mg_layout* layout, int32_t* ws,
-                       const hg_mg_batch* outs, int* err_flag, void* stream) {
+                       const hg_mg_batch* outs, int* err_flag, int ctas_per_sm, void* stream) {
   if (n_roots < 0 || roots_per_state < 0) return hg_fail(HG_ERANGE, "bad root count");
   if (n_batches < 1 || n_batches > HG_MAX_GROUP) return hg_fail(HG_ERANGE, "bad batch count %d", n_batches);
   if ((int64_t)n_roots * n_batches > INT32_MAX) return hg_fail(HG_ERANGE, "group too large");
@@ -768,7 +784,19 @@ static int build_group(const int64_t* offsets, const int32_t* targets, int64_t n
   const int total = n_roots * n_batches;
   count_launch(3);
   prof_begin(PROF_BUILD, s);
-  k_mg_build<<<total, kBuildThreads, c.smem_bytes, s>>>(offsets, targets, n_vertices, roots, total,
+  static const int cps_env = [] {  // A/B override of the resident build CTAs per SM
+    const char* e = getenv("HG_BUILD_CTAS_PER_SM");
+    return e ? atoi(e) : -1;
+  }();
+  const int cps = cps_env >= 0 ? cps_env : ctas_per_sm;
+  int grid = total;
+  if (cps > 0) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    grid = std::min(total, nsm * cps);
+  }
+  k_mg_build<<<grid, kBuildThreads, c.smem_bytes, s>>>(offsets, targets, n_vertices, roots, total,
                                                         iter_state, roots_per_state, c, ws,
                                                         err_flag, n_roots_dev, n_roots);
   HG_CUDA_TRY(cudaGetLastError());
@@ -786,7 +814,7 @@ extern "C" int hg_mg_build_n(const int64_t* offsets, const int32_t* targets, int
                              const hg_mg_layout* layout, int32_t* ws, hg_mg_batch* out,
                              int* err_flag, void* stream) {
   return build_group(offsets, targets, n_vertices, roots, n_roots, 1, n_roots_dev, iter_state,
-                     roots_per_state, layout, ws, out, err_flag, stream);
+                     roots_per_state, layout, ws, out, err_flag, 0, stream);
 }
 
 extern "C" int hg_mg_build_group(const int64_t* offsets, const int32_t* targets,
@@ -794,9 +822,11 @@ extern "C" int hg_mg_build_group(const int64_t* offsets, const int32_t* targets,
                                  int32_t n_batches, const int32_t* n_roots_dev,
                                  const uint64_t* iter_state, int32_t roots_per_state,
                                  const hg_mg_layout* layout, int32_t* ws,
-                                 const hg_mg_batch* outs, int* err_flag, void* stream) {
+                                 const hg_mg_batch* outs, int* err_flag, int32_t ctas_per_sm,
+                                 void* stream) {
   return build_group(offsets, targets, n_vertices, roots, n_roots, n_batches, n_roots_dev,
-                     iter_state, roots_per_state, layout, ws, outs, err_flag, stream);
+                     iter_state, roots_per_state, layout, ws, outs, err_flag, ctas_per_sm,
+                     stream);
 }
 
 extern "C" int hg_sample_frontier(const int64_t* offsets, const int32_t* targets,

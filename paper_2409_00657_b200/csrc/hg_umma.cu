@@ -29,7 +29,14 @@
 
 namespace hg {
 
-constexpr int kStages = 4;
+// Pipeline depth: 4 stages, 3 for 256-wide tiles (144 KB instead of 192 KB of
+// shared memory, so a GEMM CTA fits on an SM beside the build CTAs that run
+// concurrently in the graph loop; the K ranges here are 4-8 blocks, and the
+// 128 KB f32 epilogue staging still fits).
+#ifndef HG_UMMA_STAGES_256
+#define HG_UMMA_STAGES_256 3
+#endif
+__host__ __device__ constexpr int stages_for(int bn) { return bn >= 256 ? HG_UMMA_STAGES_256 : 4; }
 constexpr int BM_T = 128;
 constexpr int BK_T = 64;  // one 128-byte swizzle row of bf16
 
@@ -179,6 +186,7 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   constexpr int A_BYTES = BM_T * BK_T * 2;
   constexpr int B_BYTES = BN_T * BK_T * 2;
   constexpr int STAGE = A_BYTES + B_BYTES;
+  constexpr int kStages = stages_for(BN_T);
   constexpr uint32_t kTmemCols = BN_T <= 32 ? 32 : BN_T <= 64 ? 64 : BN_T <= 128 ? 128 : 256;
   __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], done_bar;
   __shared__ uint32_t tmem_base_sh;
@@ -186,6 +194,8 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * BM_T, n0 = blockIdx.y * BN_T;
+  pdl_trigger();
+  pdl_wait();
   const int M = args.M_dev ? *args.M_dev : args.M;
   const int K = args.K_dev ? *args.K_dev : args.K;
   if (m0 >= M) return;  // whole CTA exits together (before any barrier)
@@ -449,7 +459,7 @@ static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
 template <bool A_MN, bool B_MN, int BN_T, int EPI>
 static int launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                     const UmmaArgs& a, int split, cudaStream_t s) {
-  constexpr int smem = kStages * (BM_T * BK_T * 2 + BN_T * BK_T * 2) + 1024;
+  constexpr int smem = stages_for(BN_T) * (BM_T * BK_T * 2 + BN_T * BK_T * 2) + 1024;
   auto kern = k_umma_gemm<A_MN, B_MN, BN_T, EPI>;
   static bool attr = false;
   if (!attr) {
@@ -458,8 +468,7 @@ static int launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensor
   }
   dim3 grid((a.M + BM_T - 1) / BM_T, (a.N + BN_T - 1) / BN_T, split);
   count_launch();
-  kern<<<grid, 128, smem, s>>>(ma, mb, mc, a);
-  HG_CUDA_TRY(cudaGetLastError());
+  HG_CUDA_TRY(launch_pdl(kern, grid, dim3(128), smem, s, ma, mb, mc, a));
   return HG_OK;
 }
 

@@ -15,6 +15,7 @@ with no host synchronisation.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -31,6 +32,23 @@ from .trainer import CellRunner
 
 SEED_GRAPH, SEED_PARTITION, SEED_FEATURES, SEED_LABELS = 0x01, 0x02, 0x03, 0x04
 SEED_BATCHES, SEED_SAMPLER, SEED_MODEL, SEED_MERGE = 0x05, 0x06, 0x07, 0x08
+
+
+# Stream priorities of the graph loops: the training chain (latency-bound,
+# small grids) at high priority, the build / gather branch (throughput-bound,
+# fills every SM) at low priority, so freed SM slots go to training first.
+_TRAIN_PRIO = int(os.environ.get("HG_TRAIN_PRIO", "1"))
+# Resident build CTAs per SM on the graph loop's build branch (GroupLoop):
+# 3 x 256 threads x 48 registers leaves a GEMM / gather CTA room on every SM,
+# so the training branch is not starved while a group is being built.
+BUILD_CTAS_PER_SM = 3
+
+
+def _streams(dev):
+    """(capture stream for the training branch, side stream for the build branch)."""
+    if _TRAIN_PRIO:
+        return torch.cuda.Stream(dev, priority=-_TRAIN_PRIO), torch.cuda.Stream(dev, priority=0)
+    return torch.cuda.Stream(dev), torch.cuda.Stream(dev)
 
 
 def _u64_as_i64(vals) -> np.ndarray:
@@ -92,7 +110,7 @@ class GraphLoop:
         self.tr, self.runners, self.e2e = tr, runners, e2e
         dev = tr.device
         B = tr.B
-        self.side = torch.cuda.Stream(dev)
+        self._cap, self.side = _streams(dev)
         if e2e:
             self.pin_roots = [torch.empty(B, dtype=torch.int64).pin_memory() for _ in range(2)]
             self.pin_loss = [torch.zeros(1, dtype=torch.float32).pin_memory() for _ in range(2)]
@@ -106,7 +124,7 @@ class GraphLoop:
                 r.desc.agg1_ready = 1
                 r.n_roots = B
             g = torch.cuda.CUDAGraph()
-            cap = torch.cuda.Stream(dev)
+            cap = self._cap
             cap.wait_stream(cur)
             before = _lib.launch_count()
             with torch.cuda.graph(g, stream=cap):
@@ -171,7 +189,7 @@ class GroupLoop:
                 r.n_roots = B
         self.descp = [(C.POINTER(_lib.StepDesc) * G)(*[C.pointer(r.desc) for r in st])
                       for st in sets]
-        self.side = torch.cuda.Stream(dev)
+        self._cap, self.side = _streams(dev)
         if e2e:
             self.pin_roots = [torch.empty(G * B, dtype=torch.int64).pin_memory() for _ in range(2)]
             self.pin_loss = [torch.zeros(G, dtype=torch.float32).pin_memory() for _ in range(2)]
@@ -183,7 +201,7 @@ class GroupLoop:
         for x in range(2):
             nxt = self.gb[1 - x]
             g = torch.cuda.CUDAGraph()
-            cap = torch.cuda.Stream(dev)
+            cap = self._cap
             cap.wait_stream(cur)
             before = _lib.launch_count()
             with torch.cuda.graph(g, stream=cap):
@@ -195,7 +213,7 @@ class GroupLoop:
                     _lib.call("hg_iter_stage_group", tr._perm_buf.data_ptr(),
                               tr._states_buf.data_ptr(), tr.iters, tr._it_dev.data_ptr(), B, G,
                               G, G, None if e2e else nxt.roots.data_ptr(), nxt.keys.data_ptr(), ss)
-                    nxt.build(tr.graph, stream=ss)
+                    nxt.build(tr.graph, stream=ss, ctas_per_sm=BUILD_CTAS_PER_SM)
                     _lib.call("hg_step_prologue_group", self.descp[1 - x], G, 1, ss)
                 cs = cap.cuda_stream
                 for r in sets[x]:

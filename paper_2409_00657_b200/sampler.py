@@ -260,13 +260,16 @@ class GroupBuilder:
     def roots_ptr(self, b: int) -> int:
         return self.roots.data_ptr() + 8 * b * self.R
 
-    def build(self, g: Graph, stream=None, n_dev: int = None) -> None:
+    def build(self, g: Graph, stream=None, n_dev: int = None, ctas_per_sm: int = 0) -> None:
         """Build all K batches from self.roots / self.keys (R roots each;
-        batch b keyed by iteration state keys[b])."""
+        batch b keyed by iteration state keys[b]).  ctas_per_sm > 0 caps the
+        resident build CTAs per SM (persistent grid) to leave room for
+        concurrently running kernels."""
         s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
         _lib.call("hg_mg_build_group", g.offsets.data_ptr(), g.targets.data_ptr(), g.n_vertices,
                   self.roots.data_ptr(), self.R, self.K, n_dev, self.keys.data_ptr(), self.R,
-                  C.byref(self.layout), self.ws.data_ptr(), self.outs, self.err.data_ptr(), s)
+                  C.byref(self.layout), self.ws.data_ptr(), self.outs, self.err.data_ptr(),
+                  int(ctas_per_sm), s)
 
     def check(self, what="hg_mg_build_group"):
         code = int(self.err.item())
