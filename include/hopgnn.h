@@ -278,6 +278,11 @@ typedef struct {
   /* 1: the bf16 operand copies (Wlp, Wb, WcT, Wcp) already hold the current
    * parameters (hg_sgd_refresh ran last) -- the step skips its transposes */
   int32_t lowp_fresh;
+  /* per-layer bound on the sampled neighbours of a need[k] row (the fanout of
+   * the hop that produced layer k's pairs; 0 = unknown).  Sizes the shared-
+   * memory slots of the TMA-staged layer-1 gather; rows above it take the
+   * register path. */
+  int32_t max_deg[HG_MAX_LAYERS + 1];
 } hg_step_desc;
 
 /* Peer memory (one process per GPU): device allocations whose CUDA IPC

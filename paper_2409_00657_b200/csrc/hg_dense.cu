@@ -20,6 +20,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "hg_common.cuh"
 
@@ -40,6 +41,23 @@ template <typename T> struct Vec { static constexpr int N = 16 / sizeof(T); };
 template <typename T>
 __device__ __forceinline__ void load_vec(const T* p, float* v) {
   const uint4 raw = __ldg(reinterpret_cast<const uint4*>(p));
+  if constexpr (sizeof(T) == 4) {
+    v[0] = __uint_as_float(raw.x); v[1] = __uint_as_float(raw.y);
+    v[2] = __uint_as_float(raw.z); v[3] = __uint_as_float(raw.w);
+  } else {
+    const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+  }
+}
+
+// 16-byte vector from shared memory (TMA-staged rows)
+template <typename T>
+__device__ __forceinline__ void load_vec_s(const T* p, float* v) {
+  const uint4 raw = *reinterpret_cast<const uint4*>(p);
   if constexpr (sizeof(T) == 4) {
     v[0] = __uint_as_float(raw.x); v[1] = __uint_as_float(raw.y);
     v[2] = __uint_as_float(raw.z); v[3] = __uint_as_float(raw.w);
@@ -161,19 +179,31 @@ k_aggregate(RowSrc<T> rs, AggSegs<T> segs, int W, int out_ld, int pad_cap) {
   const int lane = threadIdx.x & 31, gi = lane / G, gl = lane % G;
   const int warps = blockDim.x >> 5;
   const int n_rows = *n_rows_dev;
-  for (int a0 = (blockIdx.x * warps + (threadIdx.x >> 5)) * P; a0 < n_rows;
-       a0 += gridDim.x * warps * P) {
-    const int a = a0 + gi;
-    const bool row_ok = a < n_rows;
-    int j0 = 0, deg = 0, sidx = 0;
-    if (row_ok) {
-      j0 = nbr_off[a];
-      deg = nbr_off[a + 1] - j0;
-      sidx = self_pos[a];
+  const int stride = gridDim.x * warps * P;
+  // Software pipeline over this warp's rows a, a+stride, ...: the CSR range
+  // and self index of row i+2 and the neighbour indices of row i+1 are in
+  // flight while row i's source rows load, so the dependent index chain
+  // (offsets -> indices -> rows) costs one DRAM round trip per row, not three.
+  int a = (blockIdx.x * warps + (threadIdx.x >> 5)) * P + gi;
+  auto meta = [&](int r, int& j0, int& deg, int& sidx) {
+    j0 = 0; deg = 0; sidx = 0;
+    if (r < n_rows) {
+      j0 = nbr_off[r];
+      deg = nbr_off[r + 1] - j0;
+      sidx = self_pos[r];
     }
-    int idx0 = gl < min(G, deg) ? nbr_idx[j0 + gl] : 0;
+  };
+  int j0, deg, sidx, j0n, degn, sidxn;
+  meta(a, j0, deg, sidx);
+  meta(a + stride, j0n, degn, sidxn);
+  int idx = gl < min(G, deg) ? nbr_idx[j0 + gl] : 0;
+  while (__any_sync(FULL, a < n_rows)) {
+    const bool row_ok = a < n_rows;
+    // prefetch: indices of the next row, range of the one after
+    const int idxn = gl < min(G, degn) ? nbr_idx[j0n + gl] : 0;
+    int j0nn, degnn, sidxnn;
+    meta(a + 2 * stride, j0nn, degnn, sidxnn);
     const T* sp = rs.row(row_ok ? sidx : 0);
-    // warp-uniform trip counts (groups of one warp hold different rows)
     const int max_deg = __reduce_max_sync(FULL, deg);
     T* o = out + (int64_t)a * out_ld;
     for (int c0 = 0; c0 < nvec; c0 += G) {
@@ -185,14 +215,14 @@ k_aggregate(RowSrc<T> rs, AggSegs<T> segs, int W, int out_ld, int pad_cap) {
       for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
       if (act) load_vec(sp + col, self);
       for (int jb = 0; jb < max_deg; jb += G) {       // neighbour chunks of G indices
-        const int idx = jb == 0 ? idx0 : (gl < deg - jb ? nbr_idx[j0 + jb + gl] : 0);
+        const int ix = jb == 0 ? idx : (gl < deg - jb ? nbr_idx[j0 + jb + gl] : 0);
         const int cnt = min(G, deg - jb);              // this group's neighbours in the chunk
         const int rounds = min(G, max_deg - jb);       // warp-uniform
         for (int t0 = 0; t0 < rounds; t0 += U) {
           uint4 x[U];
 #pragma unroll
           for (int t = 0; t < U; ++t) {
-            const int v = __shfl_sync(FULL, idx, (gi * G + ((t0 + t) & (G - 1))) & 31);
+            const int v = __shfl_sync(FULL, ix, (gi * G + ((t0 + t) & (G - 1))) & 31);
             if (act && t0 + t < cnt) x[t] = __ldg(reinterpret_cast<const uint4*>(rs.row(v) + col));
             else x[t] = make_uint4(0, 0, 0, 0);
           }
@@ -227,6 +257,216 @@ k_aggregate(RowSrc<T> rs, AggSegs<T> segs, int W, int out_ld, int pad_cap) {
         store_vec(o + col, acc);
       }
     }
+    a += stride;
+    j0 = j0n; deg = degn; sidx = sidxn; idx = idxn;
+    j0n = j0nn; degn = degnn; sidxn = sidxnn;
+  }
+}
+
+// ------------------------------------------------------------------ TMA-staged gather
+//
+// Layer-1 gather + aggregate with the source rows staged in shared memory by
+// bulk asynchronous copies (cp.async.bulk, completion counted in bytes on an
+// mbarrier).  Bytes in flight are then bounded by shared memory rather than
+// registers: one persistent CTA per SM keeps a ring of NS stages, each
+// holding a tile of TR destination rows with all their source rows
+// (self + up to max_deg neighbours).
+//   warp 0      producer: per tile, lane l owns row r0+l -- reads its CSR
+//               range and self index (coalesced across lanes), a warp scan
+//               places the rows' slots, one lane posts the tile's byte count
+//               on the stage's "full" barrier, every lane issues one 16-byte-
+//               aligned bulk copy per source row;
+//   warps 1..7  consumers: wait "full", reduce each row's slots from shared
+//               memory (16-byte lanes, G lanes per row), write agg, arrive on
+//               the stage's "empty" barrier.
+// Rows with more neighbours than the slots allow (never, when max_deg is the
+// sampling fanout) are reduced straight from global memory by the consumer.
+struct TmaMeta {
+  int32_t row;   // destination row
+  int32_t deg;
+  int32_t base;  // first slot (self), -1: not staged
+  int32_t self;  // self index (RowSrc)
+};
+
+__device__ __forceinline__ uint32_t sm_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void gbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void gbar_expect_arrive(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_addr(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void gbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void gbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n"
+      "}\n" ::"r"(sm_addr(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(sm_addr(dst)), "l"(src), "r"(bytes), "r"(sm_addr(bar)) : "memory");
+}
+
+constexpr int kTmaStages = 4;
+constexpr int kTmaThreads = 256;
+constexpr int kTmaConsumers = kTmaThreads / 32 - 1;
+
+template <typename T, bool SAGE>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+k_aggregate_tma(RowSrc<T> rs, AggSegs<T> segs, int n_segs, int cap_rows, int W, int out_ld,
+                int pad_cap, int TR, int slots, int max_deg) {
+  extern __shared__ __align__(128) uint8_t tsm[];
+  __shared__ __align__(8) uint64_t full_bar[kTmaStages], empty_bar[kTmaStages];
+  __shared__ TmaMeta meta[kTmaStages][32];
+  __shared__ int meta_n[kTmaStages];
+  constexpr int VEC = Vec<T>::N;
+  constexpr unsigned FULL = 0xffffffffu;
+  const int rowbytes = W * (int)sizeof(T);
+  const int stage_bytes = slots * rowbytes;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      gbar_init(&full_bar[s], 1);
+      gbar_init(&empty_bar[s], kTmaConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_trigger();
+  pdl_wait();
+  if (pad_cap && blockIdx.x == gridDim.x - 1) {
+    // tensor-core dW reduces over rows up to the next multiple of 64: zero them
+    for (int b = 0; b < n_segs; ++b) {
+      const int n = *segs.n_rows[b];
+      const int pad = min(pad_cap, (n + 63) / 64 * 64);
+      for (int64_t i = threadIdx.x; i < (int64_t)(pad - n) * out_ld; i += blockDim.x)
+        segs.out[b][(int64_t)n * out_ld + i] = from_f<T>(0.f);
+    }
+  }
+  const int tiles_per_seg = (cap_rows + TR - 1) / TR;
+  const int total_tiles = tiles_per_seg * n_segs;
+  if (warp == 0) {
+    // ---------------- producer
+    int i = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      const int b = t / tiles_per_seg;
+      const int r0 = (t % tiles_per_seg) * TR;
+      const int n = min(TR, *segs.n_rows[b] - r0);
+      if (n <= 0) continue;
+      const int s = i % kTmaStages;
+      if (i >= kTmaStages) gbar_wait(&empty_bar[s], ((i / kTmaStages) - 1) & 1);
+      const int32_t* off = segs.nbr_off[b];
+      int j0 = 0, deg = 0, self = 0, need = 0;
+      if (lane < n) {
+        j0 = off[r0 + lane];
+        deg = off[r0 + lane + 1] - j0;
+        self = segs.self_pos[b][r0 + lane];
+        need = deg <= max_deg ? deg + 1 : 0;
+      }
+      int base = need;  // inclusive warp scan -> exclusive slot base
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, base, o);
+        if (lane >= o) base += y;
+      }
+      const int total = __shfl_sync(FULL, base, 31);
+      base -= need;
+      if (lane < n) meta[s][lane] = TmaMeta{r0 + lane, deg, need ? base : -1, self};
+      __syncwarp();  // meta visible before the arrive releases the stage
+      if (lane == 0) {
+        meta_n[s] = n;
+        // tx bytes may land before the expectation is posted: the phase cannot
+        // complete before this arrival either way
+        gbar_expect_arrive(&full_bar[s], (uint32_t)(total * rowbytes));
+      }
+      if (need) {
+        uint8_t* dst = tsm + (size_t)s * stage_bytes + (size_t)base * rowbytes;
+        const int32_t* idx = segs.nbr_idx[b] + j0;
+        bulk_g2s(dst, rs.row(self), rowbytes, &full_bar[s]);
+        for (int j = 0; j < deg; ++j)
+          bulk_g2s(dst + (size_t)(j + 1) * rowbytes, rs.row(idx[j]), rowbytes, &full_bar[s]);
+      }
+      ++i;
+    }
+    return;
+  }
+  // ---------------- consumers
+  const int nvec = W / VEC;
+  const int G = nvec >= 32 ? 32 : (nvec >= 16 ? 16 : (nvec >= 8 ? 8 : (nvec >= 4 ? 4 : (nvec >= 2 ? 2 : 1))));
+  const int P = 32 / G;
+  const int gi = lane / G, gl = lane % G;
+  const int cw = warp - 1;
+  int i = 0;
+  for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+    const int b = t / tiles_per_seg;
+    const int r0 = (t % tiles_per_seg) * TR;
+    const int n_t = min(TR, *segs.n_rows[b] - r0);
+    if (n_t <= 0) continue;
+    const int s = i % kTmaStages;
+    gbar_wait(&full_bar[s], (i / kTmaStages) & 1);
+    const uint8_t* stage = tsm + (size_t)s * stage_bytes;
+    T* outb = segs.out[b];
+    for (int q = cw * P + gi; q - gi < n_t; q += kTmaConsumers * P) {
+      const bool ok = q < n_t;
+      TmaMeta m{0, 0, 0, 0};
+      if (ok) m = meta[s][q];
+      T* o = outb + (int64_t)m.row * out_ld;
+      for (int c0 = 0; c0 < nvec; c0 += G) {
+        const int cv = c0 + gl;
+        if (!ok || cv >= nvec) continue;
+        const int col = cv * VEC;
+        float self[VEC], acc[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[e] = 0.f;
+        if (m.base >= 0) {
+          const uint8_t* sl = stage + (size_t)m.base * rowbytes + col * sizeof(T);
+          load_vec_s(reinterpret_cast<const T*>(sl), self);
+          for (int j = 1; j <= m.deg; ++j) {
+            float x[VEC];
+            load_vec_s(reinterpret_cast<const T*>(sl + (size_t)j * rowbytes), x);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) acc[e] += x[e];
+          }
+        } else {  // more neighbours than slots: straight from global memory
+          load_vec(rs.row(m.self) + col, self);
+          const int32_t* off = segs.nbr_off[b];
+          const int j0 = off[m.row];
+          for (int j = 0; j < m.deg; ++j) {
+            float x[VEC];
+            load_vec(rs.row(segs.nbr_idx[b][j0 + j]) + col, x);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) acc[e] += x[e];
+          }
+        }
+        if constexpr (SAGE) {
+          float nb[VEC];
+          const float inv = m.deg > 0 ? 1.0f / (float)m.deg : 0.f;
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) nb[e] = m.deg > 0 ? acc[e] * inv : self[e];
+          store_vec(o + col, self);
+          store_vec(o + W + col, nb);
+        } else {
+          const float inv = 1.0f / (float)(m.deg + 1);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) acc[e] = (acc[e] + self[e]) * inv;
+          store_vec(o + col, acc);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) gbar_arrive(&empty_bar[s]);
+    ++i;
   }
 }
 
@@ -784,11 +1024,46 @@ static void launch_aggregate_n(const hg_step_desc* const* ds, int n, int k, cuda
     segs.out[b] = (T*)e->agg[k];
     cap = std::max(cap, e->max_rows[k]);
   }
+  // layer 1 with a known neighbour bound: TMA-staged persistent gather
+  // opt-in (HG_AGG_TMA=1): measured 3.7x slower than the register gather on
+  // the papers step -- one producer warp per SM serialises the index chain
+  static const bool tma_on = [] {
+    const char* e = getenv("HG_AGG_TMA");
+    return e && e[0] == '1';
+  }();
+  const int max_deg = d->max_deg[k];
+  const int rowbytes = Wd * (int)sizeof(T);
+  if (tma_on && k == 1 && max_deg > 0 && rowbytes % 16 == 0) {
+    constexpr int kSmemBudget = 200 * 1024;  // kTmaStages stages of TR rows x (max_deg+1) slots
+    const int per_row = (max_deg + 1) * rowbytes;
+    const int TR = std::min(32, kSmemBudget / kTmaStages / per_row);
+    if (TR >= 1) {
+      const int slots = TR * (max_deg + 1);
+      const size_t smem = (size_t)kTmaStages * slots * rowbytes;
+      static size_t smem_set[2] = {0, 0};
+      auto kern = d->arch == 1 ? k_aggregate_tma<T, true> : k_aggregate_tma<T, false>;
+      if (smem_set[d->arch == 1] < smem) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        smem_set[d->arch == 1] = smem;
+      }
+      const int pad_cap = pad && sizeof(T) == 2 ? d->max_rows[k] : 0;
+      prof_begin(PROF_AGG1, s);
+      count_launch();
+      launch_pdl(kern, dim3(num_sms()), dim3(kTmaThreads), smem, s, row_src<T>(d, k), segs, n,
+                 cap, Wd, d->in_dim[k], pad_cap, TR, slots, max_deg);
+      prof_end(PROF_AGG1, s);
+      return;
+    }
+  }
   // rows per CTA: 8 warps x (32 / lanes per row); blocks past the device row count exit
   const int nvec = Wd / (16 / (int)sizeof(T));
   const int lanes = nvec >= 32 ? 32 : nvec >= 16 ? 16 : nvec >= 8 ? 8 : nvec >= 4 ? 4 : nvec >= 2 ? 2 : 1;
   const int rows_per_cta = 8 * (32 / lanes);
-  dim3 grid(std::max(1, std::min((cap + rows_per_cta - 1) / rows_per_cta, num_sms() * 32)), n);
+  // a group of segments: one resident wave split over them, warps loop over
+  // their rows (the software pipeline pays off); one segment: a warp per
+  // row group over the capacity (every row's chain in flight at once)
+  const int wave = n > 1 ? std::max(1, num_sms() * HG_AGG_MINB / n) : num_sms() * 32;
+  dim3 grid(std::max(1, std::min((cap + rows_per_cta - 1) / rows_per_cta, wave)), n);
   const int pad_cap = pad && sizeof(T) == 2 ? d->max_rows[k] : 0;
   prof_begin(k == 1 ? PROF_AGG1 : PROF_AGG2, s);
   count_launch();

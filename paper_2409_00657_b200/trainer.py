@@ -55,6 +55,8 @@ class CellRunner:
         d.max_roots = max_roots
         for k in range(L + 1):
             d.max_rows[k] = self.max_rows[k]
+            # layer k's pairs come from hop L-k+1 (fanout[L-k], sampler.py:93-98)
+            d.max_deg[k] = int(fanout[L - k]) if k >= 1 else 0
             d.root_rows[k] = lay.cap_need[k]
             d.in_dim[k] = model.in_dim[k]
         d.split_k = split_k or max(1, min(64, self.max_rows[1] // 2048))
