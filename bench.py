@@ -389,7 +389,7 @@ def _run_ours(args, cfg, dev):
     tp = os.path.join(HERE, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(args.config)
+            traffic = json.load(open(tp)).get(args.config if G > 1 else args.config + "_g1")
         except Exception:
             traffic = None
     line = {
