@@ -283,6 +283,11 @@ typedef struct {
    * memory slots of the TMA-staged layer-1 gather; rows above it take the
    * register path. */
   int32_t max_deg[HG_MAX_LAYERS + 1];
+  /* 1: lowp_scratch holds one bf16 dz region per layer (rows max_rows[1] +
+   * ... + max_rows[L], layer k after layers 1..k-1), so a layer's weight-
+   * gradient GEMM can run on a forked stream while the next layer's scatter
+   * writes its own dz; 0: one shared region (serial backward). */
+  int32_t lowp_layered;
 } hg_step_desc;
 
 /* Peer memory (one process per GPU): device allocations whose CUDA IPC

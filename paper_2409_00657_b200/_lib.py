@@ -69,7 +69,8 @@ class StepDesc(C.Structure):
                 ("stage_base", C.c_void_p), ("stage_row", C.c_void_p), ("rank", C.c_int32),
                 ("agg1_ready", C.c_int32), ("WcT", C.c_void_p), ("Wcp", C.c_void_p),
                 ("dl_lowp", C.c_void_p), ("root_rows", C.c_int32 * 7),
-                ("lowp_fresh", C.c_int32), ("max_deg", C.c_int32 * 7)]
+                ("lowp_fresh", C.c_int32), ("max_deg", C.c_int32 * 7),
+                ("lowp_layered", C.c_int32)]
 
 
 V, I32, I64, U64, SZ = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_size_t

@@ -20,6 +20,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cstdlib>
 
 #include "hg_common.cuh"
@@ -1092,6 +1093,38 @@ static void scatter_root_attrs() {
   done = true;
 }
 
+// bf16 dz operand of layer k (per-layer region when lowp_layered)
+static inline bf16* dz_lowp(const hg_step_desc* d, int k) {
+  int64_t rows = 0;
+  if (d->lowp_layered)
+    for (int j = 1; j < k; ++j) rows += d->max_rows[j];
+  return (bf16*)d->lowp_scratch + rows * d->hidden;
+}
+
+// Forked stream of the backward pass: weight-gradient GEMMs (gW_c, gW_k for
+// k >= 2) depend on nothing later in the step but the final SGD, so they run
+// beside the dX -> scatter chain (joined at the end of the step; event
+// fork/join is captured as graph edges).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev[2 * HG_MAX_LAYERS + 4];
+};
+static SideStream* side_stream() {
+  static std::mutex mu;
+  static SideStream per_dev[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  SideStream& ss = per_dev[dev & 63];
+  if (!ss.s) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&ss.s, cudaStreamNonBlocking, hi) != cudaSuccess) return nullptr;
+    for (auto& e : ss.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  }
+  return &ss;
+}
+
 template <typename T>
 static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool backward) {
   const int L = d->n_layers;
@@ -1102,6 +1135,22 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
   // tensor-core path: bf16 operands, H a multiple of 64 up to 256 (one N tile)
   const bool tc = sizeof(T) == 2 && d->use_tc && H % 64 == 0 && H <= 256;
   scatter_root_attrs<T>();
+  // forked weight-gradient GEMMs (one side stream; joined before returning)
+  SideStream* side = backward && tc ? side_stream() : nullptr;
+  int n_fork = 0;
+  auto fork = [&]() -> cudaStream_t {
+    if (!side || n_fork >= 2 * HG_MAX_LAYERS + 2) return s;
+    cudaEventRecord(side->ev[n_fork], s);
+    cudaStreamWaitEvent(side->s, side->ev[n_fork], 0);
+    ++n_fork;
+    return side->s;
+  };
+  auto join = [&]() {
+    if (!n_fork) return;
+    cudaEventRecord(side->ev[n_fork], side->s);
+    cudaStreamWaitEvent(s, side->ev[n_fork], 0);
+    n_fork = 0;
+  };
   // ---- forward
   prof_begin(PROF_STEP, s);
   if (tc && !d->lowp_fresh) {
@@ -1154,11 +1203,11 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
       dim3 g((H + 31) / 32, 16);
       count_launch();
       launch_pdl(k_mask_colsum<T>, dim3(g), dim3(256), 0, s, d->dh[L], (const T*)d->h[L], tot + L, H, d->gb[L],
-                                         (bf16*)d->lowp_scratch, d->max_rows[L]);
-      // gW_c += h_Lᵀ dlogits (both MN-major, reduction over the roots)
+                                         dz_lowp(d, L), d->max_rows[L]);
+      // gW_c += h_Lᵀ dlogits (both MN-major, reduction over the roots), forked
       const int split = std::max(1, std::min(16, n_roots / 256));
       st = umma_gemm(d->h[L], H, true, d->dl_lowp, Cp, true, d->gWc, C, H, C, n_roots,
-                     nullptr, tot + L, 2, nullptr, split, s);
+                     nullptr, tot + L, 2, nullptr, split, fork());
       if (st) return st;
     }
   } else {
@@ -1172,7 +1221,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     count_launch();
     k_head<T><<<grid, 256, smem, s>>>((const T*)d->h[L], d->Wc, H, C, d->roots, n_roots,
                                       tot + L, d->label_state, d->logits, d->loss, d->dh[L],
-                                      tc ? (bf16*)d->lowp_scratch : nullptr, d->max_rows[L],
+                                      tc ? dz_lowp(d, L) : nullptr, d->max_rows[L],
                                       d->gb[L], backward ? 1 : 0);
   }
   if (!backward) { prof_end(PROF_STEP, s); return HG_OK; }
@@ -1192,8 +1241,10 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
       const int tiles = (d->in_dim[k] + 127) / 128;
       int split = (kblocks + 5) / 6;
       split = std::max(1, std::min(split, std::max(1, num_sms() / tiles)));
-      int st = umma_gemm(d->agg[k], d->in_dim[k], true, d->lowp_scratch, H, true, d->gW[k], H,
-                         d->in_dim[k], H, d->max_rows[k], nullptr, tot + k, 2, nullptr, split, s);
+      // layers >= 2 (own dz region): beside the dX -> scatter chain
+      cudaStream_t ws = k >= 2 && d->lowp_layered ? fork() : s;
+      int st = umma_gemm(d->agg[k], d->in_dim[k], true, dz_lowp(d, k), H, true, d->gW[k], H,
+                         d->in_dim[k], H, d->max_rows[k], nullptr, tot + k, 2, nullptr, split, ws);
       if (st) return st;
     } else {
       gemm<T, true, false, EPI_ATOMIC, float, T>(s, (const T*)d->agg[k], d->in_dim[k], d->dh[k], H,
@@ -1204,7 +1255,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     if (k == 1) { prof_end(PROF_DW1, s); break; }  // layer-1 dX is unused (features are not trainable)
     // dagg_k = dz_k W_k^T
     if (tc && d->in_dim[k] % 64 == 0 && d->Wb[k]) {
-      int st = umma_gemm(d->lowp_scratch, H, false, d->Wb[k], H, false, d->dagg, d->in_dim[k],
+      int st = umma_gemm(dz_lowp(d, k), H, false, d->Wb[k], H, false, d->dagg, d->in_dim[k],
                          d->max_rows[k], d->in_dim[k], H, tot + k, nullptr, 0, nullptr, 1, s);
       if (st) return st;
     } else {
@@ -1224,13 +1275,13 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
         launch_pdl(k_scatter_root<true, T>, dim3(grid), dim3(256), root_smem, s, 
             d->dagg, d->in_dim[k], d->mg.need_off[k - 1], d->mg.need_off[k], d->mg.self_pos[k],
             d->mg.nbr_off[k], d->mg.nbr_idx[k], n_roots, H, (const T*)d->h[k - 1],
-            want_f32 ? d->dh[k - 1] : nullptr, tc ? (bf16*)d->lowp_scratch : nullptr,
+            want_f32 ? d->dh[k - 1] : nullptr, tc ? dz_lowp(d, k - 1) : nullptr,
             d->gb[k - 1], tot + (k - 1), d->max_rows[k - 1]);
       else
         launch_pdl(k_scatter_root<false, T>, dim3(grid), dim3(256), root_smem, s, 
             d->dagg, d->in_dim[k], d->mg.need_off[k - 1], d->mg.need_off[k], d->mg.self_pos[k],
             d->mg.nbr_off[k], d->mg.nbr_idx[k], n_roots, H, (const T*)d->h[k - 1],
-            want_f32 ? d->dh[k - 1] : nullptr, tc ? (bf16*)d->lowp_scratch : nullptr,
+            want_f32 ? d->dh[k - 1] : nullptr, tc ? dz_lowp(d, k - 1) : nullptr,
             d->gb[k - 1], tot + (k - 1), d->max_rows[k - 1]);
       continue;
     }
@@ -1247,9 +1298,10 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
                                             d->dh[k - 1]);
     dim3 g((H + 31) / 32, 64);
     launch_pdl(k_mask_colsum<T>, dim3(g), dim3(256), 0, s, d->dh[k - 1], (const T*)d->h[k - 1], tot + (k - 1), H,
-                                       d->gb[k - 1], tc ? (bf16*)d->lowp_scratch : nullptr,
+                                       d->gb[k - 1], tc ? dz_lowp(d, k - 1) : nullptr,
                                        d->max_rows[k - 1]);
   }
+  join();
   prof_end(PROF_STEP, s);
   return HG_OK;
 }

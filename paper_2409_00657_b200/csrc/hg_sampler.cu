@@ -28,7 +28,10 @@
 
 namespace hg {
 
-constexpr int kBuildThreads = 256;
+#ifndef HG_BUILD_THREADS
+#define HG_BUILD_THREADS 256
+#endif
+constexpr int kBuildThreads = HG_BUILD_THREADS;
 #ifndef HG_BUILD_MINB
 #define HG_BUILD_MINB 5  // resident build CTAs per SM (48 regs): leaves room for the training branch
 #endif

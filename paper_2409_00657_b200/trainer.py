@@ -45,7 +45,8 @@ class CellRunner:
         self.dagg = torch.empty(dagg_rows, dtype=torch.float32, device=dev)
         self.logits = torch.empty((max_roots, model.C), dtype=torch.float32, device=dev)
         self.loss = torch.zeros(max_roots, dtype=torch.float32, device=dev)
-        self.lowp = torch.empty((self.max_rows[1], H), dtype=torch.bfloat16, device=dev)
+        # one bf16 dz region per layer (hg_step_desc.lowp_layered)
+        self.lowp = torch.empty((sum(self.max_rows[1:]), H), dtype=torch.bfloat16, device=dev)
         self.roots = torch.zeros(max_roots, dtype=torch.int64, device=dev)
         self.keys = torch.zeros(max(max_roots, 1), dtype=torch.int64, device=dev)
         d = _lib.StepDesc()
@@ -84,6 +85,7 @@ class CellRunner:
         d.logits = self.logits.data_ptr()
         d.loss = self.loss.data_ptr()
         d.lowp_scratch = self.lowp.data_ptr()
+        d.lowp_layered = 1
         # bf16 operand copies of the parameters: one set per model, shared by
         # every runner (steps are serialised on the training stream), so a
         # fused SGD + refresh (hg_sgd_refresh) keeps all of them current
