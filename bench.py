@@ -471,12 +471,18 @@ def run_distributed(args, cfg):
                        cfg["classes"], chain(cfg["seed"], 0x07), dev)
     B = cfg["batch"]
     mode = args.mode
+    # N > 1: the per-iteration three-stage loop (DistGraphLoop) unless --group is
+    # given: grouping the build measured neutral here (N=2: 11.03M vs 11.07M seeds/s),
+    # the per-iteration pre-gather + staged gather branch is what bounds the step
+    G = max(1, int(args.group))
     tr = MicrographTrainer(g, part, model, cfg["fanout"], B, cfg["seed"], mode=mode,
-                           pregather=args.pregather)
+                           pregather=args.pregather, graph_group=G)
     iters = tr.begin_epoch(0)
     torch.cuda.synchronize()
     setup_s = time.time() - t0
     K, W = args.steps, args.warmup
+    if G > 1:  # warm-up: two eager steps, then one replay of each of the three group graphs
+        W = max(W, 2 + 3 * G)
     for i in range(W):
         tr.step(i, want_loss=False)
     torch.cuda.synchronize()
@@ -508,7 +514,7 @@ def run_distributed(args, cfg):
     graph_on = tr._dgl is not None
     launches = _lib.launch_count() if rank == 0 else 0
     if graph_on:
-        launches += K * tr._dgl.launches
+        launches += (K // G if G > 1 else K) * tr._dgl.launches  # launches per replay
     led = tr.global_ledger()
     traffic = torch.tensor([tr.traffic.total(), tr.traffic.feature_bytes,
                             tr.traffic.hop_bytes, tr.traffic.allreduce_bytes], device=dev)
@@ -545,15 +551,17 @@ def run_distributed(args, cfg):
         L_ = len(cfg["fanout"])
         tot_ = tr.runners[0].builder.tensors["totals"].cpu().numpy()
         agg_bytes = gather_bytes([(int(tot_[0]), int(tot_[1]), int(tot_[L_ + 1]))], cfg)
-    # end to end: same public step, loss read back every step (W untimed warm-up steps)
-    for i in range(W):
+    # end to end: same public step, loss read back every step (W2 untimed warm-up steps,
+    # a whole number of groups so the timed steps start on a group boundary)
+    W2 = -(-W // G) * G
+    for i in range(W2):
         tr.step(W + 2 * K + i, want_loss=True)
     tr.last_loss()
     torch.cuda.synchronize()
     dist.barrier()
     e0 = time.perf_counter()
     for i in range(K):
-        tr.step(2 * W + 2 * K + i, want_loss=True)  # returns the previous step's loss
+        tr.step(W + W2 + 2 * K + i, want_loss=True)  # returns the previous step's loss
     tr.last_loss()
     torch.cuda.synchronize()
     e2e_s = torch.tensor([time.perf_counter() - e0], device=dev)
@@ -572,7 +580,7 @@ def run_distributed(args, cfg):
     mc_ms = None
     if not args.no_model_centric:
         mc_tr = MicrographTrainer(g, part, model, cfg["fanout"], B, cfg["seed"],
-                                  pregather=False, strategy="model-centric")
+                                  pregather=False, strategy="model-centric", graph_group=G)
         mc_tr.begin_epoch(0)
         for i in range(W):
             mc_tr.step(i, want_loss=False)
@@ -613,6 +621,7 @@ def run_distributed(args, cfg):
             "data": "synthetic (GPU-generated graph, keyed features/labels/weights)",
             "config": {"workload": cfg["workload"], "global_batch": S * B,
                        "fanout": list(cfg["fanout"]), "hidden": cfg["hidden"],
+                       "run_ahead_group": G,
                        "parallelism": f"micrograph x{S} ({mode}; features sharded by planted "
                                       "block, CSR replicated; remote rows "
                                       + ("pre-gathered by NCCL all-to-all)" if args.pregather

@@ -462,6 +462,105 @@ class DistGraphLoop:
         self.graphs[x].replay()
 
 
+class DistGroupLoop:
+    """DistGraphLoop over groups of G iterations (the N > 1 counterpart of
+    engine.GroupLoop).  Three sets of G runners rotate; replay x trains group
+    g (set x: G train steps, each followed by the NCCL all-reduce + SGD),
+    pre-gathers and layer-1-gathers group g+1 iteration by iteration (set
+    x+1; the mailbox staging is reused per iteration, the ledger row follows
+    the gather cursor) and stages + builds group g+2 in ONE launch (set x+2,
+    hg_mg_build_group with per-batch device root counts, persistent grid
+    beside the other branches).  Semantics are those of DistGraphLoop."""
+
+    def __init__(self, tr: "MicrographTrainer", cap: int, G: int):
+        from .engine import BUILD_CTAS_PER_SM, _streams
+        from .sampler import GroupBuilder
+        self.tr, self.cap, self.G = tr, int(cap), int(G)
+        dev = tr.device
+        mk = lambda: CellRunner(tr.graph, tr.runners[0].table, tr.model, tr.fanout,  # noqa: E731
+                                tr.runners[0].max_roots, tr.labels)
+        self.sets = [[mk() for _ in range(G)] for _ in range(3)]
+        self.gb = [GroupBuilder([r.builder for r in st], per_batch=self.cap) for st in self.sets]
+        for st, gb in zip(self.sets, self.gb):
+            for j, r in enumerate(st):
+                tr.feats.bind_staged(r, tr._stage_cap)
+                r.desc.roots = gb.roots_ptr(j)
+                r.desc.agg1_ready = 1
+        self.ctas_per_sm = BUILD_CTAS_PER_SM
+        cap_s, self.side_build = _streams(dev)
+        self.side_gather = torch.cuda.Stream(dev)
+        self.pin_loss = [torch.zeros(1, dtype=torch.float32).pin_memory() for _ in range(3)]
+        self._dummy = torch.zeros(2, dtype=torch.int64, device=dev)
+        m = tr.model
+        total = tr.S * tr.B
+        self.graphs = []
+        cur = torch.cuda.current_stream(dev)
+        before = _lib.launch_count()
+        for x in range(3):
+            run, nxt, nxt2 = (self.sets[(x + j) % 3] for j in range(3))
+            g = torch.cuda.CUDAGraph()
+            cap_s.wait_stream(cur)
+            with torch.cuda.graph(g, stream=cap_s):
+                self.side_build.wait_stream(cap_s)
+                self.side_gather.wait_stream(cap_s)
+                with torch.cuda.stream(self.side_build):
+                    self.build_ops((x + 2) % 3, self.side_build.cuda_stream)
+                with torch.cuda.stream(self.side_gather):
+                    self.gather_ops((x + 1) % 3, self.side_gather.cuda_stream)
+                cs = cap_s.cuda_stream
+                for r in run:
+                    r.desc.lowp_fresh = 1 if r.tc else 0
+                    _lib.call("hg_train_step", C.byref(r.desc), self.cap, cs)
+                    r.desc.lowp_fresh = 0
+                    if r.tc:
+                        _lib.call("hg_allreduce_sgd_refresh", tr._comm, C.byref(r.desc),
+                                  m.flat.data_ptr(), m.grad.data_ptr(), m.flat.numel(),
+                                  float(tr.lr), 1.0 / total, cs)
+                    else:
+                        _lib.call("hg_allreduce_sgd", tr._comm, m.flat.data_ptr(),
+                                  m.grad.data_ptr(), m.flat.numel(), float(tr.lr), 1.0 / total,
+                                  cs)
+                self.pin_loss[x].copy_(torch.stack([r.loss[:self.cap].sum() for r in run])
+                                       .sum().reshape(1), non_blocking=True)
+                cap_s.wait_stream(self.side_build)
+                cap_s.wait_stream(self.side_gather)
+            cur.wait_stream(cap_s)
+            self.graphs.append(g)
+        self.launches = (_lib.launch_count() - before) // 3
+        self.iters = tr.iters
+
+    def build_ops(self, k: int, s, ctas_per_sm: int = None) -> None:
+        """Build cursor+1 .. cursor+G into set k; the cursor moves by G."""
+        tr, gb, G = self.tr, self.gb[k], self.G
+        for j in range(G):
+            _lib.call("hg_iter_stage_ranged", tr._g_roots.data_ptr(), tr._g_ranges.data_ptr(),
+                      tr._g_states.data_ptr(), tr.iters, tr._g_it.data_ptr(), self.cap, 1 + j,
+                      G if j == G - 1 else 0, gb.roots_ptr(j), gb.n_dev.data_ptr() + 4 * j,
+                      gb.keys.data_ptr() + 8 * j, s)
+        gb.build(tr.graph, stream=s, n_dev=gb.n_dev.data_ptr(),
+                 ctas_per_sm=self.ctas_per_sm if ctas_per_sm is None else ctas_per_sm)
+
+    def gather_ops(self, k: int, s) -> None:
+        """Per iteration of set k: advance the gather cursor, pre-gather (ledger
+        row = that iteration), layer-1 gather."""
+        tr = self.tr
+        for r in self.sets[k]:
+            _lib.call("hg_iter_stage_ranged", tr._g_roots.data_ptr(), tr._g_ranges.data_ptr(),
+                      tr._g_states.data_ptr(), tr.iters, tr._g_pg.data_ptr(), 0, 1, 1,
+                      self._dummy.data_ptr(), self._dummy.data_ptr(),
+                      self._dummy.data_ptr() + 8, s)
+            tr.feats.pregather(r, tr._acct_rows.data_ptr(), tr._acct_total.data_ptr(), s,
+                               it_dev_ptr=tr._g_pg.data_ptr())
+            _lib.call("hg_step_prologue", C.byref(r.desc), self.cap, 1, s)
+
+    def replay(self, x: int) -> None:
+        self.graphs[x].replay()
+
+    def check(self) -> None:
+        for gb in self.gb:
+            gb.check()
+
+
 # ---------------------------------------------------------------- trainer
 
 class MicrographTrainer:
@@ -470,7 +569,7 @@ class MicrographTrainer:
     def __init__(self, graph: Graph, part: PartitionMap, model: ModelState, fanout, batch: int,
                  seed: int, lr: float = 0.1, dtype=torch.bfloat16, mode: str = "fused",
                  iterations: int = 0, group=None, use_tc: bool = True, pregather: bool = True,
-                 strategy: str = "micrograph", graphs: bool = True):
+                 strategy: str = "micrograph", graphs: bool = True, graph_group: int = 1):
         """strategy="micrograph": HopGNN feature-centric training (engine.py:562-623);
         "model-centric": the baseline it is measured against (engine.py:482-507) --
         GPU d trains all of batch d, fetching every remote row its micrographs
@@ -487,7 +586,10 @@ class MicrographTrainer:
         self.strategy = strategy
         self.pregather = pregather
         self.graphs = graphs
-        self._dgl = None       # DistGraphLoop
+        self._dgl = None       # DistGraphLoop / DistGroupLoop
+        # iterations per graph replay (DistGroupLoop when > 1)
+        self.graph_group = max(1, min(int(graph_group), _lib.MAX_GROUP))
+        self._gdone = None     # iterations < _gdone are already enqueued by a group replay
         self._gnext = None     # iteration the graph loop is positioned at
         self._eager_fast = 0   # eager fast-path steps taken (library warm-up before capture)
         self.group = group
@@ -608,6 +710,7 @@ class MicrographTrainer:
         self._g_cap = cap if self._dgl is None else self._dgl.cap
         self._acct_row_ptr(it_n - 1)
         self._gnext = None
+        self._gdone = None
 
     def _graph_loop(self):
         if self._dgl is None:
@@ -622,7 +725,10 @@ class MicrographTrainer:
                 r.desc.roots = r.roots.data_ptr()
                 r.desc.agg1_ready = 1
                 self.feats.bind_staged(r, self._stage_cap)
-            self._dgl = DistGraphLoop(self, self._g_cap)
+            if self.graph_group > 1:
+                self._dgl = DistGroupLoop(self, self._g_cap, self.graph_group)
+            else:
+                self._dgl = DistGraphLoop(self, self._g_cap)
         return self._dgl
 
     def _drain_run_ahead(self) -> None:
@@ -671,6 +777,55 @@ class MicrographTrainer:
         self._fast_iters = getattr(self, "_fast_iters", 0) + 1
         self.traffic.allreduce_bytes += 2.0 * (self.S - 1) / self.S * self.flat_bytes
         self._gnext = it + 1
+        return prev
+
+    def _step_group(self, gl: "DistGroupLoop", it: int, want_loss: bool):
+        """Group replay: trains it..it+G-1, gathers the next group, builds the
+        one after (see DistGroupLoop)."""
+        G = gl.G
+        if self._gnext != it:
+            # position: group it built + pre-gathered + gathered into set 0,
+            # group it+G built into set 1 (eagerly, on this stream)
+            self._drain_run_ahead()
+            for st, gb in zip(gl.sets, gl.gb):
+                for j, r in enumerate(st):
+                    r.desc.roots = gb.roots_ptr(j)
+                    r.desc.agg1_ready = 1
+                    self.feats.bind_staged(r, self._stage_cap)
+            for j in range(it, min(it + G, self.iters)):
+                self._acct_rows[j].zero_()  # an eager run-ahead may have charged these
+            cs = torch.cuda.current_stream(self.device).cuda_stream
+            self._g_it.fill_(it - 1)
+            self._g_pg.fill_(it - 1)
+            gl.build_ops(0, cs, ctas_per_sm=0)
+            gl.gather_ops(0, cs)
+            gl.build_ops(1, cs, ctas_per_sm=0)
+            r0 = gl.sets[0][0]
+            if r0.tc:  # replays start from bf16 operands matching the parameters
+                m = self.model
+                _lib.call("hg_sgd_refresh", C.byref(r0.desc), m.flat.data_ptr(),
+                          m.grad.data_ptr(), m.flat.numel(), 0.0, 1.0, 0, cs)
+            self._acct_iters = getattr(self, "_acct_iters", set())
+            self._acct_iters.update(range(it, min(it + G, self.iters)))
+            self._gx = 0
+        x = self._gx
+        prev = None
+        while self._loss_pending and any(b is gl.pin_loss[x] for _, b in self._loss_pending):
+            prev = self._drain_loss()
+        gl.replay(x)  # trains it..it+G-1, gathers the next group, builds the one after
+        ev = torch.cuda.Event()
+        ev.record()
+        self._loss_pending.append((ev, gl.pin_loss[x]))
+        if want_loss and prev is None and len(self._loss_pending) > 2:
+            prev = self._drain_loss()
+        if not want_loss:
+            prev = None
+        self._acct_iters = getattr(self, "_acct_iters", set())
+        self._acct_iters.update(range(it + G, min(it + 2 * G, self.iters)))
+        self._fast_iters = getattr(self, "_fast_iters", 0) + G
+        self.traffic.allreduce_bytes += G * 2.0 * (self.S - 1) / self.S * self.flat_bytes
+        self._gx = (x + 1) % 3
+        self._gnext = self._gdone = it + G
         return prev
 
     def batches(self, it: int):
@@ -799,7 +954,7 @@ class MicrographTrainer:
         s = torch.cuda.current_stream(self.device).cuda_stream
         self._eager_fast += 1
         if self._gnext is not None:
-            if self._gnext == it and self._dgl is not None:
+            if self._gnext == it and isinstance(self._dgl, DistGraphLoop):
                 # the graph loop already built `it` into runner it%3: train it here
                 return self._train_built(self._dgl.runners[it % 3], it, want_loss)
             self._drain_run_ahead()
@@ -891,7 +1046,27 @@ class MicrographTrainer:
         (a host sync) or None when want_loss is False."""
         if (self.mode == "fused" and (not self.table.removed or self.strategy == "model-centric")
                 and self._comm_ok and len(self.perm) >= (it + 1) * self.S * self.B):
-            if self._graph_eligible() and hasattr(self, "_g_roots") and it + 1 < self.iters:
+            G = self.graph_group
+            if G > 1:
+                if self._gdone is not None and self._gdone - G <= it < self._gdone:
+                    return None  # enqueued by the last group replay
+                if (self._graph_eligible() and hasattr(self, "_g_roots")
+                        and it + 2 * G <= self.iters):
+                    gl = self._graph_loop()
+                    if gl is not None:
+                        return self._step_group(gl, it, want_loss)
+                if self._gnext == it and isinstance(self._dgl, DistGroupLoop):
+                    # leaving the group loop: the last replay already pre-gathered
+                    # (and charged) iterations it..it+G-1 into set _gx: train them
+                    gl, x, out = self._dgl, self._gx, None
+                    for j in range(G):
+                        if it + j < self.iters:
+                            out = self._train_built(gl.sets[x][j], it + j, want_loss)
+                    self._gdone = it + G
+                    return out
+                self._gdone = None
+            elif (self._graph_eligible() and hasattr(self, "_g_roots")
+                    and it + 1 < self.iters):
                 gl = self._graph_loop()
                 if gl is not None:
                     return self._step_graph(gl, it, want_loss)

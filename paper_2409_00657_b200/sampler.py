@@ -242,19 +242,24 @@ class GroupBuilder:
     Owns the group's contiguous roots [K*R], iteration states [K] and
     workspace (fixed addresses: graph-capturable)."""
 
-    def __init__(self, builders):
+    def __init__(self, builders, per_batch: int = None):
         if not 1 <= len(builders) <= MAX_GROUP:
             raise ValueError(f"group of {len(builders)} batches (1..{MAX_GROUP})")
         self.builders = list(builders)
         b0 = self.builders[0]
         if any(b.fanout != b0.fanout or b.max_roots != b0.max_roots for b in self.builders):
             raise ValueError("grouped builders must share fanout and capacity")
-        self.K, self.R, self.layout, self.device = len(builders), b0.max_roots, b0.layout, b0.device
+        self.K, self.layout, self.device = len(builders), b0.layout, b0.device
+        # roots per batch (the stride of the roots buffer; <= builder capacity)
+        self.R = b0.max_roots if per_batch is None else int(per_batch)
+        if not 1 <= self.R <= b0.max_roots:
+            raise ValueError(f"per_batch {self.R} outside 1..{b0.max_roots}")
         i32 = dict(dtype=torch.int32, device=self.device)
         self.ws = torch.empty(self.K * self.R * self.layout.ws_root_ints, **i32)
         self.roots = torch.zeros(self.K * self.R, dtype=torch.int64, device=self.device)
         self.keys = torch.zeros(self.K, dtype=torch.int64, device=self.device)
         self.err = torch.zeros(1, **i32)
+        self.n_dev = torch.zeros(self.K, **i32)  # per-batch device root counts (optional)
         self.outs = (_lib.MgBatch * self.K)(*[b.cbatch for b in self.builders])
 
     def roots_ptr(self, b: int) -> int:

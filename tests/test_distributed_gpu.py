@@ -78,3 +78,21 @@ def test_graph_loop_matches_oracle(strategy):
     res = json.load(open(os.path.join(d, "res.0")))
     assert res["ok"], res["msg"]
     assert res["graph_used"], "graph loop never engaged"
+
+
+@pytest.mark.parametrize("strategy", ["micrograph", "model-centric"])
+def test_group_loop_matches_oracle(strategy):
+    """DistGroupLoop (2 iterations per replay): grouped builds with per-batch
+    device root counts, per-iteration pre-gathers and ledger rows, the exit
+    path that trains the already pre-gathered group -- ledger and parameters
+    equal the oracle's."""
+    import dist_helpers
+    world = _world()
+    d = tempfile.mkdtemp()
+    mp.spawn(dist_helpers.micrograph_worker,
+             args=(world, os.path.join(d, "init"), os.path.join(d, "res"), "fused", "f32", "peer",
+                   strategy, 9, 2),
+             nprocs=world, join=True)
+    res = json.load(open(os.path.join(d, "res.0")))
+    assert res["ok"], res["msg"]
+    assert res["graph_used"], "group loop never engaged"
