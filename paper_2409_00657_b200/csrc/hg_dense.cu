@@ -966,8 +966,7 @@ __global__ void k_sgd(float* __restrict__ p, float* __restrict__ g, bf16* __rest
 
 int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb, bool b_mn,
               void* C, int64_t ldc, int M, int N, int K, const int32_t* M_dev,
-              const int32_t* K_dev, int epi, const float* bias, int split, cudaStream_t s,
-              const void* mask = nullptr, float* colsum = nullptr);
+              const int32_t* K_dev, int epi, const float* bias, int split, cudaStream_t s);
 
 static int g_num_sms = 0;
 static int num_sms() {
@@ -1094,11 +1093,6 @@ static void scatter_root_attrs() {
   done = true;
 }
 
-static bool getenv_on(const char* name) {  // A/B switches: NAME=1 enables a variant
-  const char* e = getenv(name);
-  return e && e[0] == '1';
-}
-
 // bf16 dz operand of layer k (per-layer region when lowp_layered)
 static inline bf16* dz_lowp(const hg_step_desc* d, int k) {
   int64_t rows = 0;
@@ -1202,24 +1196,14 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
                                                    d->label_state, d->loss,
                                                    (bf16*)d->dl_lowp, Cp);
     if (backward) {
-      // dz_L = (dlogits @ W_cᵀ) * (h_L > 0) as bf16 (the dW / dX operand) and
-      // gb_L += colsum(dz_L).  Opt-in (HG_FUSE_MASK=1): all of it in the GEMM
-      // epilogue (UEPI_MASK_BF16) -- measured slower (train chain 65 -> 70 us:
-      // the per-column warp reductions of the bias gradient cost more than the
-      // separate k_mask_colsum launch)
-      if (sizeof(T) == 2 && getenv_on("HG_FUSE_MASK")) {
-        st = umma_gemm(d->dl_lowp, Cp, false, d->Wcp, Cp, false, dz_lowp(d, L), H, n_roots, H,
-                       Cp, tot + L, nullptr, 3, nullptr, 1, s, d->h[L], d->gb[L]);
-        if (st) return st;
-      } else {
-        st = umma_gemm(d->dl_lowp, Cp, false, d->Wcp, Cp, false, d->dh[L], H, n_roots, H, Cp,
-                       tot + L, nullptr, 0, nullptr, 1, s);
-        if (st) return st;
-        dim3 g((H + 31) / 32, 16);
-        count_launch();
-        launch_pdl(k_mask_colsum<T>, dim3(g), dim3(256), 0, s, d->dh[L], (const T*)d->h[L], tot + L,
-                   H, d->gb[L], dz_lowp(d, L), d->max_rows[L]);
-      }
+      // dz_L = (dlogits @ W_cᵀ) * (h_L > 0); gb_L; bf16 dz_L for the dW GEMM
+      st = umma_gemm(d->dl_lowp, Cp, false, d->Wcp, Cp, false, d->dh[L], H, n_roots, H, Cp,
+                     tot + L, nullptr, 0, nullptr, 1, s);
+      if (st) return st;
+      dim3 g((H + 31) / 32, 16);
+      count_launch();
+      launch_pdl(k_mask_colsum<T>, dim3(g), dim3(256), 0, s, d->dh[L], (const T*)d->h[L], tot + L, H, d->gb[L],
+                                         dz_lowp(d, L), d->max_rows[L]);
       // gW_c += h_Lᵀ dlogits (both MN-major, reduction over the roots), forked
       const int split = std::max(1, std::min(16, n_roots / 256));
       st = umma_gemm(d->h[L], H, true, d->dl_lowp, Cp, true, d->gWc, C, H, C, n_roots,

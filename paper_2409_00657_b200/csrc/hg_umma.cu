@@ -40,11 +40,7 @@ __host__ __device__ constexpr int stages_for(int bn) { return bn >= 256 ? HG_UMM
 constexpr int BM_T = 128;
 constexpr int BK_T = 64;  // one 128-byte swizzle row of bf16
 
-// UEPI_MASK_BF16: C = bf16(acc * (mask > 0)) with mask a bf16 [M x N] matrix
-// (ldc pitch), and colsum[n] += sum over the tile's rows of the masked values
-// (the ReLU backward of the layer output + its bias gradient, fused into the
-// GEMM that produces dz).
-enum UEpi { UEPI_STORE_F32 = 0, UEPI_BIAS_RELU_BF16 = 1, UEPI_ATOMIC_F32 = 2, UEPI_MASK_BF16 = 3 };
+enum UEpi { UEPI_STORE_F32 = 0, UEPI_BIAS_RELU_BF16 = 1, UEPI_ATOMIC_F32 = 2 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -177,8 +173,6 @@ struct UmmaArgs {
   int64_t ldc;
   const float* bias;
   int tma_epi;               // 1: epilogue through smem + TMA store/reduce (map_c valid)
-  const __nv_bfloat16* mask; // UEPI_MASK_BF16: ReLU mask source (pitch ldc)
-  float* colsum;             // UEPI_MASK_BF16: column sums (bias gradient)
 };
 
 template <bool A_MN, bool B_MN, int BN_T, int EPI>
@@ -297,7 +291,7 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     // chunk) in the now idle pipeline smem, 128B-swizzled, and one lane hands
     // the box to TMA (store, or f32 add-reduce in L2 for split-K partials).
     // Rows past the device count are written as zeros (inside the capacity).
-    constexpr int EB = (EPI == UEPI_BIAS_RELU_BF16 || EPI == UEPI_MASK_BF16) ? 2 : 4;
+    constexpr int EB = EPI == UEPI_BIAS_RELU_BF16 ? 2 : 4;
     constexpr int CW = 128 / EB;             // columns per 128-byte row
     constexpr int NCH = (BN_T + CW - 1) / CW;
     uint8_t* stage = smem + warp * (NCH * 4096);
@@ -327,34 +321,6 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             pk[j] = *reinterpret_cast<const uint32_t*>(&t);
           }
           v = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        } else if constexpr (EPI == UEPI_MASK_BF16) {
-          // 8 columns of this lane's row: mask by h > 0, then warp column sums
-          uint4 hm = make_uint4(0, 0, 0, 0);
-          if (valid)
-            hm = __ldg(reinterpret_cast<const uint4*>(args.mask + (int64_t)row * args.ldc + n0 + c +
-                                                      u * 8));
-          const uint32_t hw[4] = {hm.x, hm.y, hm.z, hm.w};
-          float xv[8];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float h0 = __uint_as_float(hw[j] << 16), h1 = __uint_as_float(hw[j] & 0xFFFF0000u);
-            xv[2 * j] = valid && h0 > 0.f ? __uint_as_float(rr[u * 8 + 2 * j]) : 0.f;
-            xv[2 * j + 1] = valid && h1 > 0.f ? __uint_as_float(rr[u * 8 + 2 * j + 1]) : 0.f;
-          }
-          uint32_t pk[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const __nv_bfloat162 t = __floats2bfloat162_rn(xv[2 * j], xv[2 * j + 1]);
-            pk[j] = *reinterpret_cast<const uint32_t*>(&t);
-          }
-          v = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            float t = xv[j];
-#pragma unroll
-            for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-            if (lane == 0 && n0 + c + u * 8 + j < args.N) atomicAdd(args.colsum + n0 + c + u * 8 + j, t);
-          }
         } else {
           v = valid ? make_uint4(rr[u * 4], rr[u * 4 + 1], rr[u * 4 + 2], rr[u * 4 + 3])
                     : make_uint4(0, 0, 0, 0);
@@ -509,10 +475,7 @@ static int launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensor
 // Generic entry: shapes are capacities (M/K) when *_dev counts are given.
 int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb, bool b_mn,
               void* C, int64_t ldc, int M, int N, int K, const int32_t* M_dev,
-              const int32_t* K_dev, int epi, const float* bias, int split, cudaStream_t s,
-              const void* mask, float* colsum) {
-  if (epi == UEPI_MASK_BF16 && (!mask || !colsum || N % 8 || ldc % 8))
-    return hg_fail(HG_ECONFIG, "umma mask epilogue needs mask, colsum and N, ldc multiples of 8");
+              const int32_t* K_dev, int epi, const float* bias, int split, cudaStream_t s) {
   if (N <= 0 || (N > 256 && N % 256)) return hg_fail(HG_ECONFIG, "umma N must be <= 256 or a multiple of 256");
   // N tile (grid.y covers the rest): the widest tile that still spreads the
   // problem over about half the SMs -- small-M GEMMs (one micrograph batch of
@@ -541,16 +504,13 @@ int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
   if (st) return st;
   // TMA epilogue when C's rows are 16-byte aligned (else row-per-thread stores)
   CUtensorMap mc;
-  const int eb = (epi == UEPI_BIAS_RELU_BF16 || epi == UEPI_MASK_BF16) ? 2 : 4;
+  const int eb = epi == UEPI_BIAS_RELU_BF16 ? 2 : 4;
   int tma_epi = ((uintptr_t)C % 16 == 0 && (ldc * eb) % 16 == 0) ? 1 : 0;
   if (tma_epi && make_map(&mc, C, (uint64_t)N, (uint64_t)M, ldc, 128 / eb, 32, eb) != HG_OK) {
     tma_epi = 0;
   }
   if (!tma_epi) memset(&mc, 0, sizeof(mc));
-  UmmaArgs a{M, N, K, M_dev, K_dev, C, ldc, bias, tma_epi,
-             reinterpret_cast<const __nv_bfloat16*>(mask), colsum};
-  if (epi == UEPI_MASK_BF16 && !tma_epi)
-    return hg_fail(HG_ECONFIG, "umma mask epilogue needs a 16-byte aligned C");
+  UmmaArgs a{M, N, K, M_dev, K_dev, C, ldc, bias, tma_epi};
 
 #define HG_UMMA_CASE(AM, BMJ, BNV, E)                                                       \
   if (a_mn == AM && b_mn == BMJ && bn == BNV && epi == E)                                   \
@@ -558,7 +518,6 @@ int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
 #define HG_UMMA_N(AM, BMJ, E) \
   HG_UMMA_CASE(AM, BMJ, 64, E) HG_UMMA_CASE(AM, BMJ, 128, E) HG_UMMA_CASE(AM, BMJ, 192, E) HG_UMMA_CASE(AM, BMJ, 256, E)
   HG_UMMA_N(false, false, UEPI_BIAS_RELU_BF16)
-  HG_UMMA_N(false, false, UEPI_MASK_BF16)
   HG_UMMA_N(false, false, UEPI_STORE_F32)
   HG_UMMA_N(true, true, UEPI_ATOMIC_F32)
   HG_UMMA_N(true, true, UEPI_STORE_F32)
@@ -574,8 +533,6 @@ extern "C" int hg_gemm_bf16(const void* A, int64_t lda, int a_mn_major, const vo
                             int b_mn_major, void* C, int64_t ldc, int32_t M, int32_t N, int32_t K,
                             int32_t epi, const float* bias, int32_t split, void* stream) {
   if (M <= 0 || K <= 0) return HG_OK;
-  if (epi == hg::UEPI_MASK_BF16) return hg_fail(HG_ECONFIG, "mask epilogue: internal to the step");
   return hg::umma_gemm(A, lda, a_mn_major != 0, B, ldb, b_mn_major != 0, C, ldc, M, N, K, nullptr,
-                       nullptr, epi, bias, split < 1 ? 1 : split, (cudaStream_t)stream, nullptr,
-                       nullptr);
+                       nullptr, epi, bias, split < 1 ? 1 : split, (cudaStream_t)stream);
 }
