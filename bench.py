@@ -261,8 +261,8 @@ def _run_ours(args, cfg, dev):
                        cfg["classes"], chain(cfg["seed"], 0x07), dev)
     B = cfg["batch"]
     G = int(args.group)
-    if G <= 0:  # auto: the largest group in 4..8 that divides K (no eager remainder), else 8
-        G = next((g for g in range(8, 3, -1) if args.steps % g == 0), 8)
+    if G <= 0:  # auto: the largest group in 4..12 that divides K (no eager remainder), else 8
+        G = next((g for g in range(12, 3, -1) if args.steps % g == 0), 8)
     tr = Trainer(g, table, model, cfg["fanout"], B, cfg["seed"], group=G)
     iters = tr.begin_epoch(0)
     torch.cuda.synchronize()
@@ -679,9 +679,9 @@ def main():
     ap.add_argument("--config", default="papers", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--group", type=int, default=0,
-                    help="iterations per graph replay at N=1 (one build + one gather launch "
-                         "per group; 1 = the per-iteration loop; 0 = auto: the largest of "
-                         "8..4 dividing --steps, else 8)")
+                    help="iterations per graph replay (one build + one gather launch per "
+                         "group; 1 = the per-iteration loop; 0 = auto at N=1: the largest of "
+                         "12..4 dividing --steps, else 8; N>1 defaults to 1)")
     ap.add_argument("--no-model-centric", action="store_true",
                     help="N>1: skip timing the model-centric strategy on the same GPUs")
     ap.add_argument("--cpu-budget", type=float, default=15.0)

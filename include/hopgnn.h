@@ -40,7 +40,7 @@ typedef enum {
 } hg_status;
 
 #define HG_MAX_LAYERS 6
-#define HG_MAX_GROUP 8   /* batches per grouped build / gather launch */
+#define HG_MAX_GROUP 16  /* batches per grouped build / gather launch */
 
 const char* hg_last_error(void);
 int hg_version(void);

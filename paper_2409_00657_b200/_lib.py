@@ -14,7 +14,7 @@ from .errors import ConfigError, InvariantViolation
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libhopgnn.so")
 MAX_LAYERS = 6
-MAX_GROUP = 8   # HG_MAX_GROUP
+MAX_GROUP = 16  # HG_MAX_GROUP
 
 _lib = None
 
