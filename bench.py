@@ -348,23 +348,27 @@ def _run_ours(args, cfg, dev):
         return perm_host[j * B:(j + n) * B]
 
     if G > 1:
-        # train_group: G iterations per call (the loader hands out G batches)
-        Wg = W // G
-        for j in range(Wg):
-            tr.train_group(host_roots(j * G, G), E0 + j * G, host_roots((j + 1) * G, G))
-        tr.last_group_loss()
-        # the remainder steps below go through train_step: warm its state too
-        tr.train_step(host_roots(Wg * G), E0 + Wg * G, host_roots(Wg * G + 1))
-        tr.train_step(host_roots(Wg * G + 1), E0 + Wg * G + 1, None)
+        # train_group: G iterations per call (the loader hands out G batches).
+        # Warm-up order: the public single-step path first (used below only for a
+        # remainder of K mod G steps), then whole groups, so the timed groups
+        # continue where the warm-up groups left the graph loop (no restart)
+        tr.train_step(host_roots(0), E0, host_roots(1))
+        tr.train_step(host_roots(1), E0 + 1, None)
         tr.last_loss()
+        Wg = max(1, W // G)
+        for j in range(Wg):
+            a = 2 + j * G
+            tr.train_group(host_roots(a, G), E0 + a, host_roots(a + G, G))
+        tr.last_group_loss()
         torch.cuda.synchronize()
-        j0 = Wg * G + 2
+        j0 = 2 + Wg * G
         ng = K // G
         e0 = time.perf_counter()
         for j in range(ng):
             a = j0 + j * G
-            nxt = host_roots(a + G, G) if (j + 1 < ng) else None
-            tr.train_group(host_roots(a, G), E0 + a, nxt)
+            # the loader always knows the next group (steady state): its build
+            # overlaps this group's training
+            tr.train_group(host_roots(a, G), E0 + a, host_roots(a + G, G))
         tr.last_group_loss()
         for j in range(j0 + ng * G, j0 + K):  # the remainder, one public step each
             tr.train_step(host_roots(j), E0 + j, host_roots(j + 1) if j + 1 < j0 + K else None)
