@@ -53,13 +53,13 @@ CONFIGS = {
                             "graph (233K V, ~115M E, 602-d feats)",
                    n=233_000, avg_deg=520.0, beta=0.5, p_in=0.9, n_blocks=8, d_cap=1 << 15,
                    arch="gcn", fanout=(10, 10, 10), dim=602, hidden=256, classes=41,
-                   batch=1024, seed=0),
+                   batch=1024, seed=0, group=1),
     # BASELINE.json configs[4]
     "deep": dict(workload="cfg5: GraphSAGE-4 fanout[10,10,5,5] hidden256 bf16 on the "
                           "papers100M shape (deep-hop stress)",
                  n=111_000_000, avg_deg=15.6, beta=0.6, p_in=0.95, n_blocks=8, d_cap=1 << 15,
                  arch="sage-mean", fanout=(10, 10, 5, 5), dim=128, hidden=256, classes=172,
-                 batch=1024, seed=0),
+                 batch=1024, seed=0, group=1),
     "small": dict(workload="smoke: GraphSAGE-2 fanout[10,5] on a 100K-vertex power-law graph",
                   n=100_000, avg_deg=18.5, beta=0.8, p_in=0.9, n_blocks=8, d_cap=1 << 14,
                   arch="sage-mean", fanout=(10, 5), dim=128, hidden=128, classes=16,
@@ -260,8 +260,10 @@ def _run_ours(args, cfg, dev):
     model = init_model(cfg["arch"], cfg["dim"], cfg["hidden"], len(cfg["fanout"]),
                        cfg["classes"], chain(cfg["seed"], 0x07), dev)
     B = cfg["batch"]
-    G = int(args.group)
+    G = int(args.group) or int(cfg.get("group", 0))
     if G <= 0:  # auto: the largest group in 4..12 that divides K (no eager remainder), else 8
+        # (configs whose training chain dwarfs the build -- reddit GCN-3, deep
+        # SAGE-4 -- set group=1: grouping measured slower there, 0.60M vs 0.68M)
         G = next((g for g in range(12, 3, -1) if args.steps % g == 0), 8)
     tr = Trainer(g, table, model, cfg["fanout"], B, cfg["seed"], group=G)
     iters = tr.begin_epoch(0)
