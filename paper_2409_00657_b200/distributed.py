@@ -374,6 +374,9 @@ class PeerFeatures:
 
 # ---------------------------------------------------------------- graph loop
 
+_DIST_PRIO = os.environ.get("HG_DIST_PRIO", "1") != "0"
+
+
 class DistGraphLoop:
     """CUDA-graph replay of the multi-GPU fast path (fused mode, initial trace
     table, NVLink push pre-gather) as a three-stage pipeline over three
@@ -396,8 +399,12 @@ class DistGraphLoop:
         self.tr, self.cap = tr, int(cap)
         dev = tr.device
         self.runners = tr.runners[:3]
-        self.side_build = torch.cuda.Stream(dev)
-        self.side_gather = torch.cuda.Stream(dev)
+        # training and the (cross-GPU latency-bound) pre-gather branch at high
+        # stream priority, the SM-filling build branch at low priority
+        from .engine import _streams
+        self._cap_s, self.side_build = _streams(dev)
+        self.side_gather = (torch.cuda.Stream(dev, priority=-1) if _DIST_PRIO
+                            else torch.cuda.Stream(dev))
         self.pin_loss = [torch.zeros(1, dtype=torch.float32).pin_memory() for _ in range(3)]
         self._dummy = torch.zeros(2, dtype=torch.int64, device=dev)
         m = tr.model
@@ -408,7 +415,7 @@ class DistGraphLoop:
         for x in range(3):
             run, nxt, nxt2 = (self.runners[(x + j) % 3] for j in range(3))
             g = torch.cuda.CUDAGraph()
-            cap_s = torch.cuda.Stream(dev)
+            cap_s = self._cap_s
             cap_s.wait_stream(cur)
             with torch.cuda.graph(g, stream=cap_s):
                 self.side_build.wait_stream(cap_s)
