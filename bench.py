@@ -63,7 +63,7 @@ CONFIGS = {
     "small": dict(workload="smoke: GraphSAGE-2 fanout[10,5] on a 100K-vertex power-law graph",
                   n=100_000, avg_deg=18.5, beta=0.8, p_in=0.9, n_blocks=8, d_cap=1 << 14,
                   arch="sage-mean", fanout=(10, 5), dim=128, hidden=128, classes=16,
-                  batch=1024, seed=0),
+                  batch=1024, seed=0, group=1),
 }
 
 
