@@ -288,6 +288,12 @@ typedef struct {
    * gradient GEMM can run on a forked stream while the next layer's scatter
    * writes its own dz; 0: one shared region (serial backward). */
   int32_t lowp_layered;
+  /* staged mode: row handle of every need[0] entry of the batch (>= 0: row
+   * of the local table, < 0: staging row -1-h), written by hg_resolve_rows
+   * after each pre-gather; the layer-1 gather then indexes it through the
+   * need-index pair lists (one L2-resident lookup per source row instead of
+   * the home / staging-row lookups by vertex id).  NULL = by vertex id. */
+  const int32_t* row_handle;
 } hg_step_desc;
 
 /* Peer memory (one process per GPU): device allocations whose CUDA IPC
@@ -357,6 +363,12 @@ int hg_pregather_push(const int32_t* ids, const int32_t* n_dev, const int32_t* h
                       unsigned long long* uniq_per_home, const int64_t* it_dev,
                       int32_t row_stride, unsigned long long* total_remote, int64_t* seq,
                       int* err, void* stream);
+/* Row handles of a batch's need[0] entries after a pre-gather:
+ * out[i] = home[v] == rank ? local_row[v] : -1 - stage_row[v], v = ids[i],
+ * for i < *n_dev (see hg_step_desc.row_handle). */
+int hg_resolve_rows(const int32_t* ids, const int32_t* n_dev, const int32_t* home, int32_t rank,
+                    const int32_t* local_row, const int32_t* stage_row, int32_t* out,
+                    void* stream);
 /* Parameter-independent prologue of a step: the layer-1 gather + aggregate
  * (sets up agg[1]; run ahead of the previous iteration's training). */
 int hg_step_prologue(const hg_step_desc* d, int32_t n_roots, int32_t backward, void* stream);

@@ -70,7 +70,7 @@ class StepDesc(C.Structure):
                 ("agg1_ready", C.c_int32), ("WcT", C.c_void_p), ("Wcp", C.c_void_p),
                 ("dl_lowp", C.c_void_p), ("root_rows", C.c_int32 * 7),
                 ("lowp_fresh", C.c_int32), ("max_deg", C.c_int32 * 7),
-                ("lowp_layered", C.c_int32)]
+                ("lowp_layered", C.c_int32), ("row_handle", C.c_void_p)]
 
 
 V, I32, I64, U64, SZ = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_size_t
@@ -128,6 +128,7 @@ SIGNATURES = {
     "hg_pregather_push": [V, V, V, I32, I32, V, V, I32, V, V, I32, V, V, I64, I64, I64, I64, I64,
                           V, V, I32, V, V, V, V],
     "hg_step_prologue": [C.POINTER(StepDesc), I32, I32, V],
+    "hg_resolve_rows": [V, V, V, I32, V, V, V, V],
     "hg_step_prologue_group": [C.POINTER(C.POINTER(StepDesc)), I32, I32, V],
     "hg_debug_build_phases": [C.POINTER(C.c_longlong), C.c_int],
 }

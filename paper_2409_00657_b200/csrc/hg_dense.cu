@@ -110,8 +110,13 @@ struct RowSrc {
   const int32_t* stage_row;
   int rank;
   bool by_vid;                // index arrays hold vertex ids (layer 1 vid lists)
+  const int32_t* handle;      // staged mode: need[0] row handles (hg_resolve_rows) or null
   __device__ __forceinline__ const T* row(int i) const {
     if (by_vid) return vrow(i);
+    if (handle) {
+      const int h = handle[i];
+      return h >= 0 ? src + (int64_t)h * ld : stage + (int64_t)(-1 - h) * ld;
+    }
     if (!need_ids0) return src + (int64_t)i * ld;
     return vrow(need_ids0[i]);
   }
@@ -996,11 +1001,14 @@ template <typename T>
 static RowSrc<T> row_src(const hg_step_desc* d, int k) {
   const T* src = k == 1 ? (const T*)d->features : (const T*)d->h[k - 1];
   const int Wd = k == 1 ? d->feat_ld : d->hidden;
-  // layer 1: pair lists by vertex id (one dependent load fewer per source row)
-  const bool vid = k == 1 && d->mg.nbr_vid1 && d->mg.self_vid1;
+  // layer 1: pair lists by vertex id (one dependent load fewer per source row),
+  // or, staged with resolved handles, need-index lists into the handles
+  const bool hnd = k == 1 && d->row_handle && d->stage_base;
+  const bool vid = k == 1 && d->mg.nbr_vid1 && d->mg.self_vid1 && !hnd;
   return RowSrc<T>{src, Wd, k == 1 ? d->mg.need_ids[0] : nullptr, k == 1 ? d->feat_row : nullptr,
                    k == 1 ? (const T* const*)d->feat_peers : nullptr, d->feat_home,
-                   (const T*)d->stage_base, k == 1 ? d->stage_row : nullptr, d->rank, vid};
+                   (const T*)d->stage_base, k == 1 ? d->stage_row : nullptr, d->rank, vid,
+                   hnd ? d->row_handle : nullptr};
 }
 
 // Layer-k gather + aggregate for n steps sharing one row source (k == 1
@@ -1017,7 +1025,8 @@ static void launch_aggregate_n(const hg_step_desc* const* ds, int n, int k, cuda
   int cap = 1;
   for (int b = 0; b < n; ++b) {
     const hg_step_desc* e = ds[b];
-    const bool vid = k == 1 && e->mg.nbr_vid1 && e->mg.self_vid1;
+    const bool vid = k == 1 && e->mg.nbr_vid1 && e->mg.self_vid1 &&
+                     !(e->row_handle && e->stage_base);
     segs.self_pos[b] = vid ? e->mg.self_vid1 : e->mg.self_pos[k];
     segs.nbr_off[b] = e->mg.nbr_off[k];
     segs.nbr_idx[b] = vid ? e->mg.nbr_vid1 : e->mg.nbr_idx[k];
@@ -1344,6 +1353,7 @@ extern "C" int hg_step_prologue_group(const hg_step_desc* const* ds, int32_t n, 
     if (e->features != d->features || e->feat_row != d->feat_row || e->feat_ld != d->feat_ld ||
         e->stage_base != d->stage_base || e->stage_row != d->stage_row ||
         e->feat_peers != d->feat_peers || e->act_dtype != d->act_dtype || e->arch != d->arch ||
+        (n > 1 && e->row_handle && e->stage_base) ||  // handles are per batch: one at a time
         e->in_dim[1] != d->in_dim[1] || e->max_rows[1] != d->max_rows[1])
       return hg_fail(HG_ECONFIG, "grouped prologue: steps must share the feature source");
   }

@@ -397,3 +397,26 @@ extern "C" int hg_remote_clear(const int32_t* ids, const int32_t* n_dev, int32_t
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;
 }
+
+__global__ void k_resolve_rows(const int32_t* __restrict__ ids, const int32_t* __restrict__ n_dev,
+                               const int32_t* __restrict__ home, int rank,
+                               const int32_t* __restrict__ local_row,
+                               const int32_t* __restrict__ stage_row, int32_t* __restrict__ out) {
+  const int n = *n_dev;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int v = ids[i];
+    out[i] = home[v] == rank ? local_row[v] : -1 - stage_row[v];
+  }
+}
+
+extern "C" int hg_resolve_rows(const int32_t* ids, const int32_t* n_dev, const int32_t* home,
+                               int32_t rank, const int32_t* local_row, const int32_t* stage_row,
+                               int32_t* out, void* stream) {
+  if (!ids || !n_dev || !home || !local_row || !stage_row || !out)
+    return hg_fail(HG_ERANGE, "hg_resolve_rows: null argument");
+  count_launch();
+  k_resolve_rows<<<148 * 4, 256, 0, (cudaStream_t)stream>>>(ids, n_dev, home, rank, local_row,
+                                                            stage_row, out);
+  HG_CUDA_TRY(cudaGetLastError());
+  return HG_OK;
+}

@@ -296,6 +296,7 @@ class PeerFeatures:
         d.feat_home = self.home.data_ptr()
         d.stage_base = None
         d.stage_row = None
+        d.row_handle = None
         d.rank = self.rank
 
     def bind_staged(self, runner: CellRunner, stage_cap: int) -> None:
@@ -348,6 +349,15 @@ class PeerFeatures:
         d.stage_base = self.mbox + self.mb_off[4]
         d.stage_row = self.stage_row.data_ptr()
         d.rank = self.rank
+        # per-batch row handles of the need[0] entries, resolved after every
+        # pre-gather (hg_resolve_rows): the layer-1 gather then does one
+        # L2-resident lookup per source row instead of home + staging-row
+        # lookups by vertex id
+        if _ROW_HANDLES:
+            if getattr(runner, "row_handle", None) is None:
+                cap0 = runner.builder.tensors["need_ids"][0].numel()
+                runner.row_handle = torch.zeros(cap0, dtype=torch.int32, device=self.device)
+            d.row_handle = runner.row_handle.data_ptr()
 
     def pregather(self, runner: CellRunner, uniq_row_ptr: int, total_ptr: int, stream,
                   it_dev_ptr=None, empty: bool = False) -> None:
@@ -365,6 +375,10 @@ class PeerFeatures:
                   self.stage_cap, self.boxes.data_ptr(), self.mbox, o[0], o[1], o[2], o[3], o[4],
                   uniq_row_ptr, it_dev_ptr, self.S, total_ptr, self.seq.data_ptr(),
                   self.err.data_ptr(), stream)
+        if runner.desc.row_handle:
+            _lib.call("hg_resolve_rows", t["need_ids"][0].data_ptr(), n_ptr, self.home.data_ptr(),
+                      self.rank, self.local_row.data_ptr(), self.stage_row.data_ptr(),
+                      runner.desc.row_handle, stream)
 
     def close(self):
         for p in self.opened:
@@ -375,6 +389,7 @@ class PeerFeatures:
 # ---------------------------------------------------------------- graph loop
 
 _DIST_PRIO = os.environ.get("HG_DIST_PRIO", "1") != "0"
+_ROW_HANDLES = os.environ.get("HG_ROW_HANDLES", "1") != "0"
 
 
 class DistGraphLoop:
