@@ -397,7 +397,12 @@ def _run_ours(args, cfg, dev):
     tp = os.path.join(HERE, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(args.config if G > 1 else args.config + "_g1")
+            tj = json.load(open(tp))
+            if G > 1 and tj.get(args.config + "_per_iteration"):
+                # ncu DRAM bytes of a grouped launch, per iteration, times this G
+                traffic = int(tj[args.config + "_per_iteration"] * G)
+            else:
+                traffic = tj.get(args.config + "_g1") if G == 1 else None
         except Exception:
             traffic = None
     line = {
