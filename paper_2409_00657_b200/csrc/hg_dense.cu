@@ -800,6 +800,93 @@ k_scatter_root(const float* __restrict__ dagg, int ld, const int32_t* __restrict
   }
 }
 
+// Top-layer special case of k_scatter_root (k == L, need[L] = [root]): every
+// need[L-1] row of root r is either the root's self row or one of its sampled
+// neighbours, each exactly once (layers are deduplicated, no self-loops), so
+// the transpose of the aggregation is a per-row map -- SAGE: self row gets
+// dagg[r, :H] (+ dagg[r, H:] when deg == 0), a neighbour dagg[r, H:] / deg;
+// GCN: every row dagg[r] / (deg + 1) -- with the same arithmetic as the
+// scatter.  One warp per row, 8 columns per lane: two dependent round trips
+// per CTA instead of the per-column loops over rows and pairs.
+template <bool SAGE, typename T>
+__global__ void __launch_bounds__(256)
+k_scatter_top(const float* __restrict__ dagg, int ld, const int32_t* __restrict__ need_off_p,
+              const int32_t* __restrict__ need_off_c, const int32_t* __restrict__ self_pos,
+              const int32_t* __restrict__ nbr_off, int n_roots, int H,
+              const T* __restrict__ h, float* __restrict__ dh_out, bf16* __restrict__ lowp,
+              float* __restrict__ gb, const int32_t* __restrict__ n_rows_dev, int cap_rows) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float red[8][257];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = lane * 8;
+  const bool lane_on = c0 < H;
+  float cs[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) cs[j] = 0.f;
+  for (int r = blockIdx.x; r < n_roots; r += gridDim.x) {
+    const int q0 = need_off_p[r], nq = need_off_p[r + 1] - q0;
+    const int rowL = need_off_c[r];
+    if (nq == 0 || need_off_c[r + 1] - rowL != 1) continue;  // empty (capacity) micrograph
+    const int srow = self_pos[rowL];
+    const int deg = nbr_off[rowL + 1] - nbr_off[rowL];
+    const float* g = dagg + (int64_t)rowL * ld;
+    float gs[8], gn[8];
+    if (lane_on) {
+#pragma unroll
+      for (int j = 0; j < 8; j += 4) {
+        const float4 a = *reinterpret_cast<const float4*>(g + c0 + j);
+        gs[j] = a.x; gs[j + 1] = a.y; gs[j + 2] = a.z; gs[j + 3] = a.w;
+        if constexpr (SAGE) {
+          const float4 b = *reinterpret_cast<const float4*>(g + H + c0 + j);
+          gn[j] = b.x; gn[j + 1] = b.y; gn[j + 2] = b.z; gn[j + 3] = b.w;
+        }
+      }
+    }
+    for (int i = warp; i < nq; i += 8) {
+      const int u = q0 + i;
+      if (!lane_on) continue;
+      float v[8], hv[8];
+      load_vec(h + (int64_t)u * H + c0, hv);
+      if constexpr (sizeof(T) == 4) load_vec(h + (int64_t)u * H + c0 + 4, hv + 4);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float x;
+        if constexpr (SAGE) {
+          x = u == srow ? (deg > 0 ? gs[j] : gs[j] + gn[j]) : (deg > 0 ? gn[j] / (float)deg : 0.f);
+        } else {
+          x = gs[j] / (float)(deg + 1);
+        }
+        v[j] = hv[j] > 0.f ? x : 0.f;
+        cs[j] += v[j];
+      }
+      const int64_t o = (int64_t)u * H + c0;
+      if (dh_out) {
+        *reinterpret_cast<float4*>(dh_out + o) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float4*>(dh_out + o + 4) = make_float4(v[4], v[5], v[6], v[7]);
+      }
+      if (lowp) store_vec(lowp + o, v);
+    }
+  }
+  if (lane_on)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) red[warp][c0 + j] = cs[j];
+  __syncthreads();
+  for (int c = threadIdx.x; c < H; c += blockDim.x) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][c];
+    atomicAdd(gb + c, t);
+  }
+  // the dW GEMM reduces over rows up to the next multiple of 64: zero the padding
+  if (lowp && blockIdx.x == 0) {
+    const int n_rows = *n_rows_dev;
+    const int pad = min(cap_rows, (n_rows + 63) / 64 * 64);
+    for (int64_t i = (int64_t)n_rows * H + threadIdx.x; i < (int64_t)pad * H; i += blockDim.x)
+      lowp[i] = __float2bfloat16_rn(0.f);
+  }
+}
+
 // dz = dh * (h > 0) in place; gb[c] += sum_rows dz[., c]
 // Optional bf16 copy of dz for the tensor-core dW GEMM, whose row reduction
 // reads up to the next multiple of 64 rows: those padding rows are zeroed.
@@ -1102,6 +1189,11 @@ static void scatter_root_attrs() {
   done = true;
 }
 
+static bool getenv_on(const char* name) {  // A/B switches: NAME=1 selects a variant
+  const char* e = getenv(name);
+  return e && e[0] == '1';
+}
+
 // bf16 dz operand of layer k (per-layer region when lowp_layered)
 static inline bf16* dz_lowp(const hg_step_desc* d, int k) {
   int64_t rows = 0;
@@ -1272,6 +1364,21 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
                                                     d->in_dim[k], tot + k, d->max_rows[k],
                                                     d->in_dim[k], nullptr, H, nullptr, nullptr, 0,
                                                     1);
+    }
+    if (k == L && H % 8 == 0 && H <= 256 && !getenv_on("HG_SCATTER_GENERIC")) {
+      // top layer: per-row map, no scatter (k_scatter_top)
+      const bool tc_dx = tc && d->in_dim[k - 1] % 64 == 0 && d->Wb[k - 1];
+      const bool want_f32 = !tc || (k - 1 >= 2 && !tc_dx);
+      const int grid = std::max(1, std::min(n_roots, num_sms() * 8));
+      count_launch();
+      auto kern = sage ? k_scatter_top<true, T> : k_scatter_top<false, T>;
+      launch_pdl(kern, dim3(grid), dim3(256), 0, s, (const float*)d->dagg, d->in_dim[k],
+                 (const int32_t*)d->mg.need_off[k - 1], (const int32_t*)d->mg.need_off[k],
+                 (const int32_t*)d->mg.self_pos[k], (const int32_t*)d->mg.nbr_off[k], n_roots, H,
+                 (const T*)d->h[k - 1], want_f32 ? d->dh[k - 1] : nullptr,
+                 tc ? dz_lowp(d, k - 1) : nullptr, d->gb[k - 1], tot + (k - 1),
+                 d->max_rows[k - 1]);
+      continue;
     }
     const size_t root_smem = (size_t)d->root_rows[k - 1] * H * sizeof(float);
     if (d->root_rows[k - 1] > 0 && root_smem <= kScatterSmem && H <= 512) {
