@@ -482,10 +482,12 @@ def run_distributed(args, cfg):
                        cfg["classes"], chain(cfg["seed"], 0x07), dev)
     B = cfg["batch"]
     mode = args.mode
-    # N > 1: the per-iteration three-stage loop (DistGraphLoop) unless --group is
-    # given: grouping the build measured neutral here (N=2: 11.03M vs 11.07M seeds/s),
-    # the per-iteration pre-gather + staged gather branch is what bounds the step
-    G = max(1, int(args.group))
+    # N > 1: the grouped three-stage loop (DistGroupLoop: one build launch and one
+    # deduplicated NVLink push per group, per-iteration ledger rows); same auto
+    # rule as N = 1 (N=2: 12.05M at G=1, 12.27M at G=5, 13.29M at G=10)
+    G = int(args.group) or int(cfg.get("group", 0))
+    if G <= 0:
+        G = next((g_ for g_ in range(12, 3, -1) if args.steps % g_ == 0), 8)
     tr = MicrographTrainer(g, part, model, cfg["fanout"], B, cfg["seed"], mode=mode,
                            pregather=args.pregather, graph_group=G)
     iters = tr.begin_epoch(0)

@@ -363,6 +363,25 @@ int hg_pregather_push(const int32_t* ids, const int32_t* n_dev, const int32_t* h
                       unsigned long long* uniq_per_home, const int64_t* it_dev,
                       int32_t row_stride, unsigned long long* total_remote, int64_t* seq,
                       int* err, void* stream);
+/* Push pre-gather of several batches at once (a run-ahead group): the
+ * remote vertices of all n_seg id lists (ids[g][0..*n_dev[g]), host arrays of
+ * device pointers) are deduplicated together and fetched with ONE
+ * request/completion handshake; no ledger counting here (per-iteration
+ * accounting: hg_remote_account_at).  Same mailbox layout as hg_pregather_push;
+ * stage_cap must hold the group's distinct remote rows. */
+int hg_pregather_push_multi(const int32_t* const* ids, const int32_t* const* n_dev, int32_t n_seg,
+                            const int32_t* home, int32_t rank, int32_t n_ranks,
+                            const int32_t* local_row, const void* shard, int32_t row_bytes,
+                            int32_t* stamp, int32_t* stage_row, int32_t stage_cap,
+                            const void* boxes, void* own_box, int64_t o_flags, int64_t o_done,
+                            int64_t o_count, int64_t o_list, int64_t o_staging, int64_t* seq,
+                            int* err, void* stream);
+/* hg_remote_account charged to row (*it_dev + ahead) of an [iters x row_stride]
+ * table (the reference's per-iteration pre-gather ledger, featstore.py:226-279). */
+int hg_remote_account_at(const int32_t* ids, const int32_t* n_dev, const int32_t* home,
+                         int32_t rank, uint32_t* bitmap, unsigned long long* uniq_table,
+                         const int64_t* it_dev, int32_t ahead, int32_t row_stride,
+                         unsigned long long* total_remote, void* stream);
 /* Row handles of a batch's need[0] entries after a pre-gather:
  * out[i] = home[v] == rank ? local_row[v] : -1 - stage_row[v], v = ids[i],
  * for i < *n_dev (see hg_step_desc.row_handle). */

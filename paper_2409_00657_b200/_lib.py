@@ -129,6 +129,9 @@ SIGNATURES = {
                           V, V, I32, V, V, V, V],
     "hg_step_prologue": [C.POINTER(StepDesc), I32, I32, V],
     "hg_resolve_rows": [V, V, V, I32, V, V, V, V],
+    "hg_pregather_push_multi": [V, V, I32, V, I32, I32, V, V, I32, V, V, I32, V, V, I64, I64,
+                                I64, I64, I64, V, V, V],
+    "hg_remote_account_at": [V, V, V, I32, V, V, V, I32, I32, V, V],
     "hg_step_prologue_group": [C.POINTER(C.POINTER(StepDesc)), I32, I32, V],
     "hg_debug_build_phases": [C.POINTER(C.c_longlong), C.c_int],
 }

@@ -34,6 +34,31 @@ __global__ void k_remote_account(const int32_t* __restrict__ ids, const int32_t*
   if ((threadIdx.x & 31) == 0 && mine) atomicAdd(total_remote, mine);
 }
 
+// The same, charged to row (*it_dev + ahead) of an [iters x row_stride] table
+// (fixed arguments for graph capture).
+__global__ void k_remote_account_at(const int32_t* __restrict__ ids,
+                                    const int32_t* __restrict__ n_dev,
+                                    const int32_t* __restrict__ home, int rank,
+                                    uint32_t* __restrict__ bitmap,
+                                    unsigned long long* __restrict__ table,
+                                    const int64_t* __restrict__ it_dev, int ahead, int row_stride,
+                                    unsigned long long* __restrict__ total_remote) {
+  const int n = *n_dev;
+  unsigned long long* uniq_per_home = table + (*it_dev + ahead) * row_stride;
+  unsigned long long mine = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int v = ids[i];
+    const int h = home[v];
+    if (h == rank) continue;
+    ++mine;
+    const uint32_t bit = 1u << (v & 31);
+    const uint32_t old = atomicOr(bitmap + (v >> 5), bit);
+    if (!(old & bit)) atomicAdd(uniq_per_home + h, 1ull);
+  }
+  for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if (total_remote && (threadIdx.x & 31) == 0 && mine) atomicAdd(total_remote, mine);
+}
+
 __global__ void k_remote_clear(const int32_t* __restrict__ ids, const int32_t* __restrict__ n_dev,
                                int n_host, uint32_t* __restrict__ bitmap) {
   const int n = n_dev ? *n_dev : n_host;
@@ -304,6 +329,55 @@ extern "C" int hg_pregather_push(const int32_t* ids, const int32_t* n_dev, const
   k_pg_signal<<<1, 32, 0, s>>>(bx, rank, n_ranks, m, seq, o_done);           // my rows written
   k_pg_wait<<<1, 32, 0, s>>>(bx, rank, n_ranks, m, seq, o_done, err);        // all rows here
   prof_end(PROF_PG_COPY, s);
+  HG_CUDA_TRY(cudaGetLastError());
+  return HG_OK;
+}
+
+extern "C" int hg_pregather_push_multi(const int32_t* const* ids, const int32_t* const* n_dev,
+                                       int32_t n_seg, const int32_t* home, int32_t rank,
+                                       int32_t n_ranks, const int32_t* local_row,
+                                       const void* shard, int32_t row_bytes, int32_t* stamp,
+                                       int32_t* stage_row, int32_t stage_cap, const void* boxes,
+                                       void* own_box, int64_t o_flags, int64_t o_done,
+                                       int64_t o_count, int64_t o_list, int64_t o_staging,
+                                       int64_t* seq, int* err, void* stream) {
+  if (row_bytes % 16) return hg_fail(HG_ECONFIG, "row bytes must be a multiple of 16");
+  if (n_seg < 1) return hg_fail(HG_ERANGE, "no segments");
+  cudaStream_t s = (cudaStream_t)stream;
+  const Mailbox m{o_flags, o_done, o_count, o_list, o_staging};
+  const uint64_t* bx = (const uint64_t*)boxes;
+  uint8_t* own = (uint8_t*)own_box;
+  int32_t* count = (int32_t*)(own + o_count);
+  HG_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t), s));
+  count_launch(5 + n_seg);
+  prof_begin(PROF_PG_MARK, s);
+  // one stamp tag for the whole call: a vertex wanted by several segments is
+  // requested once
+  for (int g = 0; g < n_seg; ++g)
+    k_stage_mark_stamp<<<148 * 2, 256, 0, s>>>(ids[g], n_dev[g], home, rank, n_ranks, stamp, seq,
+                                               (int32_t*)(own + o_list), stage_row, count,
+                                               stage_cap, nullptr, nullptr, err, nullptr, 0);
+  prof_end(PROF_PG_MARK, s);
+  prof_begin(PROF_PG_COPY, s);
+  k_pg_signal<<<1, 32, 0, s>>>(bx, rank, n_ranks, m, seq, o_flags);
+  k_pg_wait<<<1, 32, 0, s>>>(bx, rank, n_ranks, m, seq, o_flags, err);
+  k_pg_serve<<<148 * 2, 256, 0, s>>>(bx, rank, n_ranks, m, seq, home, local_row,
+                                     (const uint8_t*)shard, row_bytes, stage_cap, err);
+  k_pg_signal<<<1, 32, 0, s>>>(bx, rank, n_ranks, m, seq, o_done);
+  k_pg_wait<<<1, 32, 0, s>>>(bx, rank, n_ranks, m, seq, o_done, err);
+  prof_end(PROF_PG_COPY, s);
+  HG_CUDA_TRY(cudaGetLastError());
+  return HG_OK;
+}
+
+extern "C" int hg_remote_account_at(const int32_t* ids, const int32_t* n_dev, const int32_t* home,
+                                    int32_t rank, uint32_t* bitmap,
+                                    unsigned long long* uniq_table, const int64_t* it_dev,
+                                    int32_t ahead, int32_t row_stride,
+                                    unsigned long long* total_remote, void* stream) {
+  count_launch();
+  k_remote_account_at<<<148 * 2, 256, 0, (cudaStream_t)stream>>>(
+      ids, n_dev, home, rank, bitmap, uniq_table, it_dev, ahead, row_stride, total_remote);
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;
 }

@@ -380,6 +380,32 @@ class PeerFeatures:
                       self.rank, self.local_row.data_ptr(), self.stage_row.data_ptr(),
                       runner.desc.row_handle, stream)
 
+    def pregather_group(self, runners, uniq_table_ptr: int, total_ptr: int, stream,
+                        it_dev_ptr: int) -> None:
+        """Push pre-gather of a run-ahead group (DistGroupLoop): the reference
+        ledger is charged per iteration (row *it_dev + 1 + j for runner j, own
+        dedup per iteration, featstore.py:226-279), while the rows move in ONE
+        deduplicated push with one request/completion handshake; then every
+        runner's row handles are resolved against the shared staging map."""
+        G = len(runners)
+        o = self.mb_off
+        ids = (C.c_void_p * G)(*[r.builder.tensors["need_ids"][0].data_ptr() for r in runners])
+        ns = (C.c_void_p * G)(*[r.builder.tensors["totals"].data_ptr() for r in runners])
+        for j in range(G):
+            _lib.call("hg_remote_account_at", ids[j], ns[j], self.home.data_ptr(), self.rank,
+                      self.bitmap.data_ptr(), uniq_table_ptr, it_dev_ptr, 1 + j, self.S,
+                      total_ptr, stream)
+            _lib.call("hg_remote_clear", ids[j], ns[j], 0, self.bitmap.data_ptr(), stream)
+        _lib.call("hg_pregather_push_multi", ids, ns, G, self.home.data_ptr(), self.rank, self.S,
+                  self.local_row.data_ptr(), self.ptr, self.row_bytes, self.stamp.data_ptr(),
+                  self.stage_row.data_ptr(), self.stage_cap, self.boxes.data_ptr(), self.mbox,
+                  o[0], o[1], o[2], o[3], o[4], self.seq.data_ptr(), self.err.data_ptr(), stream)
+        for r, ip, np_ in zip(runners, ids, ns):
+            if r.desc.row_handle:
+                _lib.call("hg_resolve_rows", ip, np_, self.home.data_ptr(), self.rank,
+                          self.local_row.data_ptr(), self.stage_row.data_ptr(),
+                          r.desc.row_handle, stream)
+
     def close(self):
         for p in self.opened:
             _lib.call("hg_ipc_close", p)
@@ -390,6 +416,8 @@ class PeerFeatures:
 
 _DIST_PRIO = os.environ.get("HG_DIST_PRIO", "1") != "0"
 _ROW_HANDLES = os.environ.get("HG_ROW_HANDLES", "1") != "0"
+# DistGroupLoop: one deduplicated push per group (per-iteration ledger rows)
+_GROUP_PUSH = os.environ.get("HG_GROUP_PUSH", "1") != "0"
 
 
 class DistGraphLoop:
@@ -563,9 +591,20 @@ class DistGroupLoop:
                  ctas_per_sm=self.ctas_per_sm if ctas_per_sm is None else ctas_per_sm)
 
     def gather_ops(self, k: int, s) -> None:
-        """Per iteration of set k: advance the gather cursor, pre-gather (ledger
-        row = that iteration), layer-1 gather."""
+        """Pre-gather set k's G iterations in one push (ledger rows per
+        iteration, cursor+1 .. cursor+G), advance the gather cursor by G, and
+        run each iteration's layer-1 gather from the shared staging."""
         tr = self.tr
+        if _GROUP_PUSH:
+            tr.feats.pregather_group(self.sets[k], tr._acct_rows.data_ptr(),
+                                     tr._acct_total.data_ptr(), s, tr._g_pg.data_ptr())
+            _lib.call("hg_iter_stage_ranged", tr._g_roots.data_ptr(), tr._g_ranges.data_ptr(),
+                      tr._g_states.data_ptr(), tr.iters, tr._g_pg.data_ptr(), 0, self.G, self.G,
+                      self._dummy.data_ptr(), self._dummy.data_ptr(),
+                      self._dummy.data_ptr() + 8, s)
+            for r in self.sets[k]:
+                _lib.call("hg_step_prologue", C.byref(r.desc), self.cap, 1, s)
+            return
         for r in self.sets[k]:
             _lib.call("hg_iter_stage_ranged", tr._g_roots.data_ptr(), tr._g_ranges.data_ptr(),
                       tr._g_states.data_ptr(), tr.iters, tr._g_pg.data_ptr(), 0, 1, 1,
@@ -993,8 +1032,9 @@ class MicrographTrainer:
                                                self.fanout, self.runners[0].max_roots,
                                                self.labels))
                 lay = self.runners[0].builder.layout
-                self._stage_cap = min(self.runners[0].max_roots * lay.cap_need[0],
-                                      self.part.n_vertices)
+                # a group push stages the distinct remote rows of graph_group iterations
+                self._stage_cap = min(self.runners[0].max_roots * lay.cap_need[0]
+                                      * self.graph_group, self.part.n_vertices)
                 self._ra = RunAhead(self.runners[:2], self.device)
             r = self._ra.acquire(it, self._fast_build(it))
         n = r.n_roots
