@@ -663,6 +663,14 @@ def run_distributed(args, cfg):
                 "ratio_model_centric_over_micrograph_fused": round(
                     mc_iter / max(by_cat["feature"] / K + 2.0 * (S - 1) * pb, 1), 3),
                 "actual_nvlink_bytes_per_iter": round(float(traffic[0].item()) / K, 1),
+                # physical bytes on both sides: bf16 feature rows (+ the same
+                # gradient all-reduce), upper bound for the micrograph side (rows
+                # deduplicated per iteration; the group push dedups across the group)
+                "model_centric_actual_per_iter": round(
+                    mc_feat_iter / 2 + float(traffic[3].item()) / K, 1),
+                "ratio_model_centric_over_micrograph_actual": round(
+                    (mc_feat_iter / 2 + float(traffic[3].item()) / K)
+                    / max(float(traffic[0].item()) / K, 1), 3),
                 "epoch_reference_accounting": round(per_iter_ref * iters, 1),
                 "epoch_model_centric": round(mc_iter * iters, 1),
                 "iterations_per_epoch": iters},
