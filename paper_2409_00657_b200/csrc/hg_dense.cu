@@ -141,6 +141,7 @@ struct AggSegs {
   const int32_t* nbr_idx[HG_MAX_GROUP];
   const int32_t* n_rows[HG_MAX_GROUP];
   T* out[HG_MAX_GROUP];
+  const int32_t* handle[HG_MAX_GROUP];  // staged mode: per-batch need[0] row handles
 };
 
 #ifndef HG_AGG_U
@@ -160,9 +161,11 @@ struct AggSegs {
 // ~100K-row gather of a batch keeps >100 KB in flight per SM.
 template <typename T, bool SAGE>
 __global__ void __launch_bounds__(256, HG_AGG_MINB)
-k_aggregate(RowSrc<T> rs, AggSegs<T> segs, int W, int out_ld, int pad_cap) {
+k_aggregate(RowSrc<T> rs_in, AggSegs<T> segs, int W, int out_ld, int pad_cap) {
   pdl_trigger();
   pdl_wait();
+  RowSrc<T> rs = rs_in;
+  if (segs.handle[blockIdx.y]) rs.handle = segs.handle[blockIdx.y];  // this batch's handles
   const int32_t* __restrict__ self_pos = segs.self_pos[blockIdx.y];
   const int32_t* __restrict__ nbr_off = segs.nbr_off[blockIdx.y];
   const int32_t* __restrict__ nbr_idx = segs.nbr_idx[blockIdx.y];
@@ -1112,8 +1115,9 @@ static void launch_aggregate_n(const hg_step_desc* const* ds, int n, int k, cuda
   int cap = 1;
   for (int b = 0; b < n; ++b) {
     const hg_step_desc* e = ds[b];
-    const bool vid = k == 1 && e->mg.nbr_vid1 && e->mg.self_vid1 &&
-                     !(e->row_handle && e->stage_base);
+    const bool hnd = k == 1 && e->row_handle && e->stage_base;
+    const bool vid = k == 1 && e->mg.nbr_vid1 && e->mg.self_vid1 && !hnd;
+    segs.handle[b] = hnd ? e->row_handle : nullptr;
     segs.self_pos[b] = vid ? e->mg.self_vid1 : e->mg.self_pos[k];
     segs.nbr_off[b] = e->mg.nbr_off[k];
     segs.nbr_idx[b] = vid ? e->mg.nbr_vid1 : e->mg.nbr_idx[k];
@@ -1130,7 +1134,7 @@ static void launch_aggregate_n(const hg_step_desc* const* ds, int n, int k, cuda
   }();
   const int max_deg = d->max_deg[k];
   const int rowbytes = Wd * (int)sizeof(T);
-  if (tma_on && k == 1 && max_deg > 0 && rowbytes % 16 == 0) {
+  if (tma_on && k == 1 && max_deg > 0 && rowbytes % 16 == 0 && (n == 1 || !d->row_handle)) {
     constexpr int kSmemBudget = 200 * 1024;  // kTmaStages stages of TR rows x (max_deg+1) slots
     const int per_row = (max_deg + 1) * rowbytes;
     const int TR = std::min(32, kSmemBudget / kTmaStages / per_row);
@@ -1460,7 +1464,7 @@ extern "C" int hg_step_prologue_group(const hg_step_desc* const* ds, int32_t n, 
     if (e->features != d->features || e->feat_row != d->feat_row || e->feat_ld != d->feat_ld ||
         e->stage_base != d->stage_base || e->stage_row != d->stage_row ||
         e->feat_peers != d->feat_peers || e->act_dtype != d->act_dtype || e->arch != d->arch ||
-        (n > 1 && e->row_handle && e->stage_base) ||  // handles are per batch: one at a time
+        (e->row_handle && e->stage_base) != (d->row_handle && d->stage_base) ||
         e->in_dim[1] != d->in_dim[1] || e->max_rows[1] != d->max_rows[1])
       return hg_fail(HG_ECONFIG, "grouped prologue: steps must share the feature source");
   }

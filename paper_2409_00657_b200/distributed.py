@@ -531,6 +531,8 @@ class DistGroupLoop:
                                 tr.runners[0].max_roots, tr.labels)
         self.sets = [[mk() for _ in range(G)] for _ in range(3)]
         self.gb = [GroupBuilder([r.builder for r in st], per_batch=self.cap) for st in self.sets]
+        self.descp = [(C.POINTER(_lib.StepDesc) * G)(*[C.pointer(r.desc) for r in st])
+                      for st in self.sets]
         for st, gb in zip(self.sets, self.gb):
             for j, r in enumerate(st):
                 tr.feats.bind_staged(r, tr._stage_cap)
@@ -602,8 +604,8 @@ class DistGroupLoop:
                       tr._g_states.data_ptr(), tr.iters, tr._g_pg.data_ptr(), 0, self.G, self.G,
                       self._dummy.data_ptr(), self._dummy.data_ptr(),
                       self._dummy.data_ptr() + 8, s)
-            for r in self.sets[k]:
-                _lib.call("hg_step_prologue", C.byref(r.desc), self.cap, 1, s)
+            # the group's layer-1 gathers in ONE launch (per-batch row handles)
+            _lib.call("hg_step_prologue_group", self.descp[k], self.G, 1, s)
             return
         for r in self.sets[k]:
             _lib.call("hg_iter_stage_ranged", tr._g_roots.data_ptr(), tr._g_ranges.data_ptr(),
