@@ -418,6 +418,7 @@ _DIST_PRIO = os.environ.get("HG_DIST_PRIO", "1") != "0"
 _ROW_HANDLES = os.environ.get("HG_ROW_HANDLES", "1") != "0"
 # DistGroupLoop: one deduplicated push per group (per-iteration ledger rows)
 _GROUP_PUSH = os.environ.get("HG_GROUP_PUSH", "1") != "0"
+_GROUP_GATHER = os.environ.get("HG_GROUP_GATHER", "1") != "0"
 
 
 class DistGraphLoop:
@@ -604,8 +605,11 @@ class DistGroupLoop:
                       tr._g_states.data_ptr(), tr.iters, tr._g_pg.data_ptr(), 0, self.G, self.G,
                       self._dummy.data_ptr(), self._dummy.data_ptr(),
                       self._dummy.data_ptr() + 8, s)
-            # the group's layer-1 gathers in ONE launch (per-batch row handles)
-            _lib.call("hg_step_prologue_group", self.descp[k], self.G, 1, s)
+            if _GROUP_GATHER:  # the group's layer-1 gathers in ONE launch (per-batch handles)
+                _lib.call("hg_step_prologue_group", self.descp[k], self.G, 1, s)
+            else:
+                for r in self.sets[k]:
+                    _lib.call("hg_step_prologue", C.byref(r.desc), self.cap, 1, s)
             return
         for r in self.sets[k]:
             _lib.call("hg_iter_stage_ranged", tr._g_roots.data_ptr(), tr._g_ranges.data_ptr(),
