@@ -1,6 +1,6 @@
 """Host-side logic of the multi-GPU path on CPU: trace table / merge replay
 against the oracle, reference ledger accounting, and the pre-gather
-all-to-all exchange run for real with world_size 2 and 3 over gloo."""
+all-to-all exchange run for real with world_size 2, 3 and 8 (the driver's largest N) over gloo."""
 import os
 import tempfile
 
@@ -69,7 +69,7 @@ def test_plan_pregather_matches_oracle():
     assert [(h, ids.tolist()) for h, ids in got.by_source] == [(h, ids.tolist()) for h, ids in want]
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_pregather_all_to_all_gloo(world):
     import dist_helpers
     d = tempfile.mkdtemp()
