@@ -1281,7 +1281,8 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     if (k == 1) prof_end(PROF_GEMM1, s);
   }
   // classifier head (model.py:246, 253-265)
-  const bool tc_head = tc && C <= 256 && d->WcT && d->Wcp && d->dl_lowp;
+  const bool tc_head = tc && C <= 256 && d->WcT && d->Wcp && d->dl_lowp &&
+                       !getenv_on("HG_SIMT_HEAD");  // A/B: the fused one-kernel head
   const int Cp = (C + 63) / 64 * 64;
   if (tc_head) {
     // logits = h_L @ W_c on tcgen05 (B = W_cᵀ bf16, K-major); softmax-CE writes
