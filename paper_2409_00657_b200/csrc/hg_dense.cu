@@ -1062,6 +1062,9 @@ __global__ void k_sgd(float* __restrict__ p, float* __restrict__ g, bf16* __rest
 int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb, bool b_mn,
               void* C, int64_t ldc, int M, int N, int K, const int32_t* M_dev,
               const int32_t* K_dev, int epi, const float* bias, int split, cudaStream_t s);
+int umma_head_ce(const void* A, int64_t lda, const void* B, int64_t ldb, float* logits, int C,
+                 int n_cap, int K, const int32_t* M_dev, const int64_t* roots, uint64_t label_state,
+                 float* loss, __nv_bfloat16* dl_lowp, int ldp, cudaStream_t s);
 
 static int g_num_sms = 0;
 static int num_sms() {
@@ -1294,13 +1297,20 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
       k_pad_bf16<<<64, 256, 0, s>>>(d->Wc, H, C, (bf16*)d->Wcp, Cp);
     }
     // root rows: n_roots is the capacity, the device count N_L the actual roots
-    int st = umma_gemm(d->h[L], H, false, d->WcT, H, false, d->logits, C, n_roots, C, H,
+    int st;
+    if (C <= 192 && getenv_on("HG_FUSED_HEAD")) {  // A/B: softmax-CE in the GEMM epilogue
+      st = umma_head_ce(d->h[L], H, d->WcT, H, d->logits, C, n_roots, H, tot + L, d->roots,
+                        d->label_state, d->loss, (bf16*)d->dl_lowp, Cp, s);
+      if (st) return st;
+    } else {
+    st = umma_gemm(d->h[L], H, false, d->WcT, H, false, d->logits, C, n_roots, C, H,
                        tot + L, nullptr, 0, nullptr, 1, s);
     if (st) return st;
     count_launch();
     launch_pdl(k_softmax_ce, dim3((n_roots + 7) / 8), dim3(256), 0, s, d->logits, C, d->roots, n_roots, tot + L,
                                                    d->label_state, d->loss,
                                                    (bf16*)d->dl_lowp, Cp);
+    }
     if (backward) {
       // dz_L = (dlogits @ W_cᵀ) * (h_L > 0); gb_L; bf16 dz_L for the dW GEMM
       st = umma_gemm(d->dl_lowp, Cp, false, d->Wcp, Cp, false, d->dh[L], H, n_roots, H, Cp,

@@ -40,7 +40,7 @@ __host__ __device__ constexpr int stages_for(int bn) { return bn >= 256 ? HG_UMM
 constexpr int BM_T = 128;
 constexpr int BK_T = 64;  // one 128-byte swizzle row of bf16
 
-enum UEpi { UEPI_STORE_F32 = 0, UEPI_BIAS_RELU_BF16 = 1, UEPI_ATOMIC_F32 = 2 };
+enum UEpi { UEPI_STORE_F32 = 0, UEPI_BIAS_RELU_BF16 = 1, UEPI_ATOMIC_F32 = 2, UEPI_SOFTMAX_CE = 3 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -173,7 +173,24 @@ struct UmmaArgs {
   int64_t ldc;
   const float* bias;
   int tma_epi;               // 1: epilogue through smem + TMA store/reduce (map_c valid)
+  // UEPI_SOFTMAX_CE (classifier head, model.py:253-265): one N tile holds a
+  // root's whole logit row, so the epilogue thread of that row does the
+  // softmax-CE: loss, dlogits (f32 in C) and the bf16 padded copy.
+  const int64_t* roots;
+  uint64_t label_state;
+  float* loss;
+  __nv_bfloat16* dl_lowp;
+  int ldp;                   // dl_lowp row pitch (classes rounded up to 64)
+  int n_cap;                 // capacity rows: [M_dev, n_cap) get zeros
 };
+
+// Rows [r0, r1) of the head outputs past the device root count: no loss, no gradient.
+__device__ __forceinline__ void head_zero_row(const UmmaArgs& a, int row) {
+  float* x = reinterpret_cast<float*>(a.C) + (int64_t)row * a.ldc;
+  for (int c = 0; c < a.N; ++c) x[c] = 0.f;
+  for (int c = 0; c < a.ldp; ++c) a.dl_lowp[(int64_t)row * a.ldp + c] = __float2bfloat16_rn(0.f);
+  a.loss[row] = 0.f;
+}
 
 template <bool A_MN, bool B_MN, int BN_T, int EPI>
 __global__ void __launch_bounds__(128, 1)
@@ -198,7 +215,12 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   pdl_wait();
   const int M = args.M_dev ? *args.M_dev : args.M;
   const int K = args.K_dev ? *args.K_dev : args.K;
-  if (m0 >= M) return;  // whole CTA exits together (before any barrier)
+  if (m0 >= M) {  // whole CTA exits together (before any barrier)
+    if constexpr (EPI == UEPI_SOFTMAX_CE)
+      for (int row = m0 + threadIdx.x; row < min(m0 + BM_T, args.n_cap); row += blockDim.x)
+        head_zero_row(args, row);
+    return;
+  }
   // K range of this split, in 64-wide blocks
   const int kblocks = (K + BK_T - 1) / BK_T;
   const int per = (kblocks + gridDim.z - 1) / gridDim.z;
@@ -285,7 +307,49 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   if (false) {
 #else
   const bool valid = row < M;
-  if (args.tma_epi) {
+  if constexpr (EPI == UEPI_SOFTMAX_CE) {
+    // one TMEM sweep (4 loads in flight, warp-uniform) copies each thread's
+    // logit row into the idle pipeline smem (odd pitch: bank-conflict free);
+    // max / sum-exp / gradient then run from smem, and the warp stores its
+    // 32 rows coalesced
+    const uint32_t tb = tmem + ((uint32_t)(warp * 32) << 16);
+    const int C = args.N;
+    const int P = C | 1;
+    float* stg = reinterpret_cast<float*>(smem) + warp * 32 * P;
+    float* mine = stg + lane * P;
+#pragma unroll 1
+    for (int cb = 0; cb < C; cb += 64) {
+      uint32_t r[64];
+#pragma unroll
+      for (int q = 0; q < 64; q += 16) tmem_ld16_issue(tb + cb + q, r + q);
+#pragma unroll
+      for (int q = 0; q < 64; q += 16) tmem_wait16(r + q);
+#pragma unroll
+      for (int j = 0; j < 64; ++j)
+        if (cb + j < C) mine[cb + j] = __uint_as_float(r[j]);
+    }
+    const int label = valid ? (int)(mix64(args.label_state ^ (uint64_t)args.roots[row]) % (uint64_t)C) : 0;
+    float mx = -INFINITY, sum = 0.f;
+    for (int c = 0; c < C; ++c) mx = fmaxf(mx, mine[c]);
+    const float xl = mine[label];
+    for (int c = 0; c < C; ++c) sum += expf(mine[c] - mx);
+    const float inv = 1.0f / sum;
+    for (int c = 0; c < C; ++c)
+      mine[c] = valid ? expf(mine[c] - mx) * inv - (c == label ? 1.f : 0.f) : 0.f;
+    if (valid) args.loss[row] = logf(sum) - (xl - mx);
+    else if (row < args.n_cap) args.loss[row] = 0.f;
+    __syncwarp();
+    const int r0 = m0 + warp * 32;
+    for (int i = 0; i < 32 && r0 + i < args.n_cap; ++i) {
+      float* xo = reinterpret_cast<float*>(args.C) + (int64_t)(r0 + i) * args.ldc;
+      __nv_bfloat16* lo = args.dl_lowp + (int64_t)(r0 + i) * args.ldp;
+      for (int c = lane; c < args.ldp; c += 32) {
+        const float g = c < C ? stg[i * P + c] : 0.f;
+        if (c < C) xo[c] = g;
+        lo[c] = __float2bfloat16_rn(g);
+      }
+    }
+  } else if (args.tma_epi) {
 #endif
     // Coalesced epilogue: each warp stages its 32 rows x (128-byte column
     // chunk) in the now idle pipeline smem, 128B-swizzled, and one lane hands
@@ -525,6 +589,25 @@ int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
 #undef HG_UMMA_CASE
   return hg_fail(HG_ECONFIG, "unsupported umma variant (a_mn=%d b_mn=%d N=%d epi=%d)", (int)a_mn,
                  (int)b_mn, N, epi);
+}
+
+// Classifier head with the softmax-CE fused into the epilogue: logits
+// [n_cap x C] = h_L [n_cap x K] @ W_c (B = W_cᵀ bf16, K-major), C <= 192 so
+// one N tile covers every class.  Replaces umma_gemm + k_softmax_ce.
+int umma_head_ce(const void* A, int64_t lda, const void* B, int64_t ldb, float* logits, int C,
+                 int n_cap, int K, const int32_t* M_dev, const int64_t* roots, uint64_t label_state,
+                 float* loss, __nv_bfloat16* dl_lowp, int ldp, cudaStream_t s) {
+  if (C <= 0 || C > 192) return hg_fail(HG_ECONFIG, "fused head needs 1 <= classes <= 192");
+  if (lda % 8 || ldb % 8) return hg_fail(HG_ECONFIG, "umma leading dims must be multiples of 8");
+  CUtensorMap ma, mb, mc;
+  int st = make_map(&ma, A, (uint64_t)K, (uint64_t)n_cap, lda, BK_T, BM_T);
+  if (st) return st;
+  st = make_map(&mb, B, (uint64_t)K, (uint64_t)C, ldb, BK_T, 192u);
+  if (st) return st;
+  memset(&mc, 0, sizeof(mc));
+  UmmaArgs a{n_cap, C, K, M_dev, nullptr, logits, C, nullptr, 0,
+             roots, label_state, loss, dl_lowp, ldp, n_cap};
+  return launch_t<false, false, 192, UEPI_SOFTMAX_CE>(ma, mb, mc, a, 1, s);
 }
 
 }  // namespace hg

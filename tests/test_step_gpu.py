@@ -174,6 +174,16 @@ def test_step_matches_oracle(world, case, dtype):
     assert float(model.grad.abs().max()) == 0.0
 
 
+@pytest.mark.parametrize("case", [c for c in CASES if c[3] % 64 == 0],
+                         ids=lambda c: f"{c[0]}-{'x'.join(map(str, c[1]))}-D{c[2]}-H{c[3]}")
+def test_fused_head_matches_oracle(world, case, monkeypatch):
+    """HG_FUSED_HEAD=1: softmax-CE in the tcgen05 head GEMM's epilogue
+    (umma_head_ce) instead of the separate k_softmax_ce; 96 roots in a
+    128-root capacity also exercise the zeroed capacity rows."""
+    monkeypatch.setenv("HG_FUSED_HEAD", "1")
+    test_step_matches_oracle(world, case, torch.bfloat16)
+
+
 def test_forward_only_and_repeat_determinism(world):
     from paper_2409_00657_b200.featstore import FeatureTable
     from paper_2409_00657_b200.model import LabelOracle, init_model
