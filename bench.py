@@ -126,7 +126,20 @@ class Clocks:
 
 
 def cpu_baseline(cfg, budget_s=15.0):
-    """Single-core oracle port on a bounded sample (rank 0, N=1)."""
+    """The reference itself (gnnsim from baseline/_ref, its own sample_micrograph /
+    forward / loss_and_backward / sync_and_update) on ONE core, on a bounded
+    sample of the workload (rank 0, N=1).  Falls back to the oracle port when
+    baseline/_ref is absent."""
+    from baseline import ref_arm
+    if ref_arm.load_gnnsim() is not None:
+        per, steps = 256, max(2, int(budget_s * 300 / 256))  # ~300 seeds/s on one core
+        rate, procs, times, info = ref_arm.run(cfg, per, steps, 1, procs=1)
+        return {"value": round(rate, 2), "unit": "seeds/s", "cores": 1, "kind": "reference",
+                "sample": f"{per * len(times)} roots ({len(times)} timed steps of {per}, keyed "
+                          "sample of the workload) through gnnsim itself (baseline/_ref): "
+                          "sample_micrograph (numba) + FeatureStore-style row lookup + float64 "
+                          "forward/loss_and_backward + sync_and_update, one core (BLAS 1 thread)",
+                "rows_materialised": info["rows_materialised"]}
     from oracle.cpu_bench import run_single
     from oracle.graphgen import GraphSpec as OSpec
     spec = OSpec(n=cfg["n"], avg_deg=cfg["avg_deg"], beta=cfg["beta"], p_in=cfg["p_in"],
@@ -136,34 +149,90 @@ def cpu_baseline(cfg, budget_s=15.0):
     rate, done = run_single(spec, kw, cfg["seed"], 32, 64, budget_s=budget_s)
     return {"value": round(rate, 2), "unit": "seeds/s", "cores": 1, "kind": "port",
             "sample": f"{done} roots (32-root steps, keyed sample of the epoch) through the "
-                      "oracle port: numpy/numba sampling on lazily materialised rows + float64 "
-                      "SAGE forward/backward + SGD, one core"}
+                      "oracle port (gnnsim not installed in baseline/_ref), one core"}
+
+
+def parity_block(g, cfg, perm, it, B, n_check=256):
+    """Untimed bit-exact check of the timed iterations' micrographs: the first
+    n_check roots of iteration `it`, built by the device group build the loop
+    uses, against the CPU oracle (layers, pairs, vertices, plans)."""
+    import numpy as np
+    import torch
+    from oracle import model as OM
+    from oracle.cpu_bench import LazyGraphSampler
+    from oracle.graphgen import GraphSpec as OSpec
+    from oracle.rng import chain
+    from paper_2409_00657_b200.engine import BUILD_CTAS_PER_SM
+    from paper_2409_00657_b200.sampler import GroupBuilder, MicrographBatch, MicrographBuilder
+    fo = tuple(cfg["fanout"])
+    roots = perm[it * B:it * B + n_check].contiguous()
+    st = chain(chain(cfg["seed"], 0x06), 0, it)
+    b = MicrographBuilder(fo, n_check)
+    gb = GroupBuilder([b])
+    gb.roots.copy_(roots)
+    gb.keys.fill_(int(np.uint64(st).view(np.int64)))
+    gb.build(g, ctas_per_sm=BUILD_CTAS_PER_SM)
+    torch.cuda.synchronize()
+    gb.check()
+    batch = MicrographBatch(len(fo), n_check, b.tensors)
+    h = batch.to_host()
+    rh = roots.cpu().numpy()
+    got = batch.micrographs(rh, h)
+    spec = OSpec(n=cfg["n"], avg_deg=cfg["avg_deg"], beta=cfg["beta"], p_in=cfg["p_in"],
+                 n_blocks=cfg["n_blocks"], d_cap=cfg["d_cap"], seed=cfg["seed"])
+    want = LazyGraphSampler(spec).micrographs(rh, fo, [chain(st, int(r)) for r in rh])
+    bad = 0
+    for i, (m, w) in enumerate(zip(got, want)):
+        ok = (all(np.array_equal(x, y) for x, y in zip(m.layers, w.layers))
+              and all(np.array_equal(a, c) and np.array_equal(b_, d)
+                      for (a, b_), (c, d) in zip(m.pairs, w.pairs))
+              and np.array_equal(m.vertices, w.vertices))
+        need, steps = batch.plans(i, h)
+        o_need, o_steps = OM.build_plan(w)
+        ok = ok and all(np.array_equal(x, y) for x, y in zip(need, o_need))
+        ok = ok and all(np.array_equal(a, c) for x, y in zip(steps, o_steps) for a, c in zip(x, y))
+        bad += not ok
+    return {"roots_checked": len(got), "iteration": it, "mismatches": bad,
+            "fields": "layers, pairs, vertices, need sets, self_pos/dpos/spos/deg",
+            "checker": "CPU oracle (oracle/, pinned to gnnsim goldens), untimed"}
 
 
 def run_reference(args, cfg):
+    """The reference arm: gnnsim itself (baseline/_ref) on all host cores, 1024
+    roots per step (the bench's batch), on a bounded keyed sample of the
+    workload (baseline/ref_arm.py).  Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from oracle.cpu_bench import run_pool
-    from oracle.graphgen import GraphSpec as OSpec
-    spec = OSpec(n=cfg["n"], avg_deg=cfg["avg_deg"], beta=cfg["beta"], p_in=cfg["p_in"],
-                 n_blocks=cfg["n_blocks"], d_cap=cfg["d_cap"], seed=cfg["seed"])
-    kw = dict(arch=cfg["arch"], fanout=cfg["fanout"], dim=cfg["dim"], hidden=cfg["hidden"],
-              classes=cfg["classes"])
-    procs = os.cpu_count() or 1
-    per_step = 16 * procs
-    rate, procs, times = run_pool(spec, kw, cfg["seed"], per_step, args.steps, args.warmup, procs)
+    from baseline import ref_arm
+    per_step = cfg["batch"]
+    if ref_arm.load_gnnsim() is not None:
+        rate, procs, times, info = ref_arm.run(cfg, per_step, args.steps, args.warmup)
+        kind = "reference"
+        sample = (f"{per_step} keyed-sample roots per step (same batch as the GPU arm), "
+                  f"disjoint slices over {procs} worker processes (one core each, BLAS 1 "
+                  "thread), gnnsim's own sample_micrograph / forward / loss_and_backward / "
+                  "sync_and_update; parameters and gradient accumulators in shared memory")
+    else:
+        from oracle.cpu_bench import run_pool
+        from oracle.graphgen import GraphSpec as OSpec
+        spec = OSpec(n=cfg["n"], avg_deg=cfg["avg_deg"], beta=cfg["beta"], p_in=cfg["p_in"],
+                     n_blocks=cfg["n_blocks"], d_cap=cfg["d_cap"], seed=cfg["seed"])
+        kw = dict(arch=cfg["arch"], fanout=cfg["fanout"], dim=cfg["dim"], hidden=cfg["hidden"],
+                  classes=cfg["classes"])
+        rate, procs, times = run_pool(spec, kw, cfg["seed"], per_step, args.steps, args.warmup)
+        info, kind = {}, "port"
+        sample = f"{per_step} roots per step over {procs} processes (oracle port; gnnsim absent)"
     ms = 1000.0 * sum(times) / len(times)
     line = {"impl": "reference", "metric": "seeds_per_sec", "value": round(rate, 2),
             "unit": "seeds/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "roots_per_step": per_step,
-                       "fanout": list(cfg["fanout"]), "hidden": cfg["hidden"]},
+            "config": {"workload": cfg["workload"], "global_batch": per_step,
+                       "fanout": list(cfg["fanout"]), "hidden": cfg["hidden"],
+                       "same_config": True},
             "cpu_baseline": {"value": round(rate, 2), "unit": "seeds/s", "cores": procs,
-                             "kind": "port",
-                             "sample": f"{per_step} keyed-sample roots per step split over "
-                                       f"{procs} processes (oracle port of the reference path)"},
+                             "kind": kind, "sample": sample, **info},
             "e2e": {"value": round(rate, 2), "unit": "seeds/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
             "epoch_time_s_extrapolated": round(cfg["n"] / rate, 1)}
@@ -445,6 +514,7 @@ def _run_ours(args, cfg, dev):
     }
     if not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(cfg, budget_s=args.cpu_budget)
+        line["parity"] = parity_block(g, cfg, tr.perm, W, B)
     print(json.dumps(line), flush=True)
     return 0
 

@@ -43,6 +43,30 @@ class LazyGraphSampler:
         flat = np.concatenate(parts) if parts else np.empty(0, np.int64)
         return counts, flat
 
+    def expanded_vertices(self, roots, fanout, keys) -> np.ndarray:
+        """Sorted ids of every vertex the roots' micrographs expand (layers 1..L),
+        hop by hop, materialising each hop's frontier rows in one vectorised
+        pass (rows_csr)."""
+        L = len(fanout)
+        front = [np.array([int(r)], dtype=np.int64) for r in roots]
+        seen = [np.concatenate(front)] if front else []
+        for hop in range(1, L):
+            self.rows.prefetch(np.concatenate(front))
+            nxt = []
+            for i, f in enumerate(front):
+                _, flat = self.frontier(f, fanout[hop - 1], chain(int(keys[i]), hop))
+                nxt.append(np.unique(flat))
+            front = nxt
+            seen.extend(front)
+        out = np.unique(np.concatenate(seen)) if seen else np.empty(0, np.int64)
+        self.rows.prefetch(out)
+        return out
+
+    def micrographs(self, roots, fanout, keys):
+        """micrograph() for many roots (rows prefetched hop by hop)."""
+        self.expanded_vertices(roots, fanout, keys)
+        return [self.micrograph(int(r), fanout, int(k)) for r, k in zip(roots, keys)]
+
     def micrograph(self, root: int, fanout, key: int):
         from .sampler import Micro
         L = len(fanout)

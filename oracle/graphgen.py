@@ -204,6 +204,48 @@ def build_csr(t: GraphTables):
     return offsets, targets.astype(np.int64)
 
 
+def rows_csr(t: GraphTables, vs) -> tuple:
+    """Canonical rows of many vertices at once (vectorised ``row``): returns a
+    sub-CSR (offsets int64[len(vs)+1], targets int64) whose row i is row(t, vs[i])."""
+    vs = np.asarray(vs, dtype=np.int64)
+    if len(vs) == 0:
+        return np.zeros(1, np.int64), np.empty(0, np.int64)
+    d = raw_degree(t, vs)
+    owner = np.repeat(np.arange(len(vs), dtype=np.int64), d)
+    start = np.zeros(len(vs) + 1, dtype=np.int64)
+    np.cumsum(d, out=start[1:])
+    slots = (np.arange(int(start[-1]), dtype=np.int64) - start[owner]).astype(np.uint64)
+    v = vs[owner]
+    rk = mix64_array(v.astype(np.uint64) ^ U64(t.spec.key))
+    hA = mix64_array((U64(2) * slots) ^ rk)
+    hB = mix64_array((U64(2) * slots + U64(1)) ^ rk)
+    nb = t.spec.n_blocks
+    own = block_of(t, v)
+    inb = (hB >> U64(32)) < U64(t.thr_in) if t.thr_in <= MASK32 else np.ones(len(v), bool)
+    if nb > 1:
+        other = (own + 1 + ((hB & U64(MASK32)) % U64(nb - 1)).astype(np.int64)) % nb
+        tb = np.where(inb, own, other)
+    else:
+        tb = own
+    u = hA >> U64(32)
+    e = np.searchsorted(t.cum, u, side="right")
+    off = (((hA & U64(MASK32)) * t.lvl_size[e].astype(np.uint64)) >> U64(32)).astype(np.int64)
+    r = ((U64(1) << e.astype(np.uint64)) - U64(1)).astype(np.int64) + off
+    nbk = (t.block_start[tb + 1] - t.block_start[tb]).astype(np.uint64)
+    diff = (r.astype(np.uint64) + nbk - (t.c[tb] % nbk)) % nbk
+    tgt = t.block_start[tb] + ((diff * t.a_inv[tb]) % nbk).astype(np.int64)
+    # per row: sort, unique, drop the self-loop (one lexsort over (owner, target))
+    order = np.lexsort((tgt, owner))
+    o, x = owner[order], tgt[order]
+    keep = np.ones(len(x), dtype=bool)
+    keep[1:] = (o[1:] != o[:-1]) | (x[1:] != x[:-1])
+    keep &= x != vs[o]
+    o, x = o[keep], x[keep]
+    offsets = np.zeros(len(vs) + 1, dtype=np.int64)
+    np.cumsum(np.bincount(o, minlength=len(vs)), out=offsets[1:])
+    return offsets, x
+
+
 class LazyRows:
     """CSR facade materialising rows on demand (CPU baseline on huge specs)."""
 
@@ -217,3 +259,17 @@ class LazyRows:
             r = row(self.t, v)
             self.cache[v] = r
         return r
+
+    def prefetch(self, vs) -> None:
+        """Materialise many rows in one vectorised pass (rows_csr)."""
+        vs = np.unique(np.asarray(vs, dtype=np.int64))
+        vs = np.array([v for v in vs.tolist() if v not in self.cache], dtype=np.int64)
+        if not len(vs):
+            return
+        # chunks of <= ~4M raw slots (bounded temporaries on high-degree graphs)
+        cum = np.cumsum(raw_degree(self.t, vs))
+        cuts = np.searchsorted(cum, np.arange(1, int(cum[-1]) // (1 << 22) + 1) * (1 << 22))
+        for part in np.split(vs, np.unique(cuts[(cuts > 0) & (cuts < len(vs))])):
+            off, tgt = rows_csr(self.t, part)
+            for i, v in enumerate(part.tolist()):
+                self.cache[v] = tgt[off[i]:off[i + 1]]

@@ -272,213 +272,6 @@ k_aggregate(RowSrc<T> rs_in, AggSegs<T> segs, int W, int out_ld, int pad_cap) {
   }
 }
 
-// ------------------------------------------------------------------ TMA-staged gather
-//
-// Layer-1 gather + aggregate with the source rows staged in shared memory by
-// bulk asynchronous copies (cp.async.bulk, completion counted in bytes on an
-// mbarrier).  Bytes in flight are then bounded by shared memory rather than
-// registers: one persistent CTA per SM keeps a ring of NS stages, each
-// holding a tile of TR destination rows with all their source rows
-// (self + up to max_deg neighbours).
-//   warp 0      producer: per tile, lane l owns row r0+l -- reads its CSR
-//               range and self index (coalesced across lanes), a warp scan
-//               places the rows' slots, one lane posts the tile's byte count
-//               on the stage's "full" barrier, every lane issues one 16-byte-
-//               aligned bulk copy per source row;
-//   warps 1..7  consumers: wait "full", reduce each row's slots from shared
-//               memory (16-byte lanes, G lanes per row), write agg, arrive on
-//               the stage's "empty" barrier.
-// Rows with more neighbours than the slots allow (never, when max_deg is the
-// sampling fanout) are reduced straight from global memory by the consumer.
-struct TmaMeta {
-  int32_t row;   // destination row
-  int32_t deg;
-  int32_t base;  // first slot (self), -1: not staged
-  int32_t self;  // self index (RowSrc)
-};
-
-__device__ __forceinline__ uint32_t sm_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void gbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(bar)), "r"(count));
-}
-__device__ __forceinline__ void gbar_expect_arrive(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_addr(bar)),
-               "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void gbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sm_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void gbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE_%=;\n"
-      "bra WAIT_%=;\n"
-      "DONE_%=:\n"
-      "}\n" ::"r"(sm_addr(bar)), "r"(phase) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-      ::"r"(sm_addr(dst)), "l"(src), "r"(bytes), "r"(sm_addr(bar)) : "memory");
-}
-
-constexpr int kTmaStages = 4;
-constexpr int kTmaThreads = 256;
-constexpr int kTmaConsumers = kTmaThreads / 32 - 1;
-
-template <typename T, bool SAGE>
-__global__ void __launch_bounds__(kTmaThreads, 1)
-k_aggregate_tma(RowSrc<T> rs, AggSegs<T> segs, int n_segs, int cap_rows, int W, int out_ld,
-                int pad_cap, int TR, int slots, int max_deg) {
-  extern __shared__ __align__(128) uint8_t tsm[];
-  __shared__ __align__(8) uint64_t full_bar[kTmaStages], empty_bar[kTmaStages];
-  __shared__ TmaMeta meta[kTmaStages][32];
-  __shared__ int meta_n[kTmaStages];
-  constexpr int VEC = Vec<T>::N;
-  constexpr unsigned FULL = 0xffffffffu;
-  const int rowbytes = W * (int)sizeof(T);
-  const int stage_bytes = slots * rowbytes;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kTmaStages; ++s) {
-      gbar_init(&full_bar[s], 1);
-      gbar_init(&empty_bar[s], kTmaConsumers);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  pdl_trigger();
-  pdl_wait();
-  if (pad_cap && blockIdx.x == gridDim.x - 1) {
-    // tensor-core dW reduces over rows up to the next multiple of 64: zero them
-    for (int b = 0; b < n_segs; ++b) {
-      const int n = *segs.n_rows[b];
-      const int pad = min(pad_cap, (n + 63) / 64 * 64);
-      for (int64_t i = threadIdx.x; i < (int64_t)(pad - n) * out_ld; i += blockDim.x)
-        segs.out[b][(int64_t)n * out_ld + i] = from_f<T>(0.f);
-    }
-  }
-  const int tiles_per_seg = (cap_rows + TR - 1) / TR;
-  const int total_tiles = tiles_per_seg * n_segs;
-  if (warp == 0) {
-    // ---------------- producer
-    int i = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-      const int b = t / tiles_per_seg;
-      const int r0 = (t % tiles_per_seg) * TR;
-      const int n = min(TR, *segs.n_rows[b] - r0);
-      if (n <= 0) continue;
-      const int s = i % kTmaStages;
-      if (i >= kTmaStages) gbar_wait(&empty_bar[s], ((i / kTmaStages) - 1) & 1);
-      const int32_t* off = segs.nbr_off[b];
-      int j0 = 0, deg = 0, self = 0, need = 0;
-      if (lane < n) {
-        j0 = off[r0 + lane];
-        deg = off[r0 + lane + 1] - j0;
-        self = segs.self_pos[b][r0 + lane];
-        need = deg <= max_deg ? deg + 1 : 0;
-      }
-      int base = need;  // inclusive warp scan -> exclusive slot base
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(FULL, base, o);
-        if (lane >= o) base += y;
-      }
-      const int total = __shfl_sync(FULL, base, 31);
-      base -= need;
-      if (lane < n) meta[s][lane] = TmaMeta{r0 + lane, deg, need ? base : -1, self};
-      __syncwarp();  // meta visible before the arrive releases the stage
-      if (lane == 0) {
-        meta_n[s] = n;
-        // tx bytes may land before the expectation is posted: the phase cannot
-        // complete before this arrival either way
-        gbar_expect_arrive(&full_bar[s], (uint32_t)(total * rowbytes));
-      }
-      if (need) {
-        uint8_t* dst = tsm + (size_t)s * stage_bytes + (size_t)base * rowbytes;
-        const int32_t* idx = segs.nbr_idx[b] + j0;
-        bulk_g2s(dst, rs.row(self), rowbytes, &full_bar[s]);
-        for (int j = 0; j < deg; ++j)
-          bulk_g2s(dst + (size_t)(j + 1) * rowbytes, rs.row(idx[j]), rowbytes, &full_bar[s]);
-      }
-      ++i;
-    }
-    return;
-  }
-  // ---------------- consumers
-  const int nvec = W / VEC;
-  const int G = nvec >= 32 ? 32 : (nvec >= 16 ? 16 : (nvec >= 8 ? 8 : (nvec >= 4 ? 4 : (nvec >= 2 ? 2 : 1))));
-  const int P = 32 / G;
-  const int gi = lane / G, gl = lane % G;
-  const int cw = warp - 1;
-  int i = 0;
-  for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-    const int b = t / tiles_per_seg;
-    const int r0 = (t % tiles_per_seg) * TR;
-    const int n_t = min(TR, *segs.n_rows[b] - r0);
-    if (n_t <= 0) continue;
-    const int s = i % kTmaStages;
-    gbar_wait(&full_bar[s], (i / kTmaStages) & 1);
-    const uint8_t* stage = tsm + (size_t)s * stage_bytes;
-    T* outb = segs.out[b];
-    for (int q = cw * P + gi; q - gi < n_t; q += kTmaConsumers * P) {
-      const bool ok = q < n_t;
-      TmaMeta m{0, 0, 0, 0};
-      if (ok) m = meta[s][q];
-      T* o = outb + (int64_t)m.row * out_ld;
-      for (int c0 = 0; c0 < nvec; c0 += G) {
-        const int cv = c0 + gl;
-        if (!ok || cv >= nvec) continue;
-        const int col = cv * VEC;
-        float self[VEC], acc[VEC];
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) acc[e] = 0.f;
-        if (m.base >= 0) {
-          const uint8_t* sl = stage + (size_t)m.base * rowbytes + col * sizeof(T);
-          load_vec_s(reinterpret_cast<const T*>(sl), self);
-          for (int j = 1; j <= m.deg; ++j) {
-            float x[VEC];
-            load_vec_s(reinterpret_cast<const T*>(sl + (size_t)j * rowbytes), x);
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) acc[e] += x[e];
-          }
-        } else {  // more neighbours than slots: straight from global memory
-          load_vec(rs.row(m.self) + col, self);
-          const int32_t* off = segs.nbr_off[b];
-          const int j0 = off[m.row];
-          for (int j = 0; j < m.deg; ++j) {
-            float x[VEC];
-            load_vec(rs.row(segs.nbr_idx[b][j0 + j]) + col, x);
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) acc[e] += x[e];
-          }
-        }
-        if constexpr (SAGE) {
-          float nb[VEC];
-          const float inv = m.deg > 0 ? 1.0f / (float)m.deg : 0.f;
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) nb[e] = m.deg > 0 ? acc[e] * inv : self[e];
-          store_vec(o + col, self);
-          store_vec(o + W + col, nb);
-        } else {
-          const float inv = 1.0f / (float)(m.deg + 1);
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) acc[e] = (acc[e] + self[e]) * inv;
-          store_vec(o + col, acc);
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) gbar_arrive(&empty_bar[s]);
-    ++i;
-  }
-}
-
 // ------------------------------------------------------------------ SIMT GEMM
 //
 // C[m,n] = sum_k A(m,k) B(k,n); A(m,k) = AT ? A[k*lda+m] : A[m*lda+k],
@@ -1128,37 +921,6 @@ static void launch_aggregate_n(const hg_step_desc* const* ds, int n, int k, cuda
     segs.out[b] = (T*)e->agg[k];
     cap = std::max(cap, e->max_rows[k]);
   }
-  // layer 1 with a known neighbour bound: TMA-staged persistent gather
-  // opt-in (HG_AGG_TMA=1): measured 3.7x slower than the register gather on
-  // the papers step -- one producer warp per SM serialises the index chain
-  static const bool tma_on = [] {
-    const char* e = getenv("HG_AGG_TMA");
-    return e && e[0] == '1';
-  }();
-  const int max_deg = d->max_deg[k];
-  const int rowbytes = Wd * (int)sizeof(T);
-  if (tma_on && k == 1 && max_deg > 0 && rowbytes % 16 == 0 && (n == 1 || !d->row_handle)) {
-    constexpr int kSmemBudget = 200 * 1024;  // kTmaStages stages of TR rows x (max_deg+1) slots
-    const int per_row = (max_deg + 1) * rowbytes;
-    const int TR = std::min(32, kSmemBudget / kTmaStages / per_row);
-    if (TR >= 1) {
-      const int slots = TR * (max_deg + 1);
-      const size_t smem = (size_t)kTmaStages * slots * rowbytes;
-      static size_t smem_set[2] = {0, 0};
-      auto kern = d->arch == 1 ? k_aggregate_tma<T, true> : k_aggregate_tma<T, false>;
-      if (smem_set[d->arch == 1] < smem) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        smem_set[d->arch == 1] = smem;
-      }
-      const int pad_cap = pad && sizeof(T) == 2 ? d->max_rows[k] : 0;
-      prof_begin(PROF_AGG1, s);
-      count_launch();
-      launch_pdl(kern, dim3(num_sms()), dim3(kTmaThreads), smem, s, row_src<T>(d, k), segs, n,
-                 cap, Wd, d->in_dim[k], pad_cap, TR, slots, max_deg);
-      prof_end(PROF_AGG1, s);
-      return;
-    }
-  }
   // rows per CTA: 8 warps x (32 / lanes per row); blocks past the device row count exit
   const int nvec = Wd / (16 / (int)sizeof(T));
   const int lanes = nvec >= 32 ? 32 : nvec >= 16 ? 16 : nvec >= 8 ? 8 : nvec >= 4 ? 4 : nvec >= 2 ? 2 : 1;
@@ -1196,9 +958,14 @@ static void scatter_root_attrs() {
   done = true;
 }
 
-static bool getenv_on(const char* name) {  // A/B switches: NAME=1 selects a variant
-  const char* e = getenv(name);
-  return e && e[0] == '1';
+// A/B switch read once per process: HG_FUSED_HEAD=1 puts the softmax-CE in the
+// tcgen05 head GEMM's epilogue (umma_head_ce; tested, measured slower on B200)
+static bool fused_head_on() {
+  static const bool on = [] {
+    const char* e = getenv("HG_FUSED_HEAD");
+    return e && e[0] == '1';
+  }();
+  return on;
 }
 
 // bf16 dz operand of layer k (per-layer region when lowp_layered)
@@ -1275,7 +1042,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     if (tc) {
       int st = umma_gemm(d->agg[k], d->in_dim[k], false, d->Wlp[k], d->in_dim[k], false, d->h[k], H,
                          d->max_rows[k], H, d->in_dim[k], tot + k, nullptr, 1, d->b[k], 1, s);
-      if (st) return st;
+      if (st) { join(); return st; }
     } else {
       gemm<T, false, false, EPI_BIAS_RELU, T, T>(s, (const T*)d->agg[k], d->in_dim[k], d->W[k], H,
                                                  (T*)d->h[k], H, tot + k, d->max_rows[k], H,
@@ -1284,8 +1051,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     if (k == 1) prof_end(PROF_GEMM1, s);
   }
   // classifier head (model.py:246, 253-265)
-  const bool tc_head = tc && C <= 256 && d->WcT && d->Wcp && d->dl_lowp &&
-                       !getenv_on("HG_SIMT_HEAD");  // A/B: the fused one-kernel head
+  const bool tc_head = tc && C <= 256 && d->WcT && d->Wcp && d->dl_lowp;
   const int Cp = (C + 63) / 64 * 64;
   if (tc_head) {
     // logits = h_L @ W_c on tcgen05 (B = W_cᵀ bf16, K-major); softmax-CE writes
@@ -1298,14 +1064,14 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     }
     // root rows: n_roots is the capacity, the device count N_L the actual roots
     int st;
-    if (C <= 192 && getenv_on("HG_FUSED_HEAD")) {  // A/B: softmax-CE in the GEMM epilogue
+    if (C <= 192 && fused_head_on()) {
       st = umma_head_ce(d->h[L], H, d->WcT, H, d->logits, C, n_roots, H, tot + L, d->roots,
                         d->label_state, d->loss, (bf16*)d->dl_lowp, Cp, s);
-      if (st) return st;
+      if (st) { join(); return st; }
     } else {
     st = umma_gemm(d->h[L], H, false, d->WcT, H, false, d->logits, C, n_roots, C, H,
                        tot + L, nullptr, 0, nullptr, 1, s);
-    if (st) return st;
+    if (st) { join(); return st; }
     count_launch();
     launch_pdl(k_softmax_ce, dim3((n_roots + 7) / 8), dim3(256), 0, s, d->logits, C, d->roots, n_roots, tot + L,
                                                    d->label_state, d->loss,
@@ -1315,7 +1081,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
       // dz_L = (dlogits @ W_cᵀ) * (h_L > 0); gb_L; bf16 dz_L for the dW GEMM
       st = umma_gemm(d->dl_lowp, Cp, false, d->Wcp, Cp, false, d->dh[L], H, n_roots, H, Cp,
                      tot + L, nullptr, 0, nullptr, 1, s);
-      if (st) return st;
+      if (st) { join(); return st; }
       dim3 g((H + 31) / 32, 16);
       count_launch();
       launch_pdl(k_mask_colsum<T>, dim3(g), dim3(256), 0, s, d->dh[L], (const T*)d->h[L], tot + L, H, d->gb[L],
@@ -1324,7 +1090,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
       const int split = std::max(1, std::min(16, n_roots / 256));
       st = umma_gemm(d->h[L], H, true, d->dl_lowp, Cp, true, d->gWc, C, H, C, n_roots,
                      nullptr, tot + L, 2, nullptr, split, fork());
-      if (st) return st;
+      if (st) { join(); return st; }
     }
   } else {
     const size_t smem = ((size_t)H * (C | 1) + H + 8 * H + 8 * C) * sizeof(float);
@@ -1361,7 +1127,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
       cudaStream_t ws = k >= 2 && d->lowp_layered ? fork() : s;
       int st = umma_gemm(d->agg[k], d->in_dim[k], true, dz_lowp(d, k), H, true, d->gW[k], H,
                          d->in_dim[k], H, d->max_rows[k], nullptr, tot + k, 2, nullptr, split, ws);
-      if (st) return st;
+      if (st) { join(); return st; }
     } else {
       gemm<T, true, false, EPI_ATOMIC, float, T>(s, (const T*)d->agg[k], d->in_dim[k], d->dh[k], H,
                                                  d->gW[k], H, nullptr, d->in_dim[k], H, tot + k,
@@ -1373,14 +1139,14 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     if (tc && d->in_dim[k] % 64 == 0 && d->Wb[k]) {
       int st = umma_gemm(dz_lowp(d, k), H, false, d->Wb[k], H, false, d->dagg, d->in_dim[k],
                          d->max_rows[k], d->in_dim[k], H, tot + k, nullptr, 0, nullptr, 1, s);
-      if (st) return st;
+      if (st) { join(); return st; }
     } else {
       gemm<float, false, true, EPI_STORE, float, T>(s, d->dh[k], H, d->W[k], H, d->dagg,
                                                     d->in_dim[k], tot + k, d->max_rows[k],
                                                     d->in_dim[k], nullptr, H, nullptr, nullptr, 0,
                                                     1);
     }
-    if (k == L && H % 8 == 0 && H <= 256 && !getenv_on("HG_SCATTER_GENERIC")) {
+    if (k == L && H % 8 == 0 && H <= 256) {
       // top layer: per-row map, no scatter (k_scatter_top)
       const bool tc_dx = tc && d->in_dim[k - 1] % 64 == 0 && d->Wb[k - 1];
       const bool want_f32 = !tc || (k - 1 >= 2 && !tc_dx);

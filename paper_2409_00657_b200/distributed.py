@@ -299,11 +299,10 @@ class PeerFeatures:
         d.row_handle = None
         d.rank = self.rank
 
-    def bind_staged(self, runner: CellRunner, stage_cap: int) -> None:
-        """Staged mode: remote rows are pre-gathered into local HBM (the staging
-        rows of this rank's mailbox) by hg_pregather_push, the gather reads HBM
-        only.  The first call allocates and exchanges the mailboxes (collective:
-        every rank reaches it at the same step)."""
+    def alloc_mailbox(self, stage_cap: int) -> None:
+        """Allocate this rank's mailbox (signal counters, request list, staging
+        rows) and map every peer's (collective: all ranks call it together, at
+        trainer setup -- never lazily behind a per-rank root count)."""
         if not hasattr(self, "mbox"):
             dev = self.device
             S, row = self.S, self.ld * (2 if self.dtype == torch.bfloat16 else 4)
@@ -341,6 +340,15 @@ class PeerFeatures:
             self.seq = torch.zeros(1, dtype=torch.int64, device=dev)
             self.stamp = torch.zeros(len(self.local_row), dtype=torch.int32, device=dev)
             self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def bind_staged(self, runner: CellRunner, stage_cap: int) -> None:
+        """Staged mode: remote rows are pre-gathered into local HBM (the staging
+        rows of this rank's mailbox) by hg_pregather_push, the gather reads HBM
+        only.  The mailbox must already exist (alloc_mailbox)."""
+        if not hasattr(self, "mbox"):
+            raise InvariantViolation("bind_staged before alloc_mailbox (collective setup)")
+        if int(stage_cap) > self.stage_cap:
+            raise ValueError(f"staging capacity {stage_cap} > mailbox {self.stage_cap}")
         d = runner.desc
         d.features = self.ptr
         d.feat_row = self.local_row.data_ptr()
@@ -405,6 +413,17 @@ class PeerFeatures:
                 _lib.call("hg_resolve_rows", ip, np_, self.home.data_ptr(), self.rank,
                           self.local_row.data_ptr(), self.stage_row.data_ptr(),
                           r.desc.row_handle, stream)
+
+    def check(self) -> None:
+        """Raise if a push pre-gather gave up waiting on a peer or dropped an
+        overflowing staging slot (device flag set by k_pg_wait / k_stage_mark)."""
+        err = getattr(self, "err", None)
+        if err is None:
+            return
+        code = int(err.item())
+        if code:
+            err.zero_()
+            _lib.flag_status(code, "hg_pregather_push (peer wait timed out or staging overflow)")
 
     def close(self):
         for p in self.opened:
@@ -693,6 +712,12 @@ class MicrographTrainer:
         if not pregather:
             for r in self.runners:
                 self.feats.bind(r)
+            # the push pre-gather's mailbox is set up collectively here; a group
+            # push stages the distinct remote rows of graph_group iterations
+            lay0 = self.runners[0].builder.layout
+            self._stage_cap = min(self.runners[0].max_roots * lay0.cap_need[0]
+                                  * self.graph_group, self.part.n_vertices)
+            self.feats.alloc_mailbox(self._stage_cap)
         # device-side per-iteration pre-gather accounting (peer mode): [iter][home]
         self._acct_rows = None
         self._acct_total = torch.zeros(1, dtype=torch.int64, device=self.device)
@@ -984,7 +1009,7 @@ class MicrographTrainer:
         def launch(r, s):
             r.n_roots = n
             if not n:
-                if not self.pregather and hasattr(self.feats, "mbox"):
+                if not self.pregather:
                     # the push pre-gather is collective: take part with no requests
                     self.feats.pregather(r, self._acct_rows[it].data_ptr(),
                                          self._acct_total.data_ptr(), s, empty=True)
@@ -1029,18 +1054,14 @@ class MicrographTrainer:
         if self.pregather:  # staging exchange needs host-known sizes: no run-ahead
             r = self.runners[0]
             self._fast_build(it)(r, s)
-            if r.n_roots:
-                self._exchange([r], [r.n_roots], it)
+            # collective: a rank with no roots this iteration still takes part
+            self._exchange([r] if r.n_roots else [], [r.n_roots], it)
         else:
             if not hasattr(self, "_ra"):
                 from .engine import RunAhead
                 self.runners.append(CellRunner(self.graph, self.runners[0].table, self.model,
                                                self.fanout, self.runners[0].max_roots,
                                                self.labels))
-                lay = self.runners[0].builder.layout
-                # a group push stages the distinct remote rows of graph_group iterations
-                self._stage_cap = min(self.runners[0].max_roots * lay.cap_need[0]
-                                      * self.graph_group, self.part.n_vertices)
                 self._ra = RunAhead(self.runners[:2], self.device)
             r = self._ra.acquire(it, self._fast_build(it))
         n = r.n_roots
@@ -1260,6 +1281,7 @@ class MicrographTrainer:
         """Move device-side pre-gather counts into the ledger (reference messages:
         one per (home -> server) per iteration with rows, featstore.py:271-274)
         and the fast path's per-iteration hop / all-reduce entries."""
+        self.check()
         fast = getattr(self, "_fast_iters", 0)
         if fast:
             self._account_hops_and_sync(fast)
@@ -1318,6 +1340,16 @@ class MicrographTrainer:
         if S > 1:
             self.ledger.add(rank, (rank + 1) % S, GRADIENT, 2.0 * (S - 1) / S * pb * mult,
                             2 * (S - 1) * mult)
+
+    def check(self) -> None:
+        """Synchronise and raise on any device error flag: build errors (root
+        out of range), push pre-gather timeouts / staging overflow."""
+        for r in self.runners:
+            r.check()
+        if self._dgl is not None and hasattr(self._dgl, "check"):
+            self._dgl.check()
+        if hasattr(self.feats, "check"):
+            self.feats.check()
 
     def close(self) -> None:
         """Release peer mappings (CUDA IPC) held by this trainer."""

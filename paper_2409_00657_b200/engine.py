@@ -507,7 +507,13 @@ class Trainer:
                 self.graph, self.table, self.model, self.fanout, self.B, self.labels)],
                 self.device) if self.run_ahead else None
         e = self._e2e
-        if self.graphs and self.G == 1 and next_roots_host is not None:
+        if roots_host.numel() > self.B or (next_roots_host is not None
+                                           and next_roots_host.numel() > self.B):
+            raise ValueError(f"train_step takes at most B = {self.B} roots per step")
+        # the captured graph stages and trains exactly B roots: a short batch
+        # (the epoch tail) takes the eager path
+        if (self.graphs and self.G == 1 and next_roots_host is not None
+                and roots_host.numel() == self.B and next_roots_host.numel() == self.B):
             gl = self._graph_ready("_gl_e2e", True)
             if gl is not None:
                 return self._train_step_graph(gl, roots_host, it, next_roots_host)

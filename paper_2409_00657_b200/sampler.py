@@ -115,9 +115,9 @@ class MicrographBatch:
             h[name] = [None if x is None else x.cpu().numpy() for x in getattr(self, name)]
         return h
 
-    def micrographs(self, roots) -> list:
+    def micrographs(self, roots, h: dict = None) -> list:
         """Rebuild reference ``Micrograph`` objects (parity checks)."""
-        h = self.to_host()
+        h = self.to_host() if h is None else h
         L = self.L
         out = []
         for r, root in enumerate(np.asarray(roots).tolist()):
@@ -144,9 +144,10 @@ class MicrographBatch:
             out.append(Micrograph(int(root), tuple(layers), tuple(pairs), need[0]))
         return out
 
-    def plans(self, r: int):
-        """need sets and (self_pos, dpos, spos, deg) of root r in local numbering."""
-        h = self.to_host()
+    def plans(self, r: int, h: dict = None):
+        """need sets and (self_pos, dpos, spos, deg) of root r in local numbering
+        (h: a to_host() snapshot, reused across roots)."""
+        h = self.to_host() if h is None else h
         L = self.L
         need = [h["need_ids"][k][h["need_off"][k][r]:h["need_off"][k][r + 1]].astype(np.int64)
                 for k in range(L + 1)]
