@@ -71,6 +71,22 @@ int hg_sample_frontier(const int64_t* offsets, const int32_t* targets, int64_t n
 int hg_feature_rows(const int64_t* ids, int64_t n, int32_t dim, uint64_t state, float* out,
                     void* stream);
 
+/* replaces kernels.pick_k_smallest (_kernels_nb.py:92-106 / _kernels_np.py:87-98):
+ * the k of ids[n] with the smallest keys (mix64(state ^ id) & HI32) | i, written to
+ * out[min(k, n)] in index order.  n < 2^32. */
+int hg_pick_k_smallest(const int64_t* ids, int64_t n, int64_t k, uint64_t state, int64_t* out,
+                       void* stream);
+
+/* replaces kernels.sbm_edges (_kernels_nb.py:22-52 / _kernels_np.py:17-52): every
+ * unordered pair u < v of block_of[n] once; same-block pairs accepted by
+ * (mode_in, thr_in), the others by (mode_out, thr_out) (mode 0 never, 1 iff
+ * mix64(mix64(state ^ u) ^ v) < thr, 2 always).  *count_host receives the edge
+ * count (synchronises `stream`); with us/vs non-NULL (capacity cap) the edges are
+ * written in (u, v) lexicographic order. */
+int hg_sbm_edges(const int64_t* block_of, int64_t n, int32_t mode_in, uint64_t thr_in,
+                 int32_t mode_out, uint64_t thr_out, uint64_t state, int64_t* us, int64_t* vs,
+                 int64_t cap, int64_t* count_host, void* stream);
+
 /* ------------------------------------------------------------------------
  * 2. Counter RNG products (rng.py, engine.py:268-287, model.py:69-109)
  * --------------------------------------------------------------------- */
@@ -219,6 +235,25 @@ int hg_mg_build_group(const int64_t* offsets, const int32_t* targets, int64_t n_
                       int32_t roots_per_state, const hg_mg_layout* layout, int32_t* ws,
                       const hg_mg_batch* outs, int* err_flag, int32_t ctas_per_sm, void* stream);
 
+/* Kernel selection of hg_mg_build / _n / _group (process-wide): 0 (default)
+ * builds two-layer micrographs with hop-1 fanout <= 31 and <= 256 hop-2 pairs
+ * warp-per-root (8 roots per CTA, dynamic hop-2 task list), everything else
+ * CTA-per-root; 1 forces the CTA-per-root kernel.  Both are bit-exact with
+ * sampler.py:84-106 + model.py:183-198; the switch exists so the parity tests
+ * can compare them. */
+int hg_mg_build_mode(int32_t mode);
+
+
+/* Greedy locality partitioner (graph.py:273-327): BFS region growing into
+ * parts of <= cap vertices, seeds in seed_order (degree descending, id
+ * ascending), one warp running the reference's sequential order exactly.
+ * home int32[n] (-1 = leftover), queue int32[n] scratch. */
+int hg_partition_greedy(const int64_t* offsets, const int32_t* targets, int64_t n,
+                        int32_t n_servers, int64_t cap, const int64_t* seed_order,
+                        int32_t* home, int32_t* queue, void* stream);
+/* leftovers (home == -1) round-robin by their rank among leftovers */
+int hg_partition_leftovers(int32_t* home, int64_t n, int32_t n_servers, const int64_t* rank,
+                           void* stream);
 
 /* ------------------------------------------------------------------------
  * 5. Forward / backward of a micrograph batch (model.py:213-287) and the
@@ -294,6 +329,10 @@ typedef struct {
    * need-index pair lists (one L2-resident lookup per source row instead of
    * the home / staging-row lookups by vertex id).  NULL = by vertex id. */
   const int32_t* row_handle;
+  /* explicit class labels of the roots (int32[max_roots]); NULL = hashed by
+   * LabelOracle from label_state (model.py:93-109).  The per-micrograph
+   * loss_and_backward(state, label, model) API passes its label here. */
+  const int32_t* labels;
 } hg_step_desc;
 
 /* Peer memory (one process per GPU): device allocations whose CUDA IPC

@@ -70,7 +70,8 @@ class StepDesc(C.Structure):
                 ("agg1_ready", C.c_int32), ("WcT", C.c_void_p), ("Wcp", C.c_void_p),
                 ("dl_lowp", C.c_void_p), ("root_rows", C.c_int32 * 7),
                 ("lowp_fresh", C.c_int32), ("max_deg", C.c_int32 * 7),
-                ("lowp_layered", C.c_int32), ("row_handle", C.c_void_p)]
+                ("lowp_layered", C.c_int32), ("row_handle", C.c_void_p),
+                ("labels", C.c_void_p)]
 
 
 V, I32, I64, U64, SZ = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_size_t
@@ -98,11 +99,16 @@ SIGNATURES = {
     "hg_graph_canonicalize": [I64, I64, V, V, V, V, PSZ, V],
     "hg_graph_compact": [I64, I64, V, V, V, V, V],
     "hg_exclusive_scan_i64": [V, V, I64, V, PSZ, V],
+    "hg_pick_k_smallest": [V, I64, I64, U64, V, V],
+    "hg_sbm_edges": [V, I64, I32, U64, I32, U64, U64, V, V, I64, PI64, V],
+    "hg_partition_greedy": [V, V, I64, I32, I64, V, V, V, V],
+    "hg_partition_leftovers": [V, I64, I32, V, V],
     "hg_mg_plan_layout": [I32, C.POINTER(I32), C.POINTER(MgLayout)],
     "hg_mg_build": [V, V, I64, V, I32, V, I32, C.POINTER(MgLayout), V, C.POINTER(MgBatch),
                     V, V],
     "hg_mg_build_n": [V, V, I64, V, I32, V, V, I32, C.POINTER(MgLayout), V, C.POINTER(MgBatch),
                       V, V],
+    "hg_mg_build_mode": [I32],
     "hg_mg_build_group": [V, V, I64, V, I32, I32, V, V, I32, C.POINTER(MgLayout), V,
                           C.POINTER(MgBatch), V, I32, V],
     "hg_train_step": [C.POINTER(StepDesc), I32, V],

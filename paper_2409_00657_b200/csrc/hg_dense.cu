@@ -366,7 +366,8 @@ k_gemm(const TA* __restrict__ A, int lda, const float* __restrict__ B, int ldb, 
 // overwritten with dlogits = softmax - onehot(label).
 __global__ void k_softmax_ce(float* __restrict__ logits, int C, const int64_t* __restrict__ roots,
                              int n_roots, const int32_t* __restrict__ n_dev, uint64_t label_state,
-                             float* __restrict__ loss, bf16* __restrict__ dl_lowp, int ldp) {
+                             const int32_t* __restrict__ labels, float* __restrict__ loss,
+                             bf16* __restrict__ dl_lowp, int ldp) {
   pdl_trigger();
   pdl_wait();
   const int r = blockIdx.x * (blockDim.x / 32) + warp_id();
@@ -388,7 +389,7 @@ __global__ void k_softmax_ce(float* __restrict__ logits, int C, const int64_t* _
   for (int c = lane; c < C; c += 32) s += expf(x[c] - mx);
 #pragma unroll
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  const int label = (int)(mix64(label_state ^ (uint64_t)roots[r]) % (uint64_t)C);
+  const int label = labels ? labels[r] : (int)(mix64(label_state ^ (uint64_t)roots[r]) % (uint64_t)C);
   const float xl = x[label];
   __syncwarp();
   const float inv = 1.0f / s;
@@ -424,7 +425,8 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 k_head(const T* __restrict__ hL, const float* __restrict__ Wc, int H, int C,
        const int64_t* __restrict__ roots, int n_cap, const int32_t* __restrict__ n_dev,
-       uint64_t label_state, float* __restrict__ dlogits, float* __restrict__ loss,
+       uint64_t label_state, const int32_t* __restrict__ labels, float* __restrict__ dlogits,
+       float* __restrict__ loss,
        float* __restrict__ dz, bf16* __restrict__ dz_lowp, int cap_rows, float* __restrict__ gb,
        int backward) {
   extern __shared__ float sm[];
@@ -460,7 +462,8 @@ k_head(const T* __restrict__ hL, const float* __restrict__ Wc, int H, int C,
     for (int c = lane; c < C; c += 32) s += expf(dl[c] - mx);
 #pragma unroll
     for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    const int label = (int)(mix64(label_state ^ (uint64_t)roots[r]) % (uint64_t)C);
+    const int label = labels ? labels[r]
+                             : (int)(mix64(label_state ^ (uint64_t)roots[r]) % (uint64_t)C);
     __syncwarp();
     const float xl = dl[label];
     __syncwarp();
@@ -1064,7 +1067,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     }
     // root rows: n_roots is the capacity, the device count N_L the actual roots
     int st;
-    if (C <= 192 && fused_head_on()) {
+    if (C <= 192 && fused_head_on() && !d->labels) {
       st = umma_head_ce(d->h[L], H, d->WcT, H, d->logits, C, n_roots, H, tot + L, d->roots,
                         d->label_state, d->loss, (bf16*)d->dl_lowp, Cp, s);
       if (st) { join(); return st; }
@@ -1074,7 +1077,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     if (st) { join(); return st; }
     count_launch();
     launch_pdl(k_softmax_ce, dim3((n_roots + 7) / 8), dim3(256), 0, s, d->logits, C, d->roots, n_roots, tot + L,
-                                                   d->label_state, d->loss,
+                                                   d->label_state, d->labels, d->loss,
                                                    (bf16*)d->dl_lowp, Cp);
     }
     if (backward) {
@@ -1102,7 +1105,8 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     const int grid = std::max(1, std::min(num_sms(), (n_roots + 7) / 8));
     count_launch();
     k_head<T><<<grid, 256, smem, s>>>((const T*)d->h[L], d->Wc, H, C, d->roots, n_roots,
-                                      tot + L, d->label_state, d->logits, d->loss, d->dh[L],
+                                      tot + L, d->label_state, d->labels, d->logits, d->loss,
+                                      d->dh[L],
                                       tc ? dz_lowp(d, L) : nullptr, d->max_rows[L],
                                       d->gb[L], backward ? 1 : 0);
   }

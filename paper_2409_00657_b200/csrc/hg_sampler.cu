@@ -605,6 +605,263 @@ k_mg_build(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targ
   }
 }
 
+// ---------------------------------------------------------------- warp-per-root build (L = 2)
+//
+// Two-layer micrographs whose layers fit one warp (hop-1 fanout f1 <= 31,
+// f1 * f2 <= 256 hop-2 pairs): the configuration the benchmark trains.  A CTA
+// of 8 warps builds 8 roots, one warp each, with 3 block barriers per 8 roots
+// (the CTA-per-root kernel above pays ~20 per root, and its 8 warps wait at
+// every one for the slowest draw):
+//   P1  warp: root, key, hop-1 draw (threshold select) -- a hub root (degree
+//       > kWarpMaxDeg) is queued and drawn by the whole CTA;
+//       warp: sort-unique layer 1, row starts / degrees / pair offsets;
+//   P2  the CTA's hop-2 draws (<= 8 x 31 frontier vertices) as one task list
+//       pulled dynamically by the 8 warps (shared counter), so a root with
+//       heavy frontier vertices does not hold the other seven back; hub
+//       vertices are queued and drawn by the whole CTA afterwards;
+//   P3  warp: sort-unique layer 0 in registers, need sets by merge positions,
+//       in-layer flags, self / neighbour positions by binary search, the
+//       per-root workspace rows (same layout as build_root: k_mg_scan and
+//       k_mg_finalize are shared).
+// Bit-exact with build_root (tests/test_sampler_gpu.py compares both kernels
+// and the oracle).
+constexpr int kW2Roots = kBuildWarps;   // roots per CTA (one per warp)
+constexpr int kW2F1 = 31;               // max hop-1 fanout (need[1] <= 32 = one lane each)
+constexpr int kW2P2 = 256;              // max hop-2 pairs per root (warp_sort_unique<8>)
+constexpr int kWarpMaxDeg = 1024;       // larger rows are drawn by the whole CTA
+
+struct W2Slot {
+  uint64_t st1, st2;      // hop-1 / hop-2 states chain(key, 1), chain(key, 2)
+  int64_t lo1[32];        // CSR start of each layer-1 vertex
+  int flat1[32];          // hop-1 draws, slot order
+  int lay1[32];           // layers[1] (sorted unique)
+  int deg1[32];
+  int off1[33];           // hop-2 pair offsets per layer-1 vertex
+  int need1[32];
+  int mflag[33];          // merge prefix of need1 entries absent from layer 0
+  int flat2[kW2P2];       // hop-2 draws, frontier order
+  int lay0[kW2P2];        // layers[0]
+  int need0[kW2P2 + 33];  // need[0] = layers[0] U need[1]
+  int root, n_flat1, n_flat2, pad;
+};
+
+bool w2_eligible(const MgCarve& c) {
+  return c.L == 2 && c.fanout[0] <= kW2F1 && c.cap_lay[0] <= kW2P2;
+}
+
+size_t w2_smem(const MgCarve& c) {
+  return sizeof(W2Slot) * kW2Roots + (size_t)(kW2Roots + 1) * c.cand_cap * sizeof(uint64_t);
+}
+
+__device__ __forceinline__ int warp_incl_scan(int x) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  return x;
+}
+
+__global__ void __launch_bounds__(kBuildThreads, 4)
+k_mg_build_w2(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targets,
+              int64_t n_vertices, const int64_t* __restrict__ roots, int n_roots,
+              const uint64_t* __restrict__ iter_state, int roots_per_state, MgCarve c,
+              int32_t* __restrict__ ws, int* err, const int32_t* __restrict__ n_roots_dev,
+              int per_batch) {
+  extern __shared__ __align__(16) unsigned char w2raw[];
+  W2Slot* slots = reinterpret_cast<W2Slot*>(w2raw);
+  uint64_t* cand_base = reinterpret_cast<uint64_t*>(w2raw + sizeof(W2Slot) * kW2Roots);
+  __shared__ int nl1s[kW2Roots], hub1_list[kW2Roots], hub_list[kW2Roots * 32];
+  __shared__ int hub1_cnt, hub_cnt, task_ctr;
+  __shared__ int warp_ctr[kW2Roots + 1];
+  __shared__ uint64_t tslots[kW2Roots + 1];
+  const int w = warp_id(), lane = lane_id();
+  const unsigned full = 0xffffffffu;
+  W2Slot& S = slots[w];
+  const int f1 = c.fanout[0], f2 = c.fanout[1], m1 = c.mean[0], m2 = c.mean[1];
+  const int cap = c.cand_cap;
+  uint64_t* my_cand = cand_base + (size_t)w * cap;
+  uint64_t* cta_cand = cand_base + (size_t)kW2Roots * cap;
+  const int groups = (n_roots + kW2Roots - 1) / kW2Roots;
+  for (int gi = blockIdx.x; gi < groups; gi += gridDim.x) {
+    const int r = gi * kW2Roots + w;
+    if (threadIdx.x == 0) { hub1_cnt = 0; hub_cnt = 0; task_ctr = 0; }
+    __syncthreads();  // counters reset; the previous group's slots are free
+    const bool in_range = r < n_roots;
+    const bool empty = in_range && n_roots_dev && r % per_batch >= n_roots_dev[r / per_batch];
+    const bool live = in_range && !empty;
+    int32_t* wr = ws + (size_t)r * c.ws_root_ints;
+    if (empty && lane <= 4) wr[c.ws_cnt + lane] = 0;  // an empty micrograph (2L+1 counts)
+    // ---- P1: hop-1 draw of the root
+    if (live) {
+      int64_t root = roots[r];
+      if (root < 0 || root >= n_vertices) {
+        if (lane == 0) raise_flag(err, HG_ERANGE);
+        root = 0;
+      }
+      // roots_per_state == 0: iter_state already holds one final stream key per root
+      const uint64_t key = roots_per_state > 0
+                               ? mix64(iter_state[r / roots_per_state] ^ (uint64_t)root)
+                               : iter_state[r];
+      const uint64_t k1 = mix64(key);
+      const uint64_t st1 = mix64(k1 ^ 1ull);
+      const int64_t lo = offsets[root];
+      const int d = (int)(offsets[root + 1] - lo);
+      if (lane == 0) {
+        S.st1 = st1;
+        S.st2 = mix64(k1 ^ 2ull);
+        S.root = (int)root;
+        S.n_flat1 = d <= f1 ? d : f1;
+      }
+      if (d <= f1) {
+        for (int j = lane; j < d; j += 32) S.flat1[j] = targets[lo + j];
+      } else if (d <= kWarpMaxDeg) {
+        team_select<WarpTeam>(targets, lo, d, f1, m1, mix64(st1 ^ (uint64_t)root), S.flat1,
+                              my_cand, cap, warp_ctr + w, tslots + w, err);
+      } else if (lane == 0) {
+        hub1_list[atomicAdd(&hub1_cnt, 1)] = w;
+      }
+    }
+    __syncthreads();
+    const int nh1 = hub1_cnt;
+    for (int q = 0; q < nh1; ++q) {  // hub roots: the whole CTA draws
+      W2Slot& H = slots[hub1_list[q]];
+      const int64_t rt = H.root;
+      const int64_t lo = offsets[rt];
+      team_select<BlockTeam>(targets, lo, (int)(offsets[rt + 1] - lo), f1, m1,
+                             mix64(H.st1 ^ (uint64_t)rt), H.flat1, cta_cand, cap,
+                             warp_ctr + kW2Roots, tslots + kW2Roots, err);
+    }
+    // layer 1, its rows and the hop-2 pair offsets
+    int nl1 = 0;
+    if (live) {
+      __syncwarp();
+      nl1 = warp_sort_unique<1>(S.flat1, S.n_flat1, S.lay1);
+      __syncwarp();
+      int cnt = 0;
+      if (lane < nl1) {
+        const int v = S.lay1[lane];
+        const int64_t lo = offsets[v];
+        const int d = (int)(offsets[v + 1] - lo);
+        S.lo1[lane] = lo;
+        S.deg1[lane] = d;
+        cnt = d <= f2 ? d : f2;
+      }
+      const int incl = warp_incl_scan(cnt);
+      S.off1[lane] = incl - cnt;
+      if (lane == 31) { S.off1[32] = incl; S.n_flat2 = incl; }
+    }
+    if (lane == 0) nl1s[w] = nl1;
+    __syncthreads();
+    // ---- P2: the CTA's hop-2 draws, pulled dynamically by its warps
+    const int nb = lane < kW2Roots ? nl1s[lane] : 0;
+    const int incl_b = warp_incl_scan(nb);
+    const int excl_b = incl_b - nb;
+    const int n_tasks = __shfl_sync(full, incl_b, kW2Roots - 1);
+    for (;;) {
+      int t = 0;
+      if (lane == 0) t = atomicAdd(&task_ctr, 1);
+      t = __shfl_sync(full, t, 0);
+      if (t >= n_tasks) break;
+      const unsigned bm = __ballot_sync(full, lane < kW2Roots && excl_b <= t);
+      const int ow = 31 - __clz(bm);
+      const int i = t - __shfl_sync(full, excl_b, ow);
+      W2Slot& Q = slots[ow];
+      const int d = Q.deg1[i];
+      int32_t* out = Q.flat2 + Q.off1[i];
+      if (d <= f2) {
+        const int64_t lo = Q.lo1[i];
+        for (int j = lane; j < d; j += 32) out[j] = targets[lo + j];
+      } else if (d <= kWarpMaxDeg) {
+        team_select<WarpTeam>(targets, Q.lo1[i], d, f2, m2,
+                              mix64(Q.st2 ^ (uint64_t)Q.lay1[i]), out, my_cand, cap,
+                              warp_ctr + w, tslots + w, err);
+      } else if (lane == 0) {
+        hub_list[atomicAdd(&hub_cnt, 1)] = t;
+      }
+    }
+    __syncthreads();
+    const int nh = hub_cnt;
+    for (int q = 0; q < nh; ++q) {  // hub frontier vertices: the whole CTA draws
+      const int t = hub_list[q];
+      int ow = 0, base = 0;
+      while (base + nl1s[ow] <= t) base += nl1s[ow++];
+      W2Slot& Q = slots[ow];
+      const int i = t - base;
+      team_select<BlockTeam>(targets, Q.lo1[i], Q.deg1[i], f2, m2,
+                             mix64(Q.st2 ^ (uint64_t)Q.lay1[i]), Q.flat2 + Q.off1[i], cta_cand,
+                             cap, warp_ctr + kW2Roots, tslots + kW2Roots, err);
+    }
+    if (!live) continue;
+    // ---- P3: layer 0, need sets, plan, workspace rows (warp only)
+    __syncwarp();
+    const int T = S.n_flat2, T1 = S.n_flat1;
+    const int nl0 = warp_sort_unique<8>(S.flat2, T, S.lay0);
+    const int rt = S.root;
+    // need[1] = layers[1] U {root}
+    const int p = lower_bound(S.lay1, nl1, rt);
+    const bool rin = p < nl1 && S.lay1[p] == rt;
+    const int nn1 = nl1 + (rin ? 0 : 1);
+    if (lane < nn1) S.need1[lane] = rin ? S.lay1[lane] : (lane < p ? S.lay1[lane] : lane == p ? rt : S.lay1[lane - 1]);
+    __syncwarp();
+    // need[0] = layers[0] U need[1] by merge positions (need[1] entries not in layers[0] inserted)
+    int nd = 0;
+    if (lane < nn1) {
+      const int x = S.need1[lane];
+      const int q = lower_bound(S.lay0, nl0, x);
+      nd = (q < nl0 && S.lay0[q] == x) ? 0 : 1;
+    }
+    const int incl_nd = warp_incl_scan(nd);
+    if (lane < nn1) S.mflag[lane] = incl_nd - nd;
+    const int tb = __shfl_sync(full, incl_nd, 31);
+    if (lane == 0) S.mflag[nn1] = tb;
+    __syncwarp();
+    const int nn0 = nl0 + tb;
+    int32_t* need0_ws = wr + c.ws_need[0];
+    int32_t* inl0_ws = wr + c.ws_inl[0];
+    for (int a = lane; a < nl0; a += 32) {
+      const int x = S.lay0[a];
+      const int pos = a + S.mflag[lower_bound(S.need1, nn1, x)];
+      S.need0[pos] = x;
+      need0_ws[pos] = x;
+      inl0_ws[pos] = 1;
+    }
+    if (nd) {
+      const int x = S.need1[lane];
+      const int pos = S.mflag[lane] + lower_bound(S.lay0, nl0, x);
+      S.need0[pos] = x;
+      need0_ws[pos] = x;
+      inl0_ws[pos] = 0;
+    }
+    __syncwarp();
+    // layer 1 rows: need[1], in-layer, self positions in need[0], pair ranges
+    if (lane < nn1) {
+      const int x = S.need1[lane];
+      wr[c.ws_need[1] + lane] = x;
+      wr[c.ws_inl[1] + lane] = (rin || lane != p) ? 1 : 0;
+      wr[c.ws_self[1] + lane] = lower_bound(S.need0, nn0, x);
+      wr[c.ws_rowoff[1] + lane] = S.off1[lower_bound(S.lay1, nl1, x)];
+    }
+    if (lane == 0) {
+      wr[c.ws_rowoff[1] + nn1] = T;
+      // layer 2 = [root]: need, in-layer, self position in need[1], hop-1 pair range
+      wr[c.ws_need[2]] = rt;
+      wr[c.ws_inl[2]] = 1;
+      wr[c.ws_self[2]] = p;  // lower_bound(need[1], root)
+      wr[c.ws_rowoff[2]] = 0;
+      wr[c.ws_rowoff[2] + 1] = T1;
+      wr[c.ws_cnt + 0] = nn0;
+      wr[c.ws_cnt + 1] = nn1;
+      wr[c.ws_cnt + 2] = 1;
+      wr[c.ws_cnt + 3] = T;   // pairs of layer 1 (hop 2)
+      wr[c.ws_cnt + 4] = T1;  // pairs of layer 2 (hop 1)
+    }
+    for (int t = lane; t < T; t += 32) wr[c.ws_nbr[1] + t] = lower_bound(S.need0, nn0, S.flat2[t]);
+    if (lane < T1) wr[c.ws_nbr[2] + lane] = lower_bound(S.need1, nn1, S.flat1[lane]);
+  }
+}
+
 // Exclusive scans of the per-root counts (one CTA).  cols 0..L: need sizes,
 // cols L+1..2L: pair counts of layers 1..L.  Every count is loaded up front
 // (one strided gather in flight per thread and column) so the per-column
@@ -767,6 +1024,11 @@ extern "C" int hg_mg_build(const int64_t* offsets, const int32_t* targets, int64
                        roots_per_state, layout, ws, out, err_flag, stream);
 }
 
+// 0: the warp-per-root build wherever it applies (w2_eligible), else the CTA-per-root
+// build; 1: always the CTA-per-root build (hg_mg_build_mode, used by the parity tests
+// that compare the two kernels)
+static int g_build_mode = 0;
+
 static int build_group(const int64_t* offsets, const int32_t* targets, int64_t n_vertices,
                        const int64_t* roots, int32_t n_roots, int32_t n_batches,
                        const int32_t* n_roots_dev, const uint64_t* iter_state,
@@ -799,9 +1061,18 @@ static int build_group(const int64_t* offsets, const int32_t* targets, int64_t n
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     grid = std::min(total, nsm * cps);
   }
-  k_mg_build<<<grid, kBuildThreads, c.smem_bytes, s>>>(offsets, targets, n_vertices, roots, total,
-                                                        iter_state, roots_per_state, c, ws,
-                                                        err_flag, n_roots_dev, n_roots);
+  if (w2_eligible(c) && g_build_mode != 1) {
+    const int w2s = (int)w2_smem(c);
+    HG_CUDA_TRY(cudaFuncSetAttribute(k_mg_build_w2, cudaFuncAttributeMaxDynamicSharedMemorySize, w2s));
+    const int groups = (total + kW2Roots - 1) / kW2Roots;
+    k_mg_build_w2<<<std::min(grid, groups), kBuildThreads, w2s, s>>>(
+        offsets, targets, n_vertices, roots, total, iter_state, roots_per_state, c, ws, err_flag,
+        n_roots_dev, n_roots);
+  } else {
+    k_mg_build<<<grid, kBuildThreads, c.smem_bytes, s>>>(offsets, targets, n_vertices, roots,
+                                                          total, iter_state, roots_per_state, c,
+                                                          ws, err_flag, n_roots_dev, n_roots);
+  }
   HG_CUDA_TRY(cudaGetLastError());
   k_mg_scan<<<n_batches, 1024, 0, s>>>(ws, n_roots, c, o);
   HG_CUDA_TRY(cudaGetLastError());
@@ -830,6 +1101,12 @@ extern "C" int hg_mg_build_group(const int64_t* offsets, const int32_t* targets,
   return build_group(offsets, targets, n_vertices, roots, n_roots, n_batches, n_roots_dev,
                      iter_state, roots_per_state, layout, ws, outs, err_flag, ctas_per_sm,
                      stream);
+}
+
+extern "C" int hg_mg_build_mode(int32_t mode) {
+  if (mode < 0 || mode > 1) return hg_fail(HG_ERANGE, "build mode must be 0 (auto) or 1 (CTA per root)");
+  g_build_mode = mode;
+  return HG_OK;
 }
 
 extern "C" int hg_sample_frontier(const int64_t* offsets, const int32_t* targets,

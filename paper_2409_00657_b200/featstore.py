@@ -9,6 +9,7 @@ really moved (bf16 rows, real hop payloads).
 """
 from __future__ import annotations
 
+import struct
 from dataclasses import dataclass
 
 import numpy as np
@@ -98,6 +99,32 @@ class FetchStats:
         self.transferred += other.transferred
 
 
+_FEAT_MAGIC = b"FEAT"
+
+
+def write_feature_file(matrix, path) -> None:
+    """magic "FEAT", little-endian u64 n and dim, n*dim f32 row-major
+    (featstore.py:187-193)."""
+    matrix = np.ascontiguousarray(matrix, dtype="<f4")
+    with open(path, "wb") as f:
+        f.write(_FEAT_MAGIC)
+        f.write(struct.pack("<QQ", matrix.shape[0], matrix.shape[1]))
+        f.write(matrix.tobytes())
+
+
+def read_feature_file(path) -> np.ndarray:
+    """Inverse of write_feature_file (featstore.py:196-205), same errors."""
+    with open(path, "rb") as f:
+        magic = f.read(4)
+        if magic != _FEAT_MAGIC:
+            raise ValueError(f"bad magic {magic!r}, expected {_FEAT_MAGIC!r}")
+        n, dim = struct.unpack("<QQ", f.read(16))
+        data = np.frombuffer(f.read(4 * n * dim), dtype="<f4")
+        if len(data) != n * dim:
+            raise ValueError("feature file truncated")
+    return data.reshape(n, dim).astype(np.float32)
+
+
 class FeatureTable:
     """Rows of the feature matrix resident in HBM.
 
@@ -136,6 +163,19 @@ class FeatureTable:
         t = cls(n_vertices, dim, dtype, device, ld)
         t.fill_generated(0, n_vertices, feature_state(seed))
         return t
+
+    @classmethod
+    def from_matrix(cls, matrix, dtype=torch.float32, device="cuda", ld=None) -> "FeatureTable":
+        """A loaded feature matrix (read_feature_file; featstore.py:161-184
+        source="file") uploaded to HBM, rows padded to ld."""
+        m = torch.as_tensor(np.ascontiguousarray(matrix, dtype=np.float32))
+        t = cls(m.shape[0], m.shape[1], dtype, device, ld)
+        t.table[:, :t.dim].copy_(m.to(device=t.device, dtype=dtype))
+        return t
+
+    @classmethod
+    def from_file(cls, path, dtype=torch.float32, device="cuda", ld=None) -> "FeatureTable":
+        return cls.from_matrix(read_feature_file(path), dtype, device, ld)
 
     def rows(self, ids) -> np.ndarray:
         ids = torch.as_tensor(np.asarray(ids, dtype=np.int64), device=self.device)

@@ -20,6 +20,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from .errors import EdgeListError
 from .rng import chain, hash_vec
 
 _CSR_MAGIC = b"CSR1"
@@ -236,10 +237,160 @@ class PartitionMap:
         return np.bincount(self.home, minlength=self.n_servers)
 
 
-def partition_hash(n_vertices: int, n_servers: int, seed: int) -> PartitionMap:
-    """home(v) = chain(seed, 0xA7, v) mod S (graph.py:265-270)."""
-    h = hash_vec(chain(seed, 0xA7), np.arange(n_vertices, dtype=np.int64))
+def partition_hash(g, n_servers: int, seed: int) -> PartitionMap:
+    """home(v) = chain(seed, 0xA7, v) mod S (graph.py:265-270).  g: a Graph (the
+    reference signature) or a vertex count."""
+    if n_servers < 1:
+        raise ValueError("n_servers must be >= 1")
+    n = g.n_vertices if hasattr(g, "n_vertices") else int(g)
+    h = hash_vec(chain(seed, 0xA7), np.arange(n, dtype=np.int64))
     return PartitionMap((h % np.uint64(n_servers)).astype(np.int64), n_servers)
+
+
+def partition_greedy_locality(g: "Graph", n_servers: int, slack: float = 0.0,
+                              seed: int = 0) -> PartitionMap:
+    """BFS region growing into size-capped parts (graph.py:273-327) on the GPU
+    (csrc/hg_partition.cu): seeds by degree descending / id ascending, cap
+    ceil((1 + slack) n / S); identical homes to the reference.  The seed
+    argument is unused, as in the reference."""
+    if n_servers < 1:
+        raise ValueError("n_servers must be >= 1")
+    if slack < 0:
+        raise ValueError("slack must be >= 0")
+    n = g.n_vertices
+    cap = max(1, int(np.ceil((1.0 + slack) * n / n_servers)))
+    dev = g.device
+    home = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    if n:
+        # degree-descending, id-ascending seed order (graph.py:300): stable sort of -deg
+        order = torch.argsort(-g.degrees(), stable=True)
+        queue = torch.empty(n, dtype=torch.int32, device=dev)
+        s = torch.cuda.current_stream(dev).cuda_stream
+        _lib.call("hg_partition_greedy", g.offsets.data_ptr(), g.targets.data_ptr(), n,
+                  n_servers, cap, order.data_ptr(), home.data_ptr(), queue.data_ptr(), s)
+        left = home[:n] == -1
+        if bool(left.any()):
+            rank = torch.cumsum(left.to(torch.int64), 0) - 1
+            _lib.call("hg_partition_leftovers", home.data_ptr(), n, n_servers, rank.data_ptr(), s)
+    return PartitionMap(home[:n].cpu().numpy().astype(np.int64), n_servers, dev)
+
+
+def save_partition(p: PartitionMap, path) -> None:
+    """ASCII lines "vertex_id server_id" (graph.py:239-244)."""
+    with open(path, "w", encoding="ascii") as f:
+        f.write("".join(f"{v} {s}\n" for v, s in enumerate(p.home.tolist())))
+
+
+def load_partition(path, n_servers: int = None) -> PartitionMap:
+    """Inverse of save_partition (graph.py:247-262): '#' comments and blank lines
+    skipped, every vertex 0..n-1 exactly once."""
+    pairs = {}
+    with open(path, "r", encoding="ascii") as f:
+        for lineno, raw in enumerate(f, start=1):
+            line = raw.strip()
+            if not line or line.startswith("#"):
+                continue
+            parts = line.split()
+            if len(parts) != 2:
+                raise EdgeListError(f"line {lineno}: expected 'vertex server'")
+            pairs[int(parts[0])] = int(parts[1])
+    n = max(pairs) + 1 if pairs else 0
+    if len(pairs) != n:
+        raise ValueError("partition file must cover vertices 0..n-1 exactly")
+    home = np.array([pairs[v] for v in range(n)], dtype=np.int64)
+    servers = n_servers if n_servers is not None else (int(home.max()) + 1 if n else 1)
+    return PartitionMap(home, servers)
+
+
+def from_pairs(n_vertices: int, us, vs, symmetrize: bool = True, drop_self_loops: bool = True,
+               device="cuda") -> "Graph":
+    """Canonical CSR from edge endpoints (graph.py:77-99), built on the device:
+    duplicates collapse, self-loops dropped unless kept, both directions when
+    symmetrize."""
+    dev = torch.device(device)
+    u = torch.as_tensor(np.asarray(us, dtype=np.int64), device=dev)
+    v = torch.as_tensor(np.asarray(vs, dtype=np.int64), device=dev)
+    if drop_self_loops:
+        keep = u != v
+        u, v = u[keep], v[keep]
+    if symmetrize:
+        u, v = torch.cat([u, v]), torch.cat([v, u])
+    n = int(n_vertices)
+    if u.numel():
+        code = torch.unique(u * n + v)  # sorted: row-major, targets ascending per row
+        u, v = code // n, code % n
+    counts = torch.bincount(u, minlength=n) if n else torch.zeros(0, dtype=torch.int64,
+                                                                  device=dev)
+    offsets = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(counts, 0, out=offsets[1:])
+    if n >= 2 ** 31:
+        raise ValueError("vertex ids must fit int32 on the device")
+    return Graph(n, offsets, v.to(torch.int32), directed=not symmetrize)
+
+
+def load_edge_list(source, n_vertices: int = None, device="cuda") -> "Graph":
+    """"u v" lines -> undirected canonical CSR (graph.py:110-143), same errors."""
+    if not hasattr(source, "read"):
+        with open(source, "r", encoding="ascii") as f:
+            return load_edge_list(f, n_vertices, device)
+    us, vs, max_id = [], [], -1
+    for lineno, raw in enumerate(source, start=1):
+        line = raw.strip()
+        if not line or line.startswith("#"):
+            continue
+        parts = line.split()
+        if len(parts) != 2:
+            raise EdgeListError(f"line {lineno}: expected 'u v', got {line!r}")
+        try:
+            u, v = int(parts[0]), int(parts[1])
+        except ValueError:
+            raise EdgeListError(f"line {lineno}: non-integer vertex id in {line!r}") from None
+        if u < 0 or v < 0:
+            raise EdgeListError(f"line {lineno}: negative vertex id in {line!r}")
+        if n_vertices is not None and (u >= n_vertices or v >= n_vertices):
+            raise EdgeListError(f"line {lineno}: vertex id >= declared {n_vertices}")
+        max_id = max(max_id, u, v)
+        us.append(u)
+        vs.append(v)
+    n = n_vertices if n_vertices is not None else max_id + 1
+    return from_pairs(max(n, 0), np.array(us, dtype=np.int64), np.array(vs, dtype=np.int64),
+                      device=device)
+
+
+@dataclass(frozen=True)
+class SbmSpec:
+    """Stochastic block model (graph.py:173-191): blocks of consecutive ids."""
+
+    block_sizes: tuple
+    p_in: float
+    p_out: float
+    seed: int
+
+    def __post_init__(self):
+        object.__setattr__(self, "block_sizes", tuple(int(b) for b in self.block_sizes))
+        if any(b < 1 for b in self.block_sizes):
+            raise ValueError("block sizes must be >= 1")
+        if not (0.0 <= self.p_out <= self.p_in <= 1.0):
+            raise ValueError("need 0 <= p_out <= p_in <= 1")
+
+    @property
+    def n_vertices(self) -> int:
+        return sum(self.block_sizes)
+
+
+def generate_sbm(spec: SbmSpec, device="cuda") -> "Graph":
+    """Every unordered pair sampled once (graph.py:194-209): the pair pass is the
+    CUDA sbm_edges (kernels.sbm_edges), the CSR is built by from_pairs."""
+    from .kernels import probability_threshold, sbm_edges
+    if not spec.block_sizes:
+        raise ValueError("empty SBM spec: no blocks")
+    block_of = np.repeat(np.arange(len(spec.block_sizes), dtype=np.int64),
+                         np.array(spec.block_sizes, dtype=np.int64))
+    mi, ti = probability_threshold(spec.p_in)
+    mo, to = probability_threshold(spec.p_out)
+    us, vs = sbm_edges(torch.as_tensor(block_of, device=device), mi, ti, mo, to,
+                       chain(spec.seed, 0x5B))
+    return from_pairs(spec.n_vertices, us, vs, device=device)
 
 
 def partition_planted(spec: GraphSpec, n_servers: int) -> PartitionMap:

@@ -23,10 +23,40 @@ def _dev(x, dtype, device="cuda"):
     return torch.as_tensor(np.ascontiguousarray(x), dtype=dtype, device=device)
 
 
+# Device copies of host CSR arrays, keyed by the arrays' buffers: the
+# reference calls sample_frontier once per hop per root with the same
+# Graph.offsets / Graph.targets (frozen, sampler.py:97), so the CSR is uploaded
+# once, not per call.  The cache holds a reference to each host array (its
+# buffer cannot be freed and reused while cached); entries for arrays whose
+# CONTENTS change in place would go stale -- the reference never mutates them.
+_CSR_CACHE: dict = {}
+_CSR_CACHE_MAX = 4
+
+
+def _host_key(a):
+    if isinstance(a, np.ndarray):
+        return (a.__array_interface__["data"][0], a.shape, a.dtype.str, a.strides)
+    return None
+
+
+def _cached_csr(offsets, targets):
+    ko, kt = _host_key(offsets), _host_key(targets)
+    if ko is None or kt is None:  # device tensors (or lists): used / converted directly
+        return _dev(offsets, torch.int64), _dev(targets, torch.int32)
+    key = (ko, kt)
+    hit = _CSR_CACHE.get(key)
+    if hit is not None:
+        return hit[0], hit[1]
+    off, tgt = _dev(offsets, torch.int64), _dev(targets, torch.int32)
+    if len(_CSR_CACHE) >= _CSR_CACHE_MAX:
+        _CSR_CACHE.pop(next(iter(_CSR_CACHE)))
+    _CSR_CACHE[key] = (off, tgt, offsets, targets)
+    return off, tgt
+
+
 def sample_frontier(offsets, targets, frontier, fanout: int, state: int):
     """(counts, flat) for one frontier (_kernels_nb.py:55-90)."""
-    off = _dev(offsets, torch.int64)
-    tgt = _dev(targets, torch.int32)
+    off, tgt = _cached_csr(offsets, targets)
     fr = _dev(frontier, torch.int64)
     n = off.numel() - 1
     f = fr.numel()
@@ -49,6 +79,37 @@ def feature_rows(ids, dim: int, state: int) -> np.ndarray:
     _lib.call("hg_feature_rows", idt.data_ptr(), idt.numel(), int(dim),
               int(state) & ((1 << 64) - 1), out.data_ptr(), stream)
     return out.cpu().numpy()
+
+
+def pick_k_smallest(ids, k: int, state: int) -> np.ndarray:
+    """k of the (sorted unique) ids by smallest keyed hash, in index order
+    (_kernels_nb.py:92-106); the layer-wise sampler's shared draw."""
+    idt = _dev(ids, torch.int64)
+    n = idt.numel()
+    if k < 0:
+        raise ValueError("k must be >= 0")
+    out = torch.empty(max(min(int(k), n), 1), dtype=torch.int64, device=idt.device)
+    stream = torch.cuda.current_stream(idt.device).cuda_stream
+    _lib.call("hg_pick_k_smallest", idt.data_ptr(), n, int(k), int(state) & ((1 << 64) - 1),
+              out.data_ptr(), stream)
+    return out[:min(int(k), n)].cpu().numpy()
+
+
+def sbm_edges(block_of, mode_in: int, thr_in: int, mode_out: int, thr_out: int, state: int):
+    """(us, vs), every accepted unordered pair u < v once (_kernels_nb.py:22-52)."""
+    b = _dev(block_of, torch.int64)
+    n = b.numel()
+    stream = torch.cuda.current_stream(b.device).cuda_stream
+    cnt = C.c_int64(0)
+    m64 = (1 << 64) - 1
+    args = (b.data_ptr(), n, int(mode_in), int(thr_in) & m64, int(mode_out), int(thr_out) & m64,
+            int(state) & m64)
+    _lib.call("hg_sbm_edges", *args, None, None, 0, C.byref(cnt), stream)
+    m = cnt.value
+    us = torch.empty(max(m, 1), dtype=torch.int64, device=b.device)
+    vs = torch.empty(max(m, 1), dtype=torch.int64, device=b.device)
+    _lib.call("hg_sbm_edges", *args, us.data_ptr(), vs.data_ptr(), m, C.byref(cnt), stream)
+    return us[:m].cpu().numpy(), vs[:m].cpu().numpy()
 
 
 def probability_threshold(p: float):

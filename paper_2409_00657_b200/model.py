@@ -117,15 +117,18 @@ class ModelState:
             return np.concatenate([np.arange(self.D), self.Dp + np.arange(self.D)])
         return np.arange(self.D)
 
-    def load_reference(self, weights, biases, classifier) -> None:
-        """Set parameters from reference-layout arrays (float64 ok)."""
-        self.flat.zero_()
+    def load_reference(self, weights, biases, classifier, buf=None) -> None:
+        """Set parameters (or, buf=self.grad, the accumulator) from
+        reference-layout arrays (float64 ok)."""
+        dst = self.flat if buf is None else buf
+        dst.zero_()
         for k in range(1, self.L + 1):
             w = torch.as_tensor(np.asarray(weights[k - 1]), dtype=torch.float32)
-            self.W(k)[torch.as_tensor(self._ref_rows(k))] = w.to(self.device)
-            self.b(k).copy_(torch.as_tensor(np.asarray(biases[k - 1]), dtype=torch.float32))
-        self.Wc().copy_(torch.as_tensor(np.asarray(classifier), dtype=torch.float32))
-        self.refresh_shadow()
+            self.W(k, dst)[torch.as_tensor(self._ref_rows(k))] = w.to(self.device)
+            self.b(k, dst).copy_(torch.as_tensor(np.asarray(biases[k - 1]), dtype=torch.float32))
+        self.Wc(dst).copy_(torch.as_tensor(np.asarray(classifier), dtype=torch.float32))
+        if buf is None:
+            self.refresh_shadow()
 
     def reference_arrays(self, buf=None):
         """(weights, biases, classifier) as float64 numpy in reference layout."""

@@ -171,3 +171,126 @@ def test_glorot_matches_oracle(P):
     for rows, cols, st in ((256, 256, chain(3, 0x11, 0)), (7, 5, 99)):
         w = glorot_device(rows, cols, st, torch.float64).cpu().numpy()
         assert np.array_equal(w, OM.glorot(rows, cols, st))
+
+
+# ---------------------------------------------------------------- build kernels
+# Two-layer micrographs with f1 <= 31 and f1*f2 <= 256 are built warp-per-root
+# (k_mg_build_w2); hg_mg_build_mode(1) forces the CTA-per-root kernel.  Both
+# must agree with each other and with the oracle, including hub rows above the
+# warp draw limit (1024), self-loops (root inside its own layer 1), isolated
+# roots, device root counts (empty micrographs) and the persistent grid.
+
+def _build_both(G, fo, roots, state, n_dev=None, ctas_per_sm=0):
+    from paper_2409_00657_b200 import _lib
+    from paper_2409_00657_b200.sampler import GroupBuilder, MicrographBatch, MicrographBuilder
+    out = []
+    for mode in (0, 1):
+        _lib.call("hg_mg_build_mode", mode)
+        try:
+            R = len(roots) // 2
+            bs = [MicrographBuilder(fo, R) for _ in range(2)]
+            gb = GroupBuilder(bs)
+            gb.roots.copy_(torch.from_numpy(roots).cuda())
+            gb.keys.copy_(torch.tensor(np.array([state, chain(state, 1)], dtype=np.uint64)
+                                       .view(np.int64), device="cuda"))
+            if n_dev is not None:
+                gb.n_dev.copy_(torch.tensor(n_dev, dtype=torch.int32))
+            gb.build(G, n_dev=gb.n_dev.data_ptr() if n_dev is not None else None,
+                     ctas_per_sm=ctas_per_sm)
+            torch.cuda.synchronize()
+            gb.check()
+            out.append([(b.tensors, MicrographBatch(len(fo), R, b.tensors)) for b in bs])
+        finally:
+            _lib.call("hg_mg_build_mode", 0)
+    return out
+
+
+@pytest.mark.parametrize("fo", [(15, 10), (10, 5), (25, 10), (31, 8), (1, 200), (3, 1)])
+@pytest.mark.parametrize("cps", [0, 3])
+def test_warp_build_matches_cta_build_and_oracle(P, fo, cps):
+    from paper_2409_00657_b200.graph import GraphSpec, generate
+    kw = SPECS[1]  # rows up to 5000: hop-1 and hop-2 hubs above the warp limit
+    G = generate(GraphSpec(**kw))
+    off, tgt = G.to_host()
+    deg = np.diff(off)
+    rng = np.random.default_rng(3)
+    roots = np.concatenate([np.argsort(-deg)[:24], rng.integers(0, kw["n"], 176)]).astype(np.int64)
+    rng.shuffle(roots)
+    state = chain(chain(5, 0x06), 0, 9)
+    fast, legacy = _build_both(G, fo, roots, state, ctas_per_sm=cps)
+    R = len(roots) // 2
+    for b in range(2):
+        (tf, bf), (tl, bl) = fast[b], legacy[b]
+        assert torch.equal(tf["totals"], tl["totals"])
+        hf, hl = bf.to_host(), bl.to_host()
+        for name in ("need_off", "pair_off"):
+            for k in range(len(fo) + 1):
+                if hf[name][k] is not None:
+                    assert np.array_equal(hf[name][k], hl[name][k]), (name, k)
+        tot = tf["totals"].cpu().numpy()
+        L = len(fo)
+        for k in range(L + 1):
+            n = int(tot[k])
+            assert np.array_equal(hf["need_ids"][k][:n], hl["need_ids"][k][:n]), ("need", k)
+            assert np.array_equal(hf["in_layer"][k][:n], hl["in_layer"][k][:n]), ("inl", k)
+            if k:
+                p = int(tot[L + k])
+                assert np.array_equal(hf["self_pos"][k][:n], hl["self_pos"][k][:n])
+                assert np.array_equal(hf["nbr_off"][k][:n + 1], hl["nbr_off"][k][:n + 1])
+                assert np.array_equal(hf["nbr_idx"][k][:p], hl["nbr_idx"][k][:p])
+        st = state if b == 0 else chain(state, 1)
+        rb = roots[b * R:(b + 1) * R]
+        for r, m in zip(rb.tolist(), bf.micrographs(rb, hf)):
+            want = o_sample(off, tgt, r, fo, chain(st, r), draw=OK.sample_frontier_nb)
+            assert all(np.array_equal(a, w) for a, w in zip(m.layers, want.layers))
+            assert all(np.array_equal(d1, d2) and np.array_equal(s1, s2)
+                       for (d1, s1), (d2, s2) in zip(m.pairs, want.pairs))
+            assert np.array_equal(m.vertices, want.vertices)
+
+
+def test_warp_build_self_loops_isolated_and_device_counts(P):
+    """Self-loops put the root into its own layer 1 (need[1] == layer 1),
+    isolated roots give |V| = 1, and batch slots past the device root count
+    come out as empty micrographs -- the same in both kernels."""
+    from paper_2409_00657_b200.graph import Graph
+    rng = np.random.default_rng(11)
+    n = 300
+    rows = []
+    for v in range(n):
+        if v % 17 == 0:
+            rows.append(np.empty(0, np.int64))           # isolated
+            continue
+        d = int(rng.integers(1, 60 if v % 5 else 1500))
+        r = np.unique(rng.integers(0, n, d))
+        if v % 3 == 0:
+            r = np.union1d(r, [v])                        # self-loop
+        rows.append(r)
+    off = np.zeros(n + 1, np.int64)
+    np.cumsum([len(r) for r in rows], out=off[1:])
+    tgt = np.concatenate(rows)
+    G = Graph.from_host(off, tgt)
+    roots = rng.integers(0, n, 128).astype(np.int64)
+    roots[:8] = np.arange(0, 8 * 17, 17)                  # isolated roots
+    fo = (15, 10)
+    state = chain(3, 4)
+    fast, legacy = _build_both(G, fo, roots, state, n_dev=[64, 37])
+    for b, cnt in ((0, 64), (1, 37)):
+        tf, tl = fast[b][0], legacy[b][0]
+        assert torch.equal(tf["totals"], tl["totals"])
+        for name in ("need_ids", "in_layer", "self_pos", "nbr_idx"):
+            for k in range(3):
+                x, y = tf[name][k], tl[name][k]
+                if x is None:
+                    continue
+                n_ = int(tf["totals"][k]) if name != "nbr_idx" else int(tf["totals"][2 + k])
+                assert torch.equal(x[:n_], y[:n_]), (b, name, k)
+        bf = fast[b][1]
+        rb = roots[b * 64:b * 64 + cnt]
+        got = bf.micrographs(rb)
+        for r, m in zip(rb.tolist(), got):
+            want = o_sample(off, tgt, r, fo, chain(state if b == 0 else chain(state, 1), r))
+            assert all(np.array_equal(a, w) for a, w in zip(m.layers, want.layers))
+            assert np.array_equal(m.vertices, want.vertices)
+        # slots past the device count: empty micrographs
+        no = tf["need_off"][0].cpu().numpy()
+        assert no[cnt] == no[64]
