@@ -235,6 +235,31 @@ int hg_mg_build_group(const int64_t* offsets, const int32_t* targets, int64_t n_
                       int32_t roots_per_state, const hg_mg_layout* layout, int32_t* ws,
                       const hg_mg_batch* outs, int* err_flag, int32_t ctas_per_sm, void* stream);
 
+/* Partitioned topology (north_star: CSR rows sharded by home server): shard h
+ * is a local CSR (offsets int64[n_h + 1], targets int32) in HBM of GPU h,
+ * passed as device pointers valid on the calling GPU (its own shard, peers'
+ * mapped over NVLink with hg_ipc_open).  Vertex v's row: contiguous
+ * partitions (home_of == NULL) -- shard h holds [vstart[h], vstart[h+1]),
+ * local row v - vstart[h]; arbitrary partitions -- shard home_of[v], local row
+ * row_of[v] (int32[n] each, device).  Row degrees must be < 2^26. */
+#define HG_MAX_SHARDS 16
+typedef struct {
+  int32_t n_shards;
+  const int64_t* offsets[HG_MAX_SHARDS];
+  const int32_t* targets[HG_MAX_SHARDS];
+  int64_t vstart[HG_MAX_SHARDS + 1];
+  const int32_t* home_of;
+  const int32_t* row_of;
+} hg_csr_shards;
+
+/* hg_mg_build_group over a sharded CSR (remote rows read over NVLink). */
+int hg_mg_build_group_sharded(const hg_csr_shards* shards, int64_t n_vertices,
+                              const int64_t* roots, int32_t n_roots, int32_t n_batches,
+                              const int32_t* n_roots_dev, const uint64_t* iter_state,
+                              int32_t roots_per_state, const hg_mg_layout* layout, int32_t* ws,
+                              const hg_mg_batch* outs, int* err_flag, int32_t ctas_per_sm,
+                              void* stream);
+
 /* Kernel selection of hg_mg_build / _n / _group (process-wide): 0 (default)
  * builds two-layer micrographs with hop-1 fanout <= 31 and <= 256 hop-2 pairs
  * warp-per-root (8 roots per CTA, dynamic hop-2 task list), everything else
@@ -342,6 +367,7 @@ typedef struct {
  * total_remote += #remote occurrences; bitmap: n/32 words, zero on entry/exit. */
 int hg_alloc(size_t bytes, void** out);
 int hg_free(void* p);
+int hg_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
 int hg_ipc_handle(void* p, void* handle_out);
 int hg_ipc_open(const void* handle, void** out);
 int hg_ipc_close(void* p);

@@ -39,6 +39,17 @@ class MgBatch(C.Structure):
                 ("nbr_vid1", C.c_void_p), ("self_vid1", C.c_void_p)]
 
 
+MAX_SHARDS = 16  # HG_MAX_SHARDS
+
+
+class CsrShards(C.Structure):
+    """hg_csr_shards (include/hopgnn.h section 4)."""
+
+    _fields_ = [("n_shards", C.c_int32), ("offsets", C.c_void_p * MAX_SHARDS),
+                ("targets", C.c_void_p * MAX_SHARDS), ("vstart", C.c_int64 * (MAX_SHARDS + 1)),
+                ("home_of", C.c_void_p), ("row_of", C.c_void_p)]
+
+
 class GraphTables(C.Structure):
     _fields_ = [("n", C.c_int64), ("n_blocks", C.c_int32), ("n_levels", C.c_int32),
                 ("key", C.c_uint64), ("deg_key", C.c_uint64), ("thr_in", C.c_uint32), ("in_always", C.c_int32),
@@ -111,6 +122,8 @@ SIGNATURES = {
     "hg_mg_build_mode": [I32],
     "hg_mg_build_group": [V, V, I64, V, I32, I32, V, V, I32, C.POINTER(MgLayout), V,
                           C.POINTER(MgBatch), V, I32, V],
+    "hg_mg_build_group_sharded": [C.POINTER(CsrShards), I64, V, I32, I32, V, V, I32,
+                                  C.POINTER(MgLayout), V, C.POINTER(MgBatch), V, I32, V],
     "hg_train_step": [C.POINTER(StepDesc), I32, V],
     "hg_forward": [C.POINTER(StepDesc), I32, V],
     "hg_sgd_update": [V, V, V, I64, C.c_float, C.c_float, V],
@@ -118,6 +131,7 @@ SIGNATURES = {
     "hg_allreduce_sgd_refresh": [V, C.POINTER(StepDesc), V, V, I64, C.c_float, C.c_float, V],
     "hg_gemm_bf16": [V, I64, C.c_int, V, I64, C.c_int, V, I64, I32, I32, I32, I32, V, I32, V],
     "hg_alloc": [C.c_size_t, C.POINTER(C.c_void_p)],
+    "hg_memcpy_d2d": [V, V, C.c_size_t, V],
     "hg_free": [V],
     "hg_ipc_handle": [V, V],
     "hg_ipc_open": [V, C.POINTER(C.c_void_p)],

@@ -428,6 +428,12 @@ extern "C" int hg_alloc(size_t bytes, void** out) {
   return HG_OK;
 }
 
+extern "C" int hg_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream) {
+  if (bytes) HG_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice,
+                                         (cudaStream_t)stream));
+  return HG_OK;
+}
+
 extern "C" int hg_free(void* p) {
   if (p) HG_CUDA_TRY(cudaFree(p));
   return HG_OK;

@@ -44,6 +44,39 @@ struct MgOuts {
   hg_mg_batch b[HG_MAX_GROUP];
 };
 
+// The CSR the builds read: one table (single GPU, replicated), or one shard
+// per home server mapped over NVLink (partitioned topology, north_star): the
+// row of v lives in shard home(v) at local row v - vstart[home(v)]
+// (contiguous partitions, e.g. planted blocks), or at row_of[v] with home
+// from home_of[v] (arbitrary partitions).
+struct CsrView {
+  const int64_t* off[HG_MAX_SHARDS];
+  const int32_t* tgt[HG_MAX_SHARDS];
+  int64_t vstart[HG_MAX_SHARDS + 1];
+  const int32_t* home_of;  // NULL: contiguous ranges (vstart)
+  const int32_t* row_of;
+  int S;
+};
+
+__device__ __forceinline__ int csr_row(const CsrView& g, int64_t v, int64_t* lo) {
+  int h = 0;
+  int64_t r = v;
+  if (g.S > 1) {
+    if (g.home_of) {
+      h = g.home_of[v];
+      r = g.row_of[v];
+    } else {
+      while (h + 1 < g.S && v >= g.vstart[h + 1]) ++h;
+      r = v - g.vstart[h];
+    }
+  }
+  const int64_t* off = g.off[h];
+  *lo = off[r];
+  return (int)(off[r + 1] - *lo) | (h << 26);  // degree < 2^26, shard in the top bits
+}
+__device__ __forceinline__ int row_deg(int packed) { return packed & ((1 << 26) - 1); }
+__device__ __forceinline__ int row_shard(int packed) { return packed >> 26; }
+
 struct MgCarve {
   int L;
   int fanout[HG_MAX_LAYERS];
@@ -437,7 +470,7 @@ __device__ long long g_phase[4096][16];
 
 // One root's micrograph (CTA-wide); r indexes roots / iter_state / ws.
 __device__ __forceinline__ void build_root(
-    const int r, const int64_t* __restrict__ offsets, const int32_t* __restrict__ targets,
+    const int r, const CsrView& g,
     int64_t n_vertices, const int64_t* __restrict__ roots, const uint64_t* __restrict__ iter_state,
     int roots_per_state, const MgCarve& c, int32_t* __restrict__ ws, int* err,
     const int32_t* __restrict__ n_roots_dev, int per_batch) {
@@ -483,20 +516,23 @@ __device__ __forceinline__ void build_root(
     int* flat = sm + c.sm_flat[h];
     const uint64_t state = mix64(mix64(key) ^ (uint64_t)h);  // chain(key, hop)
     for (int i = threadIdx.x; i < F; i += blockDim.x) {
-      const int v = front[i];
-      const int64_t d = offsets[v + 1] - offsets[v];
-      degs[i] = (int)d;
-      cnt[i] = d <= fo ? (int)d : fo;
+      int64_t lo;
+      const int pk = csr_row(g, front[i], &lo);
+      const int d = row_deg(pk);
+      degs[i] = pk;
+      cnt[i] = d <= fo ? d : fo;
     }
     __syncthreads();
     const int T = block_scan_small(cnt, off, F, scan);
     HG_PHASE(1 + 4 * (h - 1));
     // small tasks: one warp each
     for (int i = warp_id(); i < F; i += kBuildWarps) {
-      const int d = degs[i];
+      const int d = row_deg(degs[i]);
       if (d > kBigTask) continue;
       const int v = front[i];
-      const int64_t lo = offsets[v];
+      int64_t lo;
+      csr_row(g, v, &lo);
+      const int32_t* targets = g.tgt[row_shard(degs[i])];
       int32_t* out = flat + off[i];
       if (d <= fo) {
         for (int j = lane_id(); j < d; j += 32) out[j] = targets[lo + j];
@@ -510,10 +546,12 @@ __device__ __forceinline__ void build_root(
     HG_PHASE(2 + 4 * (h - 1));
     // hubs: the whole CTA
     for (int i = 0; i < F; ++i) {
-      const int d = degs[i];
+      const int d = row_deg(degs[i]);
       if (d <= kBigTask) continue;
       const int v = front[i];
-      team_select<BlockTeam>(targets, offsets[v], d, fo, mean, mix64(state ^ (uint64_t)v),
+      int64_t lo;
+      csr_row(g, v, &lo);
+      team_select<BlockTeam>(g.tgt[row_shard(degs[i])], lo, d, fo, mean, mix64(state ^ (uint64_t)v),
                              flat + off[i], cand_base + (size_t)kBuildWarps * c.cand_cap,
                              c.cand_cap, warp_ctr + kBuildWarps, tslots + kBuildWarps, err);
     }
@@ -593,13 +631,12 @@ __device__ __forceinline__ void build_root(
 // roots: capping the resident build CTAs per SM leaves registers for the
 // training kernels that run beside the build in the graph loop.
 __global__ void __launch_bounds__(kBuildThreads, HG_BUILD_MINB)
-k_mg_build(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targets,
-           int64_t n_vertices, const int64_t* __restrict__ roots, int n_roots,
+k_mg_build(const CsrView g, int64_t n_vertices, const int64_t* __restrict__ roots, int n_roots,
            const uint64_t* __restrict__ iter_state, int roots_per_state, MgCarve c,
            int32_t* __restrict__ ws, int* err, const int32_t* __restrict__ n_roots_dev,
            int per_batch) {
   for (int r = blockIdx.x; r < n_roots; r += gridDim.x) {
-    build_root(r, offsets, targets, n_vertices, roots, iter_state, roots_per_state, c, ws, err,
+    build_root(r, g, n_vertices, roots, iter_state, roots_per_state, c, ws, err,
                n_roots_dev, per_batch);
     __syncthreads();  // shared tiles are reused by the next root
   }
@@ -664,8 +701,7 @@ __device__ __forceinline__ int warp_incl_scan(int x) {
 }
 
 __global__ void __launch_bounds__(kBuildThreads, 4)
-k_mg_build_w2(const int64_t* __restrict__ offsets, const int32_t* __restrict__ targets,
-              int64_t n_vertices, const int64_t* __restrict__ roots, int n_roots,
+k_mg_build_w2(const CsrView g, int64_t n_vertices, const int64_t* __restrict__ roots, int n_roots,
               const uint64_t* __restrict__ iter_state, int roots_per_state, MgCarve c,
               int32_t* __restrict__ ws, int* err, const int32_t* __restrict__ n_roots_dev,
               int per_batch) {
@@ -706,8 +742,10 @@ k_mg_build_w2(const int64_t* __restrict__ offsets, const int32_t* __restrict__ t
                                : iter_state[r];
       const uint64_t k1 = mix64(key);
       const uint64_t st1 = mix64(k1 ^ 1ull);
-      const int64_t lo = offsets[root];
-      const int d = (int)(offsets[root + 1] - lo);
+      int64_t lo;
+      const int pk = csr_row(g, root, &lo);
+      const int d = row_deg(pk);
+      const int32_t* targets = g.tgt[row_shard(pk)];
       if (lane == 0) {
         S.st1 = st1;
         S.st2 = mix64(k1 ^ 2ull);
@@ -728,8 +766,9 @@ k_mg_build_w2(const int64_t* __restrict__ offsets, const int32_t* __restrict__ t
     for (int q = 0; q < nh1; ++q) {  // hub roots: the whole CTA draws
       W2Slot& H = slots[hub1_list[q]];
       const int64_t rt = H.root;
-      const int64_t lo = offsets[rt];
-      team_select<BlockTeam>(targets, lo, (int)(offsets[rt + 1] - lo), f1, m1,
+      int64_t lo;
+      const int pk = csr_row(g, rt, &lo);
+      team_select<BlockTeam>(g.tgt[row_shard(pk)], lo, row_deg(pk), f1, m1,
                              mix64(H.st1 ^ (uint64_t)rt), H.flat1, cta_cand, cap,
                              warp_ctr + kW2Roots, tslots + kW2Roots, err);
     }
@@ -741,11 +780,11 @@ k_mg_build_w2(const int64_t* __restrict__ offsets, const int32_t* __restrict__ t
       __syncwarp();
       int cnt = 0;
       if (lane < nl1) {
-        const int v = S.lay1[lane];
-        const int64_t lo = offsets[v];
-        const int d = (int)(offsets[v + 1] - lo);
+        int64_t lo;
+        const int pk = csr_row(g, S.lay1[lane], &lo);
+        const int d = row_deg(pk);
         S.lo1[lane] = lo;
-        S.deg1[lane] = d;
+        S.deg1[lane] = pk;
         cnt = d <= f2 ? d : f2;
       }
       const int incl = warp_incl_scan(cnt);
@@ -768,7 +807,8 @@ k_mg_build_w2(const int64_t* __restrict__ offsets, const int32_t* __restrict__ t
       const int ow = 31 - __clz(bm);
       const int i = t - __shfl_sync(full, excl_b, ow);
       W2Slot& Q = slots[ow];
-      const int d = Q.deg1[i];
+      const int d = row_deg(Q.deg1[i]);
+      const int32_t* targets = g.tgt[row_shard(Q.deg1[i])];
       int32_t* out = Q.flat2 + Q.off1[i];
       if (d <= f2) {
         const int64_t lo = Q.lo1[i];
@@ -789,7 +829,7 @@ k_mg_build_w2(const int64_t* __restrict__ offsets, const int32_t* __restrict__ t
       while (base + nl1s[ow] <= t) base += nl1s[ow++];
       W2Slot& Q = slots[ow];
       const int i = t - base;
-      team_select<BlockTeam>(targets, Q.lo1[i], Q.deg1[i], f2, m2,
+      team_select<BlockTeam>(g.tgt[row_shard(Q.deg1[i])], Q.lo1[i], row_deg(Q.deg1[i]), f2, m2,
                              mix64(Q.st2 ^ (uint64_t)Q.lay1[i]), Q.flat2 + Q.off1[i], cta_cand,
                              cap, warp_ctr + kW2Roots, tslots + kW2Roots, err);
     }
@@ -1029,7 +1069,37 @@ extern "C" int hg_mg_build(const int64_t* offsets, const int32_t* targets, int64
 // that compare the two kernels)
 static int g_build_mode = 0;
 
-static int build_group(const int64_t* offsets, const int32_t* targets, int64_t n_vertices,
+static CsrView single_view(const int64_t* offsets, const int32_t* targets) {
+  CsrView g{};
+  g.S = 1;
+  g.off[0] = offsets;
+  g.tgt[0] = targets;
+  return g;
+}
+
+static int view_from(const hg_csr_shards* sh, int64_t n_vertices, CsrView* g) {
+  if (!sh || sh->n_shards < 1 || sh->n_shards > HG_MAX_SHARDS)
+    return hg_fail(HG_ECONFIG, "csr shards: n_shards must be 1..%d", HG_MAX_SHARDS);
+  *g = CsrView{};
+  g->S = sh->n_shards;
+  for (int h = 0; h < g->S; ++h) {
+    if (!sh->offsets[h] || !sh->targets[h]) return hg_fail(HG_ECONFIG, "csr shard %d missing", h);
+    g->off[h] = sh->offsets[h];
+    g->tgt[h] = sh->targets[h];
+  }
+  g->home_of = sh->home_of;
+  g->row_of = sh->row_of;
+  if (g->S > 1 && !g->home_of) {
+    if (sh->vstart[0] != 0 || sh->vstart[g->S] != n_vertices)
+      return hg_fail(HG_ECONFIG, "csr shards: vstart must cover [0, n_vertices)");
+    for (int h = 0; h <= g->S; ++h) g->vstart[h] = sh->vstart[h];
+  } else if (g->S > 1 && !g->row_of) {
+    return hg_fail(HG_ECONFIG, "csr shards: home_of needs row_of");
+  }
+  return HG_OK;
+}
+
+static int build_group(const CsrView& g, int64_t n_vertices,
                        const int64_t* roots, int32_t n_roots, int32_t n_batches,
                        const int32_t* n_roots_dev, const uint64_t* iter_state,
                        int32_t roots_per_state, const hg_mg_layout* layout, int32_t* ws,
@@ -1066,10 +1136,10 @@ static int build_group(const int64_t* offsets, const int32_t* targets, int64_t n
     HG_CUDA_TRY(cudaFuncSetAttribute(k_mg_build_w2, cudaFuncAttributeMaxDynamicSharedMemorySize, w2s));
     const int groups = (total + kW2Roots - 1) / kW2Roots;
     k_mg_build_w2<<<std::min(grid, groups), kBuildThreads, w2s, s>>>(
-        offsets, targets, n_vertices, roots, total, iter_state, roots_per_state, c, ws, err_flag,
+        g, n_vertices, roots, total, iter_state, roots_per_state, c, ws, err_flag,
         n_roots_dev, n_roots);
   } else {
-    k_mg_build<<<grid, kBuildThreads, c.smem_bytes, s>>>(offsets, targets, n_vertices, roots,
+    k_mg_build<<<grid, kBuildThreads, c.smem_bytes, s>>>(g, n_vertices, roots,
                                                           total, iter_state, roots_per_state, c,
                                                           ws, err_flag, n_roots_dev, n_roots);
   }
@@ -1087,7 +1157,8 @@ extern "C" int hg_mg_build_n(const int64_t* offsets, const int32_t* targets, int
                              const uint64_t* iter_state, int32_t roots_per_state,
                              const hg_mg_layout* layout, int32_t* ws, hg_mg_batch* out,
                              int* err_flag, void* stream) {
-  return build_group(offsets, targets, n_vertices, roots, n_roots, 1, n_roots_dev, iter_state,
+  return build_group(single_view(offsets, targets), n_vertices, roots, n_roots, 1, n_roots_dev,
+                     iter_state,
                      roots_per_state, layout, ws, out, err_flag, 0, stream);
 }
 
@@ -1098,9 +1169,23 @@ extern "C" int hg_mg_build_group(const int64_t* offsets, const int32_t* targets,
                                  const hg_mg_layout* layout, int32_t* ws,
                                  const hg_mg_batch* outs, int* err_flag, int32_t ctas_per_sm,
                                  void* stream) {
-  return build_group(offsets, targets, n_vertices, roots, n_roots, n_batches, n_roots_dev,
-                     iter_state, roots_per_state, layout, ws, outs, err_flag, ctas_per_sm,
-                     stream);
+  return build_group(single_view(offsets, targets), n_vertices, roots, n_roots, n_batches,
+                     n_roots_dev, iter_state, roots_per_state, layout, ws, outs, err_flag,
+                     ctas_per_sm, stream);
+}
+
+extern "C" int hg_mg_build_group_sharded(const hg_csr_shards* shards, int64_t n_vertices,
+                                         const int64_t* roots, int32_t n_roots,
+                                         int32_t n_batches, const int32_t* n_roots_dev,
+                                         const uint64_t* iter_state, int32_t roots_per_state,
+                                         const hg_mg_layout* layout, int32_t* ws,
+                                         const hg_mg_batch* outs, int* err_flag,
+                                         int32_t ctas_per_sm, void* stream) {
+  CsrView g;
+  int st = view_from(shards, n_vertices, &g);
+  if (st) return st;
+  return build_group(g, n_vertices, roots, n_roots, n_batches, n_roots_dev, iter_state,
+                     roots_per_state, layout, ws, outs, err_flag, ctas_per_sm, stream);
 }
 
 extern "C" int hg_mg_build_mode(int32_t mode) {

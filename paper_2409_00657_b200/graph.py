@@ -206,6 +206,128 @@ def generate(spec: GraphSpec, device="cuda", chunk_slots: int = 1 << 30) -> Grap
     return Graph(n, offsets, targets[:m] if m else targets[:0])
 
 
+class ShardedGraph:
+    """CSR topology partitioned by home server (north_star): this GPU holds
+    only the rows of the vertices homed on it; every peer's shard is mapped
+    over NVLink (CUDA IPC), and the micrograph builds read a remote row in
+    place from its owner (hg_mg_build_group_sharded).  Contiguous partitions
+    (planted blocks) address rows by vertex ranges; arbitrary ones through
+    per-vertex home / local-row arrays.  Collective construction: every rank
+    of the group calls it together."""
+
+    def __init__(self, n_vertices: int, part: "PartitionMap", rank: int,
+                 local_offsets: torch.Tensor, local_targets: torch.Tensor, group=None):
+        import torch.distributed as dist
+        self.n_vertices = int(n_vertices)
+        self.part, self.rank, self.S = part, int(rank), part.n_servers
+        if self.S > _lib.MAX_SHARDS:
+            raise ValueError(f"at most {_lib.MAX_SHARDS} shards")
+        dev = local_offsets.device
+        self.device = dev
+        # the local shard in raw (IPC-exportable) allocations
+        self._mine, self._opened = [], []
+        ptrs = []
+        for t in (local_offsets.contiguous(), local_targets.contiguous()):
+            p = C.c_void_p()
+            nbytes = max(t.numel() * t.element_size(), 16)
+            _lib.call("hg_alloc", nbytes, C.byref(p))
+            _lib.call("hg_memcpy_d2d", p.value, t.data_ptr(), t.numel() * t.element_size(),
+                      torch.cuda.current_stream(dev).cuda_stream)
+            self._mine.append(p.value)
+            ptrs.append(p.value)
+        torch.cuda.synchronize(dev)
+        self.n_targets_local = int(local_targets.numel())
+        handles = []
+        for p in ptrs:
+            h = (C.c_char * 64)()
+            _lib.call("hg_ipc_handle", p, h)
+            handles.append(bytes(h))
+        every = [None] * self.S
+        if dist.is_initialized() and self.S > 1:
+            dist.all_gather_object(every, handles, group=group)
+        else:
+            every = [handles]
+        sh = _lib.CsrShards()
+        sh.n_shards = self.S
+        for h, hs in enumerate(every):
+            for j, hb in enumerate(hs):
+                if h == self.rank:
+                    ptr = ptrs[j]
+                else:
+                    q = C.c_void_p()
+                    _lib.call("hg_ipc_open", (C.c_char * 64).from_buffer_copy(hb), C.byref(q))
+                    self._opened.append(q.value)
+                    ptr = q.value
+                (sh.offsets if j == 0 else sh.targets)[h] = ptr
+        self._address(sh)
+
+    @staticmethod
+    def _rows_of(g: "Graph", part: "PartitionMap", h: int):
+        dev = g.device
+        mine = torch.from_numpy(np.flatnonzero(part.home == h)).to(dev)
+        lo, hi = g.offsets[mine], g.offsets[mine + 1]
+        ln = hi - lo
+        off = torch.zeros(mine.numel() + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(ln, 0, out=off[1:])
+        m = int(off[-1].item())
+        idx = (torch.repeat_interleave(lo - off[:-1], ln) +
+               torch.arange(m, device=dev)) if m else torch.zeros(0, dtype=torch.int64, device=dev)
+        tgt = g.targets[idx] if m else torch.zeros(1, dtype=torch.int32, device=dev)
+        return off, tgt
+
+    @classmethod
+    def split_local(cls, g: "Graph", part: "PartitionMap") -> "ShardedGraph":
+        """All S shards of g on ONE device (no IPC): the sharded addressing of
+        the builds on a single GPU (tests)."""
+        obj = cls.__new__(cls)
+        obj.n_vertices, obj.part, obj.rank, obj.S = g.n_vertices, part, 0, part.n_servers
+        obj.device, obj._mine, obj._opened = g.device, [], []
+        obj._keep = [cls._rows_of(g, part, h) for h in range(obj.S)]
+        sh = _lib.CsrShards()
+        sh.n_shards = obj.S
+        for h, (off, tgt) in enumerate(obj._keep):
+            sh.offsets[h], sh.targets[h] = off.data_ptr(), tgt.data_ptr()
+        obj._address(sh)
+        return obj
+
+    def _address(self, sh) -> None:
+        home = self.part.home
+        contiguous = bool(np.all(np.diff(home) >= 0)) if len(home) else True
+        if contiguous:
+            starts = np.searchsorted(home, np.arange(self.S)) if len(home) else np.zeros(self.S)
+            for h in range(self.S):
+                sh.vstart[h] = int(starts[h])
+            sh.vstart[self.S] = self.n_vertices
+            self.home_of = self.row_of = None
+        else:
+            row_of = np.empty(len(home), dtype=np.int32)
+            for h in range(self.S):
+                idx = np.flatnonzero(home == h)
+                row_of[idx] = np.arange(len(idx), dtype=np.int32)
+            self.home_of = self.part.home_device(self.device)
+            self.row_of = torch.from_numpy(row_of).to(self.device)
+            sh.home_of = self.home_of.data_ptr()
+            sh.row_of = self.row_of.data_ptr()
+        self.contiguous = contiguous
+        self.shards = sh
+
+    @classmethod
+    def from_graph(cls, g: "Graph", part: "PartitionMap", rank: int, group=None):
+        """This rank's rows of a full CSR (the full graph may be freed afterwards)."""
+        off, tgt = cls._rows_of(g, part, rank)
+        return cls(g.n_vertices, part, rank, off, tgt, group)
+
+    def close(self) -> None:
+        """Unmap the peers' shards and free this rank's (after a barrier: peers
+        may still read it)."""
+        for p in self._opened:
+            _lib.call("hg_ipc_close", p)
+        self._opened = []
+        for p in self._mine:
+            _lib.call("hg_free", p)
+        self._mine = []
+
+
 # ---------------------------------------------------------------- partitions
 
 class PartitionMap:

@@ -218,6 +218,11 @@ class MicrographBuilder:
         s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
         rp = roots if isinstance(roots, int) else roots.data_ptr()
         kp = keys if isinstance(keys, int) else keys.data_ptr()
+        if getattr(g, "shards", None) is not None:  # partitioned CSR (graph.ShardedGraph)
+            _lib.call("hg_mg_build_group_sharded", C.byref(g.shards), g.n_vertices, rp, n, 1,
+                      n_dev, kp, int(roots_per_state), C.byref(self.layout), self.ws.data_ptr(),
+                      C.byref(self.cbatch), self.err.data_ptr(), 0, s)
+            return MicrographBatch(self.L, n, self.tensors)
         if n_dev is not None:  # n is the capacity; the device count says how many are real
             _lib.call("hg_mg_build_n", g.offsets.data_ptr(), g.targets.data_ptr(), g.n_vertices,
                       rp, n, n_dev, kp, int(roots_per_state), C.byref(self.layout),
@@ -272,6 +277,12 @@ class GroupBuilder:
         resident build CTAs per SM (persistent grid) to leave room for
         concurrently running kernels."""
         s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        if getattr(g, "shards", None) is not None:  # partitioned CSR (graph.ShardedGraph)
+            _lib.call("hg_mg_build_group_sharded", C.byref(g.shards), g.n_vertices,
+                      self.roots.data_ptr(), self.R, self.K, n_dev, self.keys.data_ptr(), self.R,
+                      C.byref(self.layout), self.ws.data_ptr(), self.outs, self.err.data_ptr(),
+                      int(ctas_per_sm), s)
+            return
         _lib.call("hg_mg_build_group", g.offsets.data_ptr(), g.targets.data_ptr(), g.n_vertices,
                   self.roots.data_ptr(), self.R, self.K, n_dev, self.keys.data_ptr(), self.R,
                   C.byref(self.layout), self.ws.data_ptr(), self.outs, self.err.data_ptr(),

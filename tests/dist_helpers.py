@@ -60,7 +60,7 @@ def pregather_worker(rank, world, init_file, result_file):
 
 
 def micrograph_worker(rank, world, init_file, result_file, mode, dtype_name, feat_mode="pg",
-                      strategy="micrograph", iters=3, graph_group=1):
+                      strategy="micrograph", iters=3, graph_group=1, csr="replicated"):
     """Full multi-GPU micrograph (or model-centric) iterations vs the oracle
     engine (ledger exact, parameters within tolerance)."""
     import json
@@ -78,8 +78,13 @@ def micrograph_worker(rank, world, init_file, result_file, mode, dtype_name, fea
                                             n_blocks=4, d_cap=600, seed=11)))
     home = (keyed(chain(seed, 0x02, 0xA7), np.arange(3000)) % np.uint64(world)).astype(np.int64)
     dtype = torch.float32 if dtype_name == "f32" else torch.bfloat16
+    if csr == "sharded-blocks":  # contiguous homes: planted-block style partition
+        home = (np.arange(3000) * world) // 3000
     G = Graph.from_host(off, tgt, f"cuda:{rank}")
     part = PartitionMap(home, world, f"cuda:{rank}")
+    if csr != "replicated":  # this rank keeps only its rows; peers' shards over NVLink
+        from paper_2409_00657_b200.graph import ShardedGraph
+        G = ShardedGraph.from_graph(G, part, rank)
     model = init_model(arch, D, H, len(fo), C, chain(seed, 0x07), f"cuda:{rank}")
     tr = MicrographTrainer(G, part, model, fo, B, seed, lr=0.1, dtype=dtype, mode=mode,
                            iterations=iters, pregather=(feat_mode == "pg"), strategy=strategy,

@@ -96,3 +96,22 @@ def test_group_loop_matches_oracle(strategy):
     res = json.load(open(os.path.join(d, "res.0")))
     assert res["ok"], res["msg"]
     assert res["graph_used"], "group loop never engaged"
+
+
+@pytest.mark.parametrize("strategy,csr", [("micrograph", "sharded-hash"),
+                                          ("micrograph", "sharded-blocks"),
+                                          ("model-centric", "sharded-hash")])
+def test_sharded_csr_matches_oracle(strategy, csr):
+    """Partitioned CSR (north_star): every rank holds only its homed rows and
+    reads peers' rows over NVLink inside the builds; grouped graph loop
+    engaged.  Ledger and parameters equal the oracle's."""
+    import dist_helpers
+    world = _world()
+    d = tempfile.mkdtemp()
+    mp.spawn(dist_helpers.micrograph_worker,
+             args=(world, os.path.join(d, "init"), os.path.join(d, "res"), "fused", "f32", "peer",
+                   strategy, 9, 2, csr),
+             nprocs=world, join=True)
+    res = json.load(open(os.path.join(d, "res.0")))
+    assert res["ok"], res["msg"]
+    assert res["graph_used"], "group loop never engaged"

@@ -294,3 +294,49 @@ def test_warp_build_self_loops_isolated_and_device_counts(P):
         # slots past the device count: empty micrographs
         no = tf["need_off"][0].cpu().numpy()
         assert no[cnt] == no[64]
+
+
+@pytest.mark.parametrize("fo", [(15, 10), (10, 10, 5, 5)])
+@pytest.mark.parametrize("kind,S", [("blocks", 2), ("blocks", 8), ("hash", 3)])
+def test_sharded_csr_build_matches_replicated(P, fo, kind, S):
+    """Partitioned topology (graph.ShardedGraph): rows addressed per home shard
+    (contiguous ranges or home/local-row arrays) build exactly what the
+    replicated CSR builds -- both kernels, single and grouped builds."""
+    from paper_2409_00657_b200.graph import (GraphSpec, PartitionMap, ShardedGraph, generate,
+                                             partition_hash)
+    from paper_2409_00657_b200.sampler import GroupBuilder, MicrographBuilder
+    kw = SPECS[1]
+    G = generate(GraphSpec(**kw))
+    n = kw["n"]
+    part = (PartitionMap((np.arange(n) * S) // n, S) if kind == "blocks"
+            else partition_hash(n, S, 5))
+    SG = ShardedGraph.split_local(G, part)
+    assert SG.contiguous == (kind == "blocks")
+    deg = np.diff(G.to_host()[0])
+    roots = np.concatenate([np.argsort(-deg)[:16],
+                            np.random.default_rng(S).integers(0, n, 112)]).astype(np.int64)
+    st = torch.tensor([np.uint64(chain(7, S)).view(np.int64), np.uint64(chain(8, S)).view(np.int64)],
+                      device="cuda")
+    outs = []
+    for g in (G, SG):
+        bs = [MicrographBuilder(fo, 64) for _ in range(2)]
+        gb = GroupBuilder(bs)
+        gb.roots.copy_(torch.from_numpy(roots).cuda())
+        gb.keys.copy_(st)
+        gb.build(g, ctas_per_sm=2)
+        single = MicrographBuilder(fo, 64)
+        single.build(g, torch.from_numpy(roots[:64]).cuda(), st[:1], 64)
+        torch.cuda.synchronize()
+        gb.check()
+        single.check()
+        outs.append([b.tensors for b in bs] + [single.tensors])
+    for a, b in zip(*outs):
+        assert torch.equal(a["totals"], b["totals"])
+        L = len(fo)
+        for k in range(L + 1):
+            nk = int(a["totals"][k])
+            assert torch.equal(a["need_ids"][k][:nk], b["need_ids"][k][:nk])
+            if k:
+                p = int(a["totals"][L + k])
+                assert torch.equal(a["nbr_idx"][k][:p], b["nbr_idx"][k][:p])
+                assert torch.equal(a["nbr_off"][k][:nk + 1], b["nbr_off"][k][:nk + 1])
