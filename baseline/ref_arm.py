@@ -21,13 +21,15 @@ are materialised (oracle/graphgen.py rows_csr, the data generator) only for
 the vertices the sampled micrographs expand -- every other row is empty and
 never read -- and each worker holds the feature rows (gnnsim
 ``kernels.feature_rows``, the values the FeatureStore is filled with,
-featstore.py:161-184) of its own micrographs' vertices, looked up with
-``searchsorted`` + ``take`` like ``FeatureStore.rows``.
+featstore.py:161-184) of every sampled micrograph's vertices, looked up
+with ``searchsorted`` + ``take`` like ``FeatureStore.rows``.
 
 Parallelism (all host cores, no per-step IPC of parameters or gradients):
-worker w owns a disjoint slice of every step's roots; parameters and the
-per-worker gradient accumulators live in shared memory; two barriers per
-step; the parent runs gnnsim's ``sync_and_update`` on the shared buffers.
+the workers pull the step's roots in chunks of 4 from a shared counter (a
+hub micrograph costs 10-100x a typical one, so static slices leave cores
+idle); parameters and the per-worker gradient accumulators live in shared
+memory; two barriers per step; the parent runs gnnsim's ``sync_and_update``
+on the shared buffers.
 """
 from __future__ import annotations
 
@@ -137,38 +139,34 @@ class Shared:
         return GradAccumulator(w, Gradients(v[:L], v[L:2 * L], v[2 * L]))
 
 
-def _worker(w, P, wl, shared, bar, arch, dim, classes, lseed):
+CHUNK = 4  # roots a worker takes per grab of the step's shared counter
+
+
+def _worker(w, wl, shared, bar, ctr, arch, classes, lseed, fid, ftab):
     # one core per worker: numpy's BLAS would otherwise spawn a thread per
     # core in every worker and oversubscribe the host
     from threadpoolctl import threadpool_limits
     threadpool_limits(1)
-    import gnnsim.kernels as K
     from gnnsim.model import LabelOracle, accumulate, forward, loss_and_backward
-    from gnnsim.rng import chain
     from gnnsim.sampler import sample_micrograph
     model = shared.model(arch)
     acc = shared.acc(w)
     labels = LabelOracle(classes, lseed)
-    fstate = chain(chain(wl.cfg["seed"], 0x03), 0xFE)
-    mine = [np.array_split(np.arange(wl.B), P)[w] for _ in range(wl.steps)]
-    # untimed: this worker's feature rows (the FeatureStore's values)
-    ids = []
-    for s in range(wl.steps):
-        for i in mine[s]:
-            m = sample_micrograph(wl.graph, int(wl.roots[s][i]), wl.scfg, wl.keys[s][i])
-            ids.append(m.vertices)
-    fid = np.unique(np.concatenate(ids)) if ids else np.empty(0, np.int64)
-    ftab = K.feature_rows(fid, dim, fstate)
     bar.wait()  # ready
     for s in range(wl.steps):
         bar.wait()  # step s starts
         acc.reset()
-        # engine.py:290-295 (sample the cell's micrographs), then run_cell
-        # (engine.py:428-445): one fetch of the cell's unique needs, per
-        # micrograph searchsorted + forward + label + backward + accumulate
-        micros = [sample_micrograph(wl.graph, int(wl.roots[s][i]), wl.scfg, wl.keys[s][i])
-                  for i in mine[s]]
-        if micros:
+        while True:  # dynamic schedule: hub micrographs cost 10-100x a typical one
+            with ctr.get_lock():
+                i0 = ctr.value
+                ctr.value = i0 + CHUNK
+            if i0 >= wl.B:
+                break
+            # engine.py:290-295 (sample the micrographs), then run_cell
+            # (engine.py:428-445): one fetch of the unique needs, per micrograph
+            # searchsorted + forward + label + backward + accumulate
+            micros = [sample_micrograph(wl.graph, int(wl.roots[s][i]), wl.scfg, wl.keys[s][i])
+                      for i in range(i0, min(i0 + CHUNK, wl.B))]
             needs = np.unique(np.concatenate([m.vertices for m in micros]))
             rows = ftab[np.searchsorted(fid, needs)]
             for m in micros:
@@ -195,13 +193,21 @@ def run(cfg: dict, roots_per_step: int, steps: int, warmup: int, procs: int = No
     template = init_model(arch, dim, hidden, len(wl.fanout), classes, chain(seed, 0x07))
     shared = Shared(template, procs)
     lseed = chain(seed, 0x04)
-    # compile gnnsim's numba kernels once, before the fork
+    # untimed, before the fork (shared copy-on-write by the workers): the
+    # FeatureStore's rows of every vertex the sampled micrographs touch
+    # (gnnsim kernels.feature_rows, the values init_features fills it with)
+    import gnnsim.kernels as K
     from gnnsim.sampler import sample_micrograph
-    sample_micrograph(wl.graph, int(wl.roots[0][0]), wl.scfg, wl.keys[0][0])
+    ids = [sample_micrograph(wl.graph, int(r), wl.scfg, k).vertices
+           for s in range(wl.steps) for r, k in zip(wl.roots[s], wl.keys[s])]
+    fid = np.unique(np.concatenate(ids))
+    del ids
+    ftab = K.feature_rows(fid, dim, chain(chain(seed, 0x03), 0xFE))
     ctx = mp.get_context("fork")
     bar = ctx.Barrier(procs + 1)
-    ps = [ctx.Process(target=_worker, args=(w, procs, wl, shared, bar, arch, dim, classes, lseed),
-                      daemon=True) for w in range(procs)]
+    ctr = ctx.Value("q", 0)
+    ps = [ctx.Process(target=_worker, args=(w, wl, shared, bar, ctr, arch, classes, lseed, fid,
+                                            ftab), daemon=True) for w in range(procs)]
     for p in ps:
         p.start()
     model = shared.model(arch)
@@ -212,6 +218,7 @@ def run(cfg: dict, roots_per_step: int, steps: int, warmup: int, procs: int = No
     try:
         for s in range(wl.steps):
             a = time.perf_counter()
+            ctr.value = 0
             bar.wait()
             bar.wait()
             sync_and_update([model], accs, wl.B, 0.1)

@@ -66,6 +66,7 @@ def grads_bf16(st, label, P, tc):
         self_pos, dpos, spos, deg = st["steps"][k - 1]
         dz = dh * (st["zs"][k - 1] > 0.0)
         G.W[k - 1][...] = st["aggs"][k - 1].T @ _bf(dz)
+        G.b[k - 1][...] = dz.sum(0)  # from the bf16 chain too (dh = bf16 W_c @ bf16 dl, ...)
         # tensor-core dX (layers >= 2): bf16 dz times bf16 W
         dagg = _bf(dz) @ _bf(orig[k - 1]).T if orig[k - 1].shape[0] % 64 == 0 else dz @ orig[k - 1].T
         prev = np.zeros_like(st["h"][k - 1])
