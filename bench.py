@@ -161,7 +161,7 @@ def parity_block(g, cfg, perm, it, B, n_check=256):
     from oracle import model as OM
     from oracle.cpu_bench import LazyGraphSampler
     from oracle.graphgen import GraphSpec as OSpec
-    from oracle.rng import chain
+    from oracle.rng import chain, mix64
     from paper_2409_00657_b200.engine import BUILD_CTAS_PER_SM
     from paper_2409_00657_b200.sampler import GroupBuilder, MicrographBatch, MicrographBuilder
     fo = tuple(cfg["fanout"])
@@ -180,7 +180,8 @@ def parity_block(g, cfg, perm, it, B, n_check=256):
     got = batch.micrographs(rh, h)
     spec = OSpec(n=cfg["n"], avg_deg=cfg["avg_deg"], beta=cfg["beta"], p_in=cfg["p_in"],
                  n_blocks=cfg["n_blocks"], d_cap=cfg["d_cap"], seed=cfg["seed"])
-    want = LazyGraphSampler(spec).micrographs(rh, fo, [chain(st, int(r)) for r in rh])
+    # stream_key(seed, epoch, it, root) = mix64(chain(seed, epoch, it) ^ root) (sampler.py:52-54)
+    want = LazyGraphSampler(spec).micrographs(rh, fo, [mix64(st ^ int(r)) for r in rh])
     bad = 0
     for i, (m, w) in enumerate(zip(got, want)):
         ok = (all(np.array_equal(x, y) for x, y in zip(m.layers, w.layers))

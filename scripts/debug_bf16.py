@@ -62,3 +62,38 @@ for i, r in enumerate(roots.tolist()[:32]):
 out = {k: (np.max(np.array(v), 0).tolist() if v else None) for k, v in errs.items()}
 print(json.dumps(out))
 json.dump(out, open("gpurun_out/debug_bf16.json", "w"))
+
+# --- pinpoint: device operands and the dh GEMM, in torch from the device's own buffers
+n = len(roots)
+Cp = run.dl16.shape[1]
+dl16 = run.dl16[:n].float()
+wcp = run.wcp.float()                      # [H x Cp]
+dh_t = dl16 @ wcp.t()                      # torch fp32 of the same bf16 operands
+h2d = run.h[2][:n].float()
+dz_t = dh_t * (h2d > 0)
+dz_dev = run.dh[2][:n]
+pin = {"dh_gemm_vs_torch": rel(dz_dev.cpu().numpy(), dz_t.cpu().numpy()),
+       "lowp2_vs_f32dz": rel(run.lowp[mr[1]:mr[1] + n].float().cpu().numpy(), dz_dev.cpu().numpy()),
+       "wcp_vs_Wc": rel(wcp[:, :C].cpu().numpy(), _bf(P.Wc)),
+       "wcp_pad_zero": float(wcp[:, C:].abs().max().item()) if Cp > C else 0.0,
+       "dl16_vs_dlogits": rel(dl16[:, :C].cpu().numpy(), _bf(dl[:n, :C])),
+       "max_rows": list(run.max_rows), "Cp": Cp}
+print(json.dumps(pin))
+# --- the per-micrograph shim on one root
+from paper_2409_00657_b200 import micro as M
+m = o_sample(off, tgt, int(roots[0]), fo, stream_key(sseed, 0, 3, int(roots[0])), draw=OK.sample_frontier_nb)
+x = OK.feature_rows(m.vertices, D, feature_state(seed))
+m32 = init_model(arch, D, H, 2, C, mseed)
+one = M._OneRoot(m, x, m32)
+one.run("hg_forward")
+torch.cuda.synchronize()
+r = one.runner
+t = r.builder.tensors
+shim = {"totals": t["totals"].cpu().tolist(), "need0": t["need_ids"][0][:8].cpu().tolist(),
+        "agg1_abs": float(r.agg[1][:int(t["totals"][1])].abs().max()),
+        "h1_abs": float(r.h[1][:int(t["totals"][1])].abs().max()),
+        "h2_abs": float(r.h[2][:1].abs().max()), "logits": r.logits[0, :4].cpu().tolist(),
+        "table_abs": float(r.table.table.abs().max()), "feat_row": r.desc.feat_row,
+        "features": r.desc.features, "table_ptr": r.table.table.data_ptr(),
+        "act_dtype": r.desc.act_dtype, "use_tc": r.desc.use_tc}
+print(json.dumps(shim))

@@ -33,7 +33,7 @@ from bench import CONFIGS
 from oracle import model as OM
 from oracle.cpu_bench import LazyGraphSampler
 from oracle.graphgen import GraphSpec as OSpec, rows_csr
-from oracle.rng import chain
+from oracle.rng import chain, mix64
 
 from bf16_oracle import errors, oracle_cell
 
@@ -161,7 +161,7 @@ def _sampling_case(name, roots_per_batch, batches, n_hubs, first_it):
     gb.check()
     for b, it in enumerate(its):
         rh = roots[b].cpu().numpy()
-        keys = [chain(states[b], int(r)) for r in rh]
+        keys = [mix64(states[b] ^ int(r)) for r in rh]
         from paper_2409_00657_b200.sampler import MicrographBatch
         batch = MicrographBatch(len(fo), R, builders[b].tensors)
         stats[f"group_it{it}"] = _compare(batch, rh, keys, fo, oracle, f"{name} group it {it}")
@@ -171,11 +171,11 @@ def _sampling_case(name, roots_per_batch, batches, n_hubs, first_it):
     torch.cuda.synchronize()
     hb.check()
     hh = hubs.cpu().numpy()
-    hkeys = [chain(states[0], int(r)) for r in hh]
+    hkeys = [mix64(states[0] ^ int(r)) for r in hh]
     stats["hubs"] = _compare(batch, hh, hkeys, fo, oracle, f"{name} hubs")
     stats["hubs"]["min_root_degree"] = int(g.degrees()[hubs].min())
     stats["rows"] = _touched_rows_match(g, oracle, fo, np.concatenate([roots[0].cpu().numpy()[:256], hh]),
-                                        [chain(states[0], int(r)) for r in
+                                        [mix64(states[0] ^ int(r)) for r in
                                          np.concatenate([roots[0].cpu().numpy()[:256], hh])])
     _report(f"sampling_{name}", stats)
     return stats
@@ -245,7 +245,7 @@ def test_cfg4_group_loop_matches_oracle():
     for it in range(ITERS):
         roots = perm[it * B:(it + 1) * B]
         st = _iter_state(seed, 0, it)
-        micros = oracle.micrographs(roots, fo, [chain(st, int(r)) for r in roots])
+        micros = oracle.micrographs(roots, fo, [mix64(st ^ int(r)) for r in roots])
         losses, Gr = oracle_cell(None, None, roots, fo, sseed, (0, it), P, D, fstate, lseed, C,
                                  bf16_feats=True, tc=True, micros=micros)
         o_loss[it] = float(losses.sum())

@@ -8,7 +8,7 @@ from oracle import engine as OE
 from oracle import kernels as OK
 from oracle import model as OM
 from oracle.graphgen import GraphSpec as OSpec, build_csr, build_tables
-from oracle.rng import chain
+from oracle.rng import chain, mix64
 from oracle.sampler import sample_micrograph as o_sample, stream_key
 
 pytestmark = pytest.mark.gpu
@@ -241,7 +241,7 @@ def test_warp_build_matches_cta_build_and_oracle(P, fo, cps):
         st = state if b == 0 else chain(state, 1)
         rb = roots[b * R:(b + 1) * R]
         for r, m in zip(rb.tolist(), bf.micrographs(rb, hf)):
-            want = o_sample(off, tgt, r, fo, chain(st, r), draw=OK.sample_frontier_nb)
+            want = o_sample(off, tgt, r, fo, mix64(st ^ r), draw=OK.sample_frontier_nb)
             assert all(np.array_equal(a, w) for a, w in zip(m.layers, want.layers))
             assert all(np.array_equal(d1, d2) and np.array_equal(s1, s2)
                        for (d1, s1), (d2, s2) in zip(m.pairs, want.pairs))
@@ -288,7 +288,7 @@ def test_warp_build_self_loops_isolated_and_device_counts(P):
         rb = roots[b * 64:b * 64 + cnt]
         got = bf.micrographs(rb)
         for r, m in zip(rb.tolist(), got):
-            want = o_sample(off, tgt, r, fo, chain(state if b == 0 else chain(state, 1), r))
+            want = o_sample(off, tgt, r, fo, mix64((state if b == 0 else chain(state, 1)) ^ r))
             assert all(np.array_equal(a, w) for a, w in zip(m.layers, want.layers))
             assert np.array_equal(m.vertices, want.vertices)
         # slots past the device count: empty micrographs
