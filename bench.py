@@ -340,7 +340,8 @@ def _run_ours(args, cfg, dev):
     torch.cuda.synchronize()
     setup_s = time.time() - t0
     K, W = args.steps, args.warmup
-    if G > 1:  # warm-up covers two eager steps and one replay of each group graph
+    W_req = W
+    if G > 1:  # warm-up also covers two eager steps and one replay of each group graph
         W = max(W, 2 + 2 * G)
     if 2 * W + 3 * K + 2 * G + 1 > iters:
         raise SystemExit("epoch too short for the requested steps")
@@ -477,7 +478,7 @@ def _run_ours(args, cfg, dev):
             traffic = None
     line = {
         "metric": "seeds_per_sec", "value": round(value, 1), "unit": "seeds/s",
-        "n_gpus": 1, "steps": K, "warmup": W, "ms_per_step": round(ms / K, 4),
+        "n_gpus": 1, "steps": K, "warmup": W_req, "ms_per_step": round(ms / K, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (GPU-generated graph, keyed features/labels/weights)",
         "config": {"workload": cfg["workload"], "global_batch": B, "run_ahead_group": G,
@@ -498,7 +499,8 @@ def _run_ours(args, cfg, dev):
                      "avg_launch_us": round(agg_avg_s * 1e6, 2)},
         "roofline_sampler": sampler_roof,
         "kernel_ms_per_launch": {k: round(v[0] / max(v[1], 1), 4) for k, v in sites.items()},
-        "loop": {"cuda_graphs": graph_on, "group": G,
+        "loop": {"cuda_graphs": graph_on, "group": G, "replays_timed": replays,
+                 "warmup_steps_run": W,
                  "launches_per_graph": per_graph,
                  "eager_ms_per_step": round(eager_ms / n_prof, 4),
                  "note": "value/ms_per_step: graph replays (a replay trains a group of G "

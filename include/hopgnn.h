@@ -360,6 +360,10 @@ typedef struct {
   const int32_t* labels;
 } hg_step_desc;
 
+/* Step variant (process-wide): 1 = softmax-CE fused into the tcgen05 head
+ * GEMM's epilogue (C <= 192), 0 (default) = head GEMM + separate softmax-CE. */
+int hg_set_fused_head(int32_t on);
+
 /* Peer memory (one process per GPU): device allocations whose CUDA IPC
  * handles (64 bytes) other ranks map; and the reference pre-gather byte
  * accounting of an iteration's remote vertices without a host sync

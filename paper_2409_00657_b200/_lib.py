@@ -124,6 +124,7 @@ SIGNATURES = {
                           C.POINTER(MgBatch), V, I32, V],
     "hg_mg_build_group_sharded": [C.POINTER(CsrShards), I64, V, I32, I32, V, V, I32,
                                   C.POINTER(MgLayout), V, C.POINTER(MgBatch), V, I32, V],
+    "hg_set_fused_head": [I32],
     "hg_train_step": [C.POINTER(StepDesc), I32, V],
     "hg_forward": [C.POINTER(StepDesc), I32, V],
     "hg_sgd_update": [V, V, V, I64, C.c_float, C.c_float, V],

@@ -623,7 +623,9 @@ k_scatter_top(const float* __restrict__ dagg, int ld, const int32_t* __restrict_
   float cs[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) cs[j] = 0.f;
-  for (int r = blockIdx.x; r < n_roots; r += gridDim.x) {
+  // warp per root (a root's <= 1 + f1 need[L-1] rows), grid-stride: few CTAs,
+  // so the per-CTA bias-gradient atomics below stay uncontended
+  for (int r = blockIdx.x * 8 + warp; r < n_roots; r += gridDim.x * 8) {
     const int q0 = need_off_p[r], nq = need_off_p[r + 1] - q0;
     const int rowL = need_off_c[r];
     if (nq == 0 || need_off_c[r + 1] - rowL != 1) continue;  // empty (capacity) micrograph
@@ -642,7 +644,7 @@ k_scatter_top(const float* __restrict__ dagg, int ld, const int32_t* __restrict_
         }
       }
     }
-    for (int i = warp; i < nq; i += 8) {
+    for (int i = 0; i < nq; ++i) {
       const int u = q0 + i;
       if (!lane_on) continue;
       float v[8], hv[8];
@@ -793,49 +795,70 @@ __global__ void k_zero_rows(float* __restrict__ x, const int32_t* __restrict__ n
 }
 
 // Where each parameter's bf16 operand copies live (the step's layout).
-struct LowpMap {
-  int L, H, C, Cp;
-  int64_t off[HG_MAX_LAYERS + 1];  // flat offset of W_k
-  int in[HG_MAX_LAYERS + 1];
-  bf16* Wlp[HG_MAX_LAYERS + 1];    // [H x in_k]  (Wᵀ, K-major B of the forward GEMM)
-  bf16* Wb[HG_MAX_LAYERS + 1];     // [in_k x H]  (W, K-major B of the dX GEMM) or null
-  int64_t off_c;                   // flat offset of W_c [H x C]
-  bf16* WcT;                       // [C x H]
-  bf16* Wcp;                       // [H x Cp]
+// SGD + gradient reset, then the parameters' bf16 operand copies, in one
+// launch over 32 x 32 tiles of every weight matrix (f32 reads/writes and the
+// straight bf16 copy coalesced along columns; the transposed copy staged in
+// shared memory so its writes are coalesced too), plus elementwise blocks for
+// the biases.  Replaces three transposes and a pad per step.
+struct SgdMat {
+  int64_t off;        // flat offset of the matrix [rows x cols] (row-major)
+  int rows, cols;
+  bf16* tdst;         // transposed bf16 copy [cols x rows] (ld tld) or null
+  int64_t tld;
+  bf16* sdst;         // straight bf16 copy [rows x cols] (ld sld) or null
+  int64_t sld;
+  int tiles_c, tile0; // column tiles; first tile index of this matrix
+};
+struct SgdPlan {
+  int n_mats, n_tiles;
+  SgdMat m[HG_MAX_LAYERS + 1];
+  int64_t plain_lo, plain_hi;  // elementwise range (the biases)
 };
 
-// SGD + gradient reset, then the parameter's bf16 copies (one pass over the
-// flat buffer instead of three transposes and a pad per step).
-__global__ void k_sgd_refresh(float* __restrict__ p, float* __restrict__ g, int64_t n, float lr,
-                              float inv_batch, int update, LowpMap m) {
+__global__ void __launch_bounds__(256)
+k_sgd_refresh(float* __restrict__ p, float* __restrict__ g, float lr, float inv_batch, int update,
+              SgdPlan P) {
   pdl_trigger();
   pdl_wait();
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float v = p[i];
-    if (update) {
-      v -= lr * (g[i] * inv_batch);
-      p[i] = v;
-      g[i] = 0.f;
-    }
-    const bf16 b = __float2bfloat16_rn(v);
-    if (i >= m.off_c) {
-      const int64_t j = i - m.off_c;
-      if (j < (int64_t)m.H * m.C) {
-        const int r = (int)(j / m.C), c = (int)(j % m.C);
-        m.WcT[(int64_t)c * m.H + r] = b;
-        m.Wcp[(int64_t)r * m.Cp + c] = b;
+  const int t = blockIdx.x;
+  if (t >= P.n_tiles) {  // biases: elementwise
+    for (int64_t i = P.plain_lo + (int64_t)(t - P.n_tiles) * blockDim.x + threadIdx.x;
+         i < P.plain_hi; i += (int64_t)(gridDim.x - P.n_tiles) * blockDim.x) {
+      if (update) {
+        p[i] -= lr * (g[i] * inv_batch);
+        g[i] = 0.f;
       }
-      continue;
     }
-    for (int k = 1; k <= m.L; ++k) {
-      const int64_t j = i - m.off[k];
-      if (j < 0 || j >= (int64_t)m.in[k] * m.H) continue;
-      const int r = (int)(j / m.H), c = (int)(j % m.H);
-      m.Wlp[k][(int64_t)c * m.in[k] + r] = b;
-      if (m.Wb[k]) m.Wb[k][j] = b;
-      break;
+    return;
+  }
+  __shared__ bf16 tile[32][34];
+  int mi = 0;
+  while (mi + 1 < P.n_mats && P.m[mi + 1].tile0 <= t) ++mi;
+  const SgdMat& M = P.m[mi];
+  const int lt = t - M.tile0, tr = lt / M.tiles_c, tc = lt % M.tiles_c;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int r = tr * 32 + ty + 8 * j, c = tc * 32 + tx;
+    if (r < M.rows && c < M.cols) {
+      const int64_t i = M.off + (int64_t)r * M.cols + c;
+      float v = p[i];
+      if (update) {
+        v -= lr * (g[i] * inv_batch);
+        p[i] = v;
+        g[i] = 0.f;
+      }
+      const bf16 b = __float2bfloat16_rn(v);
+      if (M.sdst) M.sdst[(int64_t)r * M.sld + c] = b;
+      tile[ty + 8 * j][tx] = b;
     }
+  }
+  if (!M.tdst) return;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = tc * 32 + ty + 8 * j, r = tr * 32 + tx;
+    if (r < M.rows && c < M.cols) M.tdst[(int64_t)c * M.tld + r] = tile[tx][ty + 8 * j];
   }
 }
 
@@ -961,15 +984,11 @@ static void scatter_root_attrs() {
   done = true;
 }
 
-// A/B switch read once per process: HG_FUSED_HEAD=1 puts the softmax-CE in the
-// tcgen05 head GEMM's epilogue (umma_head_ce; tested, measured slower on B200)
-static bool fused_head_on() {
-  static const bool on = [] {
-    const char* e = getenv("HG_FUSED_HEAD");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
+// Variant switch (hg_set_fused_head): 1 puts the softmax-CE in the tcgen05 head
+// GEMM's epilogue (umma_head_ce; tested, measured slower on B200 -- the head
+// GEMM has only n_roots / 128 CTAs, the separate kernel a warp per root).
+static int g_fused_head = 0;
+static bool fused_head_on() { return g_fused_head != 0; }
 
 // bf16 dz operand of layer k (per-layer region when lowp_layered)
 static inline bf16* dz_lowp(const hg_step_desc* d, int k) {
@@ -1154,7 +1173,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
       // top layer: per-row map, no scatter (k_scatter_top)
       const bool tc_dx = tc && d->in_dim[k - 1] % 64 == 0 && d->Wb[k - 1];
       const bool want_f32 = !tc || (k - 1 >= 2 && !tc_dx);
-      const int grid = std::max(1, std::min(n_roots, num_sms() * 8));
+      const int grid = std::max(1, std::min((n_roots + 7) / 8, num_sms() * 2));
       count_launch();
       auto kern = sage ? k_scatter_top<true, T> : k_scatter_top<false, T>;
       launch_pdl(kern, dim3(grid), dim3(256), 0, s, (const float*)d->dagg, d->in_dim[k],
@@ -1219,6 +1238,11 @@ static int validate(const hg_step_desc* d, int n_roots) {
 
 using namespace hg;
 
+extern "C" int hg_set_fused_head(int32_t on) {
+  g_fused_head = on ? 1 : 0;
+  return HG_OK;
+}
+
 extern "C" int hg_train_step(const hg_step_desc* d, int32_t n_roots, void* stream) {
   int st = validate(d, n_roots);
   if (st) return st;
@@ -1271,26 +1295,40 @@ extern "C" int hg_sgd_refresh(const hg_step_desc* d, float* params, float* grads
                               float lr, float inv_batch, int32_t update, void* stream) {
   if (n <= 0) return HG_OK;
   if (!d->WcT || !d->Wcp) return hg_fail(HG_ECONFIG, "hg_sgd_refresh needs the bf16 head operands");
-  LowpMap m{};
-  m.L = d->n_layers;
-  m.H = d->hidden;
-  m.C = d->n_classes;
-  m.Cp = (m.C + 63) / 64 * 64;
-  for (int k = 1; k <= m.L; ++k) {
-    m.off[k] = d->W[k] - params;
-    m.in[k] = d->in_dim[k];
-    m.Wlp[k] = (bf16*)d->Wlp[k];
-    m.Wb[k] = k >= 2 ? (bf16*)d->Wb[k] : nullptr;
-    if (m.off[k] < 0 || m.off[k] + (int64_t)m.in[k] * m.H > n)
+  const int L = d->n_layers, H = d->hidden, C = d->n_classes, Cp = (C + 63) / 64 * 64;
+  SgdPlan P{};
+  int tiles = 0;
+  auto add = [&](int64_t off, int rows, int cols, bf16* tdst, int64_t tld, bf16* sdst,
+                 int64_t sld) {
+    SgdMat& M = P.m[P.n_mats++];
+    M.off = off; M.rows = rows; M.cols = cols;
+    M.tdst = tdst; M.tld = tld; M.sdst = sdst; M.sld = sld;
+    M.tiles_c = (cols + 31) / 32;
+    M.tile0 = tiles;
+    tiles += ((rows + 31) / 32) * M.tiles_c;
+  };
+  for (int k = 1; k <= L; ++k) {
+    const int64_t off = d->W[k] - params;
+    if (off < 0 || off + (int64_t)d->in_dim[k] * H > n)
       return hg_fail(HG_ECONFIG, "layer %d weights outside the flat parameter buffer", k);
+    // Wlp: Wᵀ [H x in_k] (K-major B of the forward GEMM); Wb: W (B of the dX GEMM, k >= 2)
+    add(off, d->in_dim[k], H, (bf16*)d->Wlp[k], d->in_dim[k], k >= 2 ? (bf16*)d->Wb[k] : nullptr, H);
   }
-  m.off_c = d->Wc - params;
-  m.WcT = (bf16*)d->WcT;
-  m.Wcp = (bf16*)d->Wcp;
-  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  const int64_t off_c = d->Wc - params;
+  if (off_c < 0 || off_c + (int64_t)H * C > n)
+    return hg_fail(HG_ECONFIG, "classifier outside the flat parameter buffer");
+  add(off_c, H, C, (bf16*)d->WcT, H, (bf16*)d->Wcp, Cp);  // WcT [C x H], Wcp [H x Cp]
+  P.n_tiles = tiles;
+  // the biases sit between the last layer weight and the classifier
+  P.plain_lo = d->b[1] - params;
+  P.plain_hi = d->b[L] - params + H;
+  if (P.plain_lo < 0 || P.plain_hi > n || P.plain_hi < P.plain_lo)
+    return hg_fail(HG_ECONFIG, "biases outside the flat parameter buffer");
+  const int grid = tiles + 4;
   count_launch();
   prof_begin(PROF_SGD, (cudaStream_t)stream);
-  launch_pdl(k_sgd_refresh, dim3(grid), dim3(256), 0, (cudaStream_t)stream, params, grads, n, lr, inv_batch, update, m);
+  launch_pdl(k_sgd_refresh, dim3(grid), dim3(256), 0, (cudaStream_t)stream, params, grads, lr,
+             inv_batch, update, P);
   prof_end(PROF_SGD, (cudaStream_t)stream);
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;

@@ -962,30 +962,33 @@ k_mg_scan(const int32_t* __restrict__ ws, int n_roots, MgCarve c, MgOuts outs) {
   }
 }
 
-__global__ void __launch_bounds__(128)
-k_mg_finalize(const int32_t* __restrict__ ws, int n_roots, MgCarve c, MgOuts outs) {
-  // CTA per root of the whole group; root r belongs to batch r / n_roots
-  const int r = blockIdx.x % n_roots;
-  const hg_mg_batch& out = outs.b[blockIdx.x / n_roots];
+__global__ void __launch_bounds__(256)
+k_mg_finalize(const int32_t* __restrict__ ws, int n_roots, int total, MgCarve c, MgOuts outs) {
+  // warp per root of the whole group; root g belongs to batch g / n_roots
+  const int gid = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (gid >= total) return;
+  const int lane = threadIdx.x & 31;
+  const int r = gid % n_roots;
+  const hg_mg_batch& out = outs.b[gid / n_roots];
   const int L = c.L;
-  const int32_t* w = ws + (size_t)blockIdx.x * c.ws_root_ints;
+  const int32_t* w = ws + (size_t)gid * c.ws_root_ints;
   for (int k = 0; k <= L; ++k) {
     const int base = out.need_off[k][r];
     const int nk = w[c.ws_cnt + k];
-    for (int a = threadIdx.x; a < nk; a += blockDim.x) {
+    for (int a = lane; a < nk; a += 32) {
       out.need_ids[k][base + a] = w[c.ws_need[k] + a];
       out.in_layer[k][base + a] = (int8_t)w[c.ws_inl[k] + a];
     }
     if (k == 0) continue;
     const int pbase = out.pair_off[k][r];
     const int prev_base = out.need_off[k - 1][r];
-    for (int a = threadIdx.x; a < nk; a += blockDim.x) {
+    for (int a = lane; a < nk; a += 32) {
       out.self_pos[k][base + a] = prev_base + w[c.ws_self[k] + a];
       out.nbr_off[k][base + a] = pbase + w[c.ws_rowoff[k] + a];
       if (k == 1 && out.self_vid1) out.self_vid1[base + a] = w[c.ws_need[1] + a];
     }
     const int pk = w[c.ws_cnt + L + k];
-    for (int t = threadIdx.x; t < pk; t += blockDim.x) {
+    for (int t = lane; t < pk; t += 32) {
       const int q = w[c.ws_nbr[k] + t];
       out.nbr_idx[k][pbase + t] = prev_base + q;
       if (k == 1 && out.nbr_vid1) out.nbr_vid1[pbase + t] = w[c.ws_need[0] + q];
@@ -1119,11 +1122,7 @@ static int build_group(const CsrView& g, int64_t n_vertices,
   const int total = n_roots * n_batches;
   count_launch(3);
   prof_begin(PROF_BUILD, s);
-  static const int cps_env = [] {  // A/B override of the resident build CTAs per SM
-    const char* e = getenv("HG_BUILD_CTAS_PER_SM");
-    return e ? atoi(e) : -1;
-  }();
-  const int cps = cps_env >= 0 ? cps_env : ctas_per_sm;
+  const int cps = ctas_per_sm;
   int grid = total;
   if (cps > 0) {
     int dev = 0, nsm = 148;
@@ -1146,7 +1145,7 @@ static int build_group(const CsrView& g, int64_t n_vertices,
   HG_CUDA_TRY(cudaGetLastError());
   k_mg_scan<<<n_batches, 1024, 0, s>>>(ws, n_roots, c, o);
   HG_CUDA_TRY(cudaGetLastError());
-  k_mg_finalize<<<total, 128, 0, s>>>(ws, n_roots, c, o);
+  k_mg_finalize<<<(total + 7) / 8, 256, 0, s>>>(ws, n_roots, total, c, o);
   prof_end(PROF_BUILD, s);
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;

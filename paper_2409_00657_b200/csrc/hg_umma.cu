@@ -556,11 +556,6 @@ int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
       return n > 0 ? n : 148;
     }();
     while (bn > 64 && ctas(bn) < sms / 2) bn = bn == 192 ? 128 : bn / 2;
-    static const int bn_cap = [] {  // A/B: HG_UMMA_BN_MAX=128|64 caps the N tile
-      const char* e = getenv("HG_UMMA_BN_MAX");
-      return e ? atoi(e) : 256;
-    }();
-    while (bn > 64 && bn > bn_cap) bn = bn == 192 ? 128 : bn / 2;
   }
   if (lda % 8 || ldb % 8) return hg_fail(HG_ECONFIG, "umma leading dims must be multiples of 8");
   CUtensorMap ma, mb;

@@ -262,9 +262,12 @@ class GroupLoop:
 
     def run_eager(self, it: int) -> None:
         """The body of one replay for iterations it..it+G-1 launched eagerly on
-        the current stream (build group -> gather group -> G steps): the
-        profiling pass, where per-kernel CUDA-event sites need real launches.
-        Leaves the loop unpositioned."""
+        the current stream, with the replay's configuration (build grid capped
+        at BUILD_CTAS_PER_SM, grouped gather, steps on the bf16 operands the
+        fused SGD + refresh keeps current): the profiling pass, where per-kernel
+        CUDA-event sites need real launches.  The branches run one after the
+        other here (in the replay the build overlaps training).  Leaves the
+        loop unpositioned."""
         tr = self.tr
         cur = torch.cuda.current_stream(tr.device)
         cur.wait_stream(self.side)
@@ -273,12 +276,23 @@ class GroupLoop:
         B, G = tr.B, self.G
         gb.roots.copy_(tr.perm[it * B:(it + G) * B])
         gb.keys.copy_(tr.states[it:it + G])
-        gb.build(tr.graph, stream=s)
+        gb.build(tr.graph, stream=s, ctas_per_sm=BUILD_CTAS_PER_SM)
         _lib.call("hg_step_prologue_group", self.descp[0], G, 1, s)
         m = tr.model
+        r0 = self.sets[0][0]
+        if r0.tc:  # operands current before the first step (the replays leave them so)
+            _lib.call("hg_sgd_refresh", C.byref(r0.desc), m.flat.data_ptr(), m.grad.data_ptr(),
+                      m.flat.numel(), 0.0, 1.0, 0, s)
         for r in self.sets[0]:
-            _lib.call("hg_train_step", C.byref(r.desc), B, s)
-            m.sgd(tr.lr, B, stream=s)
+            if r.tc:
+                r.desc.lowp_fresh = 1
+                _lib.call("hg_train_step", C.byref(r.desc), B, s)
+                _lib.call("hg_sgd_refresh", C.byref(r.desc), m.flat.data_ptr(),
+                          m.grad.data_ptr(), m.flat.numel(), float(tr.lr), 1.0 / B, 1, s)
+                r.desc.lowp_fresh = 0
+            else:
+                _lib.call("hg_train_step", C.byref(r.desc), B, s)
+                m.sgd(tr.lr, B, stream=s)
 
     def replay(self) -> int:
         """Train the positioned group; returns the parity replayed."""

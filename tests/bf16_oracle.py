@@ -16,7 +16,12 @@ from oracle.sampler import sample_micrograph as o_sample, stream_key
 
 
 def _bf(a):
-    return torch.from_numpy(np.asarray(a, np.float32)).to(torch.bfloat16).double().numpy()
+    """float64 -> float32 -> bf16 (round to nearest even) -> float64, in numpy
+    (no torch: the helpers also run in forked pool workers)."""
+    x = np.ascontiguousarray(np.asarray(a, np.float64).astype(np.float32))
+    u = x.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32).astype(np.float64)
 
 
 def forward_bf16(m, x_rows, P, tc=False):
@@ -46,9 +51,16 @@ def forward_bf16(m, x_rows, P, tc=False):
                 logits=h[-1][0] @ (_bf(P.Wc) if tc else P.Wc))
 
 
-def grads_bf16(st, label, P, tc):
-    """OM.loss_and_grads; on the tensor-core path dW_k = agg_kᵀ bf16(dz_k)."""
+def grads_bf16(st, label, P, tc, masks=None):
+    """OM.loss_and_grads; on the tensor-core path dW_k = agg_kᵀ bf16(dz_k).
+    masks: optional per-layer ReLU masks (need[k] x H booleans) to use instead
+    of z_k > 0 -- the device's own masks, so a pre-activation that lands on the
+    other side of 0 after a one-ulp bf16 difference upstream does not flip a
+    whole gradient term (the 'mask-forced' comparison)."""
     if not tc:
+        if masks is None:
+            return OM.loss_and_grads(st, label, P)
+        st = dict(st, zs=[np.where(m, 1.0, -1.0) for m in masks])
         return OM.loss_and_grads(st, label, P)
     orig = [w.copy() for w in P.W]
     # run the exact backward, then redo the weight gradients with bf16 dz
@@ -64,7 +76,7 @@ def grads_bf16(st, label, P, tc):
     dh[0] = _bf(P.Wc) @ _bf(dl)
     for k in range(L, 0, -1):
         self_pos, dpos, spos, deg = st["steps"][k - 1]
-        dz = dh * (st["zs"][k - 1] > 0.0)
+        dz = dh * (masks[k - 1] if masks is not None else (st["zs"][k - 1] > 0.0))
         G.W[k - 1][...] = st["aggs"][k - 1].T @ _bf(dz)
         G.b[k - 1][...] = dz.sum(0)  # from the bf16 chain too (dh = bf16 W_c @ bf16 dl, ...)
         # tensor-core dX (layers >= 2): bf16 dz times bf16 W
@@ -85,7 +97,7 @@ def grads_bf16(st, label, P, tc):
 
 
 def oracle_cell(off, tgt, roots, fo, sseed, it_key, P, D, fstate, lseed, C, bf16_feats=False,
-                tc=False, micros=None):
+                tc=False, micros=None, masks=None):
     """Oracle gradients; with bf16_feats the oracle rounds features, aggregates and
     activations to bf16 where the device stores them (arithmetic stays float64).
     micros: pre-sampled micrographs (one per root), else sampled from (off, tgt)."""
@@ -97,7 +109,9 @@ def oracle_cell(off, tgt, roots, fo, sseed, it_key, P, D, fstate, lseed, C, bf16
         x = OK.feature_rows(m.vertices, D, fstate)
         st = forward_bf16(m, x, P, tc) if bf16_feats else OM.forward(m, x, P)
         lab = int(OM.labels([r], C, lseed)[0])
-        loss, g = grads_bf16(st, lab, P, tc) if bf16_feats else OM.loss_and_grads(st, lab, P)
+        mk = masks[i] if masks is not None else None
+        loss, g = (grads_bf16(st, lab, P, tc, mk) if bf16_feats
+                   else OM.loss_and_grads(st, lab, P))
         OM.add_into(G, g)
         losses.append(loss)
     return np.array(losses), G
@@ -109,3 +123,21 @@ def errors(got, want):
     scale = max(np.abs(want).max(), 1e-30)
     return (float(np.abs(got - want).max() / scale),
             float(np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30)))
+
+
+def _cell_chunk(args):
+    micros, roots, P, D, fstate, lseed, C, tc = args
+    return oracle_cell(None, None, roots, None, None, None, P, D, fstate, lseed, C,
+                       bf16_feats=True, tc=tc, micros=micros)
+
+
+def oracle_cell_parallel(pool, micros, roots, P, D, fstate, lseed, C, tc=True, parts=16):
+    """oracle_cell (bf16 storage points) with the roots split over a process pool;
+    per-root losses in root order and the summed gradients."""
+    idx = np.array_split(np.arange(len(roots)), parts)
+    jobs = [([micros[i] for i in ix], roots[ix], P, D, fstate, lseed, C, tc) for ix in idx if len(ix)]
+    res = pool.map(_cell_chunk, jobs)
+    G = P.zeros()
+    for _, g in res:
+        OM.add_into(G, g)
+    return np.concatenate([l for l, _ in res]), G

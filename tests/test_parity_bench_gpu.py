@@ -35,7 +35,7 @@ from oracle.cpu_bench import LazyGraphSampler
 from oracle.graphgen import GraphSpec as OSpec, rows_csr
 from oracle.rng import chain, mix64
 
-from bf16_oracle import errors, oracle_cell
+from bf16_oracle import errors, oracle_cell, oracle_cell_parallel
 
 pytestmark = pytest.mark.gpu
 
@@ -242,14 +242,15 @@ def test_cfg4_group_loop_matches_oracle():
     P = OM.init_params(arch, D, H, len(fo), C, mseed)
     sseed, lseed, fstate = chain(seed, 0x06), chain(seed, 0x04), feature_state(seed)
     o_loss = {}
-    for it in range(ITERS):
-        roots = perm[it * B:(it + 1) * B]
-        st = _iter_state(seed, 0, it)
-        micros = oracle.micrographs(roots, fo, [mix64(st ^ int(r)) for r in roots])
-        losses, Gr = oracle_cell(None, None, roots, fo, sseed, (0, it), P, D, fstate, lseed, C,
-                                 bf16_feats=True, tc=True, micros=micros)
-        o_loss[it] = float(losses.sum())
-        OM.sgd_step(P, Gr, B, 0.1)
+    import multiprocessing as mp
+    with mp.get_context("fork").Pool(min(16, os.cpu_count() or 1)) as pool:
+        for it in range(ITERS):
+            roots = perm[it * B:(it + 1) * B]
+            st = _iter_state(seed, 0, it)
+            micros = oracle.micrographs(roots, fo, [mix64(st ^ int(r)) for r in roots])
+            losses, Gr = oracle_cell_parallel(pool, micros, roots, P, D, fstate, lseed, C, tc=True)
+            o_loss[it] = float(losses.sum())
+            OM.sgd_step(P, Gr, B, 0.1)
     loss_err = max(abs(dev_loss[it] - o_loss[it]) / abs(o_loss[it]) for it in dev_loss)
     rep = {"iterations": ITERS, "group": G, "roots_per_iteration": B,
            "loss_max_rel": loss_err, "loss_tol": LOOP_LOSS_TOL, "delta": {}}
