@@ -530,7 +530,7 @@ def run_distributed(args, cfg):
     import torch
     import torch.distributed as dist
     from paper_2409_00657_b200 import _lib
-    from paper_2409_00657_b200.distributed import (MicrographTrainer,
+    from paper_2409_00657_b200.distributed import (DistGroupLoop, MicrographTrainer,
                                                    model_centric_feature_rows)
     from paper_2409_00657_b200.featstore import FEATURE, GRADIENT, MODEL
     from paper_2409_00657_b200.graph import GraphSpec, PartitionMap, generate
@@ -551,6 +551,12 @@ def run_distributed(args, cfg):
     blocks = (np.arange(spec.n, dtype=np.int64) * spec.n_blocks) // spec.n
     part = PartitionMap((blocks * S) // spec.n_blocks, S, dev)
     del blocks
+    if args.csr == "sharded":  # partitioned topology: this GPU keeps only its homed rows
+        from paper_2409_00657_b200.graph import ShardedGraph
+        full = g
+        g = ShardedGraph.from_graph(full, part, rank)
+        del full
+        torch.cuda.empty_cache()
     model = init_model(cfg["arch"], cfg["dim"], cfg["hidden"], len(cfg["fanout"]),
                        cfg["classes"], chain(cfg["seed"], 0x07), dev)
     B = cfg["batch"]
@@ -605,15 +611,25 @@ def run_distributed(args, cfg):
     traffic = torch.tensor([tr.traffic.total(), tr.traffic.feature_bytes,
                             tr.traffic.hop_bytes, tr.traffic.allreduce_bytes], device=dev)
     dist.all_reduce(traffic)
-    # per-kernel timing: the same loop eagerly for K more steps with event sites
-    tr.graphs = False
+    # per-kernel timing: the replayed loop's work run eagerly (branch after branch)
+    # for K more iterations with CUDA-event sites -- the grouped build, the group
+    # push + grouped layer-1 gather, the G train steps (DistGroupLoop.run_eager)
     if rank == 0:
         _lib.prof_enable(True)
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dist.barrier()
     p0.record()
-    for i in range(K):
-        tr.step(W + K + i, want_loss=False)
+    n_prof = K
+    if G > 1 and isinstance(tr._dgl, DistGroupLoop):
+        n_prof = max(1, K // G) * G
+        cs = torch.cuda.current_stream(dev).cuda_stream
+        for j in range(n_prof // G):
+            tr._dgl.run_eager(W + K + j * G, cs)
+    else:
+        tr.graphs = False
+        for i in range(K):
+            tr.step(W + K + i, want_loss=False)
+        tr.graphs = True
     p1.record()
     torch.cuda.synchronize()
     eager_ms = p0.elapsed_time(p1)
@@ -635,8 +651,13 @@ def run_distributed(args, cfg):
     agg_bytes = None
     if rank == 0:
         L_ = len(cfg["fanout"])
-        tot_ = tr.runners[0].builder.tensors["totals"].cpu().numpy()
-        agg_bytes = gather_bytes([(int(tot_[0]), int(tot_[1]), int(tot_[L_ + 1]))], cfg)
+        prof_runners = (tr._dgl.sets[0] if G > 1 and isinstance(tr._dgl, DistGroupLoop)
+                        else tr.runners[:1])  # the batches of the last profiled gather launch
+        sizes_ = []
+        for r_ in prof_runners:
+            tot_ = r_.builder.tensors["totals"].cpu().numpy()
+            sizes_.append((int(tot_[0]), int(tot_[1]), int(tot_[L_ + 1])))
+        agg_bytes = gather_bytes(sizes_, cfg)
     # end to end: same public step, loss read back every step (W2 untimed warm-up steps,
     # a whole number of groups so the timed steps start on a group boundary)
     W2 = -(-W // G) * G
@@ -694,7 +715,9 @@ def run_distributed(args, cfg):
                      "frac": round(ach / hbm_, 4) if ach else None, "traffic": None,
                      "peak_source": peak_kind_, "bytes_per_launch": agg_bytes,
                      "avg_launch_us": round(agg_us, 2),
-                     "note": "rank 0, eager pass; bytes from the last built batch"}
+                     "iterations_per_launch": len(sizes_) if rank == 0 else None,
+                     "note": "rank 0, eager pass of the replayed loop's work (grouped staged "
+                             "gather over G iterations); bytes from the profiled batches"}
         by_cat = led.bytes_by_category()
         per_iter_ref = sum(by_cat.values()) / K
         mc_feat_iter = float(mc.item()) * cfg["dim"] * 4 / n_mc
@@ -709,7 +732,7 @@ def run_distributed(args, cfg):
                        "fanout": list(cfg["fanout"]), "hidden": cfg["hidden"],
                        "run_ahead_group": G,
                        "parallelism": f"micrograph x{S} ({mode}; features sharded by planted "
-                                      "block, CSR replicated; remote rows "
+                                      f"block, CSR {args.csr}; remote rows "
                                       + ("pre-gathered by NCCL all-to-all)" if args.pregather
                                          else "read over NVLink by the gather kernel)"),
                        "l2": "inputs larger than L2"},
@@ -782,6 +805,9 @@ def main():
     ap.add_argument("--pregather", action="store_true",
                     help="multi-GPU: stage remote rows with NCCL all-to-all instead of NVLink "
                          "peer reads")
+    ap.add_argument("--csr", default="sharded", choices=["sharded", "replicated"],
+                    help="multi-GPU topology: CSR rows partitioned by home (remote rows read "
+                         "over NVLink in the builds) or a full copy per GPU")
     ap.add_argument("--mode", default="fused", choices=["fused", "faithful"],
                     help="multi-GPU model-hop payload (see distributed.py)")
     args = ap.parse_args()

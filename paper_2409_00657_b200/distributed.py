@@ -642,6 +642,39 @@ class DistGroupLoop:
     def replay(self, x: int) -> None:
         self.graphs[x].replay()
 
+    def run_eager(self, it: int, s) -> None:
+        """One replay's work for iterations it..it+G-1 launched eagerly on stream
+        s, branch after branch (build the group, pre-gather + grouped layer-1
+        gather, then the G train steps with all-reduce + SGD): the profiling
+        pass of bench.py, where per-kernel CUDA-event sites need real launches.
+        Collective: every rank runs it for the same `it`.  Leaves the loop
+        unpositioned (the next step re-positions it)."""
+        tr = self.tr
+        tr._g_it.fill_(it - 1)
+        tr._g_pg.fill_(it - 1)
+        self.build_ops(0, s)
+        self.gather_ops(0, s)
+        m = tr.model
+        total = tr.S * tr.B
+        r0 = self.sets[0][0]
+        if r0.tc:  # operands current before the first step (the replays leave them so)
+            _lib.call("hg_sgd_refresh", C.byref(r0.desc), m.flat.data_ptr(), m.grad.data_ptr(),
+                      m.flat.numel(), 0.0, 1.0, 0, s)
+        for r in self.sets[0]:
+            if r.tc:
+                r.desc.lowp_fresh = 1
+                _lib.call("hg_train_step", C.byref(r.desc), self.cap, s)
+                r.desc.lowp_fresh = 0
+                _lib.call("hg_allreduce_sgd_refresh", tr._comm, C.byref(r.desc),
+                          m.flat.data_ptr(), m.grad.data_ptr(), m.flat.numel(), float(tr.lr),
+                          1.0 / total, s)
+            else:
+                _lib.call("hg_train_step", C.byref(r.desc), self.cap, s)
+                _lib.call("hg_allreduce_sgd", tr._comm, m.flat.data_ptr(), m.grad.data_ptr(),
+                          m.flat.numel(), float(tr.lr), 1.0 / total, s)
+        tr._gnext = None
+        tr._gdone = None
+
     def check(self) -> None:
         for gb in self.gb:
             gb.check()

@@ -44,9 +44,8 @@ class SamplerConfig:
             raise ValueError("n_layers must be >= 1")
         if len(self.fanout) != self.n_layers or any(f < 1 for f in self.fanout):
             raise ValueError("need one fanout >= 1 per layer")
-        if self.mode != NODE_WISE:
-            # layer-wise sampling is outside the B200 hot path
-            raise ValueError(f"unsupported sampling mode {self.mode!r} (node-wise only)")
+        if self.mode not in (NODE_WISE, LAYER_WISE):
+            raise ValueError(f"unknown sampling mode {self.mode!r}")
 
     def stream_key(self, epoch: int, iteration: int, root: int) -> int:
         return stream_key(self.seed, epoch, iteration, root)
@@ -304,10 +303,56 @@ def _as_u64_tensor(vals, device):
 
 
 def sample_micrograph(g: Graph, root: int, cfg: SamplerConfig, key: int) -> Micrograph:
-    """Sample one root's micrograph under `key` (sampler.py:84-106)."""
+    """Sample one root's micrograph under `key` (sampler.py:84-106); node-wise
+    through the batched device build, layer-wise hop by hop on the device."""
     if not 0 <= int(root) < g.n_vertices:
         raise ValueError(f"root {root} out of range for {g.n_vertices} vertices")
+    if cfg.mode == LAYER_WISE:
+        return _layer_wise_micrograph(g, int(root), cfg, key)
     return sample_micrographs(g, [root], cfg, [key])[0]
+
+
+def layer_wise_hop(g: Graph, frontier: torch.Tensor, budget: int, state: int):
+    """One layer-wise hop (sampler.py:109-120) on the device: the frontier's
+    neighbour spans, their distinct ids as candidates, a shared draw of
+    `budget` of them (kernels.pick_k_smallest, hg_pick_k_smallest), and the
+    (dst, src) pairs whose source was drawn.  Returns device int64 tensors."""
+    from .kernels import pick_k_smallest
+    dev = g.device
+    if frontier.numel() == 0:
+        e = torch.empty(0, dtype=torch.int64, device=dev)
+        return e, e
+    lo, hi = g.offsets[frontier], g.offsets[frontier + 1]
+    ln = hi - lo
+    start = torch.zeros(frontier.numel() + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(ln, 0, out=start[1:])
+    m = int(start[-1].item())
+    dst_all = torch.repeat_interleave(torch.arange(frontier.numel(), device=dev), ln)
+    flat_all = g.targets[torch.repeat_interleave(lo - start[:-1], ln) +
+                         torch.arange(m, device=dev)].long() if m else dst_all
+    cand = torch.unique(flat_all)
+    sel = torch.as_tensor(pick_k_smallest(cand, int(budget), state), device=dev)
+    keep = torch.isin(flat_all, sel)
+    return dst_all[keep], flat_all[keep]
+
+
+def _layer_wise_micrograph(g: Graph, root: int, cfg: SamplerConfig, key: int) -> Micrograph:
+    """sample_micrograph's hop loop with layer-wise hops (sampler.py:93-106)."""
+    L = cfg.n_layers
+    dev = g.device
+    layers = [None] * (L + 1)
+    pairs = [None] * L
+    layers[L] = torch.tensor([root], dtype=torch.int64, device=dev)
+    for k in range(L - 1, -1, -1):
+        hop = L - k
+        dst, flat = layer_wise_hop(g, layers[k + 1], cfg.fanout[hop - 1], chain(key, hop))
+        layers[k] = torch.unique(flat)
+        pairs[k] = (dst, torch.searchsorted(layers[k], flat))
+    host = [x.cpu().numpy().astype(np.int64) for x in layers]
+    hp = tuple((d.cpu().numpy().astype(np.int64), s_.cpu().numpy().astype(np.int64))
+               for d, s_ in pairs)
+    verts = np.unique(np.concatenate(host))
+    return Micrograph(int(root), tuple(host), hp, verts)
 
 
 def sample_micrographs(g: Graph, roots, cfg: SamplerConfig, keys) -> list:

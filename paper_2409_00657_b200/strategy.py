@@ -240,13 +240,15 @@ class World:
         return self.graph.n_vertices
 
 
-def build_world(cfg, device="cuda") -> World:
+def build_world(cfg, device="cuda", modes_ok: bool = False) -> World:
     """engine.py:235-258 on the GPU.  Graph: "sbm" (generate_sbm, CUDA pair pass),
-    a CSR1 file (*.csr) or an edge list; partitioner hash / greedy / file."""
+    a CSR1 file (*.csr) or an edge list; partitioner hash / greedy / file.
+    The batched trainer samples node-wise; layer-wise worlds (modes_ok) serve
+    the locality report (sampler.sample_micrograph, layer-wise hops)."""
     cfg = as_run_config(cfg)
-    if cfg.mode != "node-wise":
-        raise ConfigError("layer-wise sampling runs through kernels.pick_k_smallest / "
-                          "sampler.sample_micrograph, not the batched trainer")
+    if cfg.mode != "node-wise" and not modes_ok:
+        raise ConfigError("the batched trainer samples node-wise; layer-wise micrographs come "
+                          "from sampler.sample_micrograph (kernels.pick_k_smallest)")
     if cfg.graph == "sbm":
         graph = generate_sbm(SbmSpec(tuple(cfg.blocks), cfg.p_in, cfg.p_out,
                                      chain(cfg.seed, SEED_GRAPH)), device)

@@ -109,11 +109,13 @@ def test_step_matches_oracle(world, case, dtype, fused_head=False):
     P = OM.init_params(arch, D, H, len(fo), C, mseed)
     want_loss, want_g = oracle_cell(off, tgt, roots, fo, sseed, (0, 3), P, D,
                                     feature_state(seed), lseed, C, bf, tc=tc)
-    forced = None
+    forced = P_forced = None
     if bf:
         masks = _device_masks(run, batch, len(roots), len(fo))
         forced = oracle_cell(off, tgt, roots, fo, sseed, (0, 3), P, D, feature_state(seed),
                              lseed, C, True, tc=tc, masks=masks)[1]
+        P_forced = P.copy()
+        OM.sgd_step(P_forced, forced, len(roots), 0.1)
     tol = TOL[dtype] * (2 if tc else 1)
     mf = 1.0 if dtype == torch.float32 else BF16_MAX_FACTOR
     got = {"loss": (run.losses(), want_loss)}
@@ -128,22 +130,27 @@ def test_step_matches_oracle(world, case, dtype, fused_head=False):
     rec = {}
     for what, (a, b) in got.items():  # every error recorded before any assertion
         rec[what] = dict(zip(("max_abs_rel", "norm_rel"), errors(a, b)))
+    params = [a.copy() for a in model.params()]
     if forced is not None:
         for i, (a, b) in enumerate(zip(grads, forced.arrays())):
             rec[f"grad[{i}] mask-forced"] = dict(zip(("max_abs_rel", "norm_rel"), errors(a, b)))
+        for i, (a, b) in enumerate(zip(params, P_forced.arrays())):
+            rec[f"param[{i}] mask-forced"] = dict(zip(("max_abs_rel", "norm_rel"), errors(a, b)))
     tag = "tc" if tc else str(dtype).split(".")[-1]
     _report(f"step_{arch}_{'x'.join(map(str, fo))}_D{D}_H{H}_C{C}_{tag}"
             + ("_fusedhead" if fused_head else ""),
             {"tol": tol, "max_factor": mf, "errors": rec})
     for what, (a, b) in got.items():
-        if bf and what.startswith("grad"):
+        if bf and what != "loss":
             _, nrel = errors(a, b)  # free-running: norm only (see docstring)
             assert nrel <= tol, f"{what}: norm-rel {nrel:.3e} > {tol}"
             continue
-        close(a, b, tol, what, 1.0 if what == "loss" else mf)
+        close(a, b, tol, what, 1.0)
     if forced is not None:
         for i, (a, b) in enumerate(zip(grads, forced.arrays())):
             close(a, b, tol, f"grad[{i}] mask-forced", mf)
+        for i, (a, b) in enumerate(zip(params, P_forced.arrays())):
+            close(a, b, tol, f"param[{i}] mask-forced", mf)
     assert float(model.grad.abs().max()) == 0.0
 
 
