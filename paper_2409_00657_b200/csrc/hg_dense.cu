@@ -618,8 +618,6 @@ k_scatter_top(const float* __restrict__ dagg, int ld, const int32_t* __restrict_
               float* __restrict__ gb, const int32_t* __restrict__ n_rows_dev, int cap_rows) {
   pdl_trigger();
   pdl_wait();
-  // warp per need[L-1] row (row-parallel: every row's short dependent chain in
-  // flight at once); its root by binary search over the roots' row offsets
   __shared__ float red[8][257];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c0 = lane * 8;
@@ -628,58 +626,61 @@ k_scatter_top(const float* __restrict__ dagg, int ld, const int32_t* __restrict_
 #pragma unroll
   for (int j = 0; j < 8; ++j) cs[j] = 0.f;
   const int n_rows = *n_rows_dev;
-  for (int u = blockIdx.x * 8 + warp; u < n_rows; u += gridDim.x * 8) {
-    int lo = 0, hi = n_roots;  // root r with need_off_p[r] <= u < need_off_p[r + 1]
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (need_off_p[mid] <= u) lo = mid; else hi = mid;
-    }
-    const int r = lo;
+  // warp per root (its <= 1 + f1 need[L-1] rows), four rows' loads in flight
+  // at a time
+  for (int r = blockIdx.x * 8 + warp; r < n_roots; r += gridDim.x * 8) {
+    const int q0 = need_off_p[r], nq = need_off_p[r + 1] - q0;
     const int rowL = need_off_c[r];
-    if (!lane_on || need_off_c[r + 1] - rowL != 1) continue;  // empty (capacity) micrograph
+    if (!lane_on || nq == 0 || need_off_c[r + 1] - rowL != 1) continue;  // empty micrograph
     const int srow = self_pos[rowL];
     const int deg = nbr_off[rowL + 1] - nbr_off[rowL];
     const float* g = dagg + (int64_t)rowL * ld;
-    float x[8], hv[8];
-    load_vec(h + (int64_t)u * H + c0, hv);
-    if constexpr (sizeof(T) == 4) load_vec(h + (int64_t)u * H + c0 + 4, hv + 4);
+    float gs[8], gn[8];
 #pragma unroll
     for (int j = 0; j < 8; j += 4) {
       const float4 a = *reinterpret_cast<const float4*>(g + c0 + j);
-      x[j] = a.x; x[j + 1] = a.y; x[j + 2] = a.z; x[j + 3] = a.w;
-    }
-    if constexpr (SAGE) {
-      // self half -> the self row (plus the neighbour half when deg == 0);
-      // neighbour half / deg -> every sampled neighbour row
-      float gn[8];
-#pragma unroll
-      for (int j = 0; j < 8; j += 4) {
+      gs[j] = a.x; gs[j + 1] = a.y; gs[j + 2] = a.z; gs[j + 3] = a.w;
+      if constexpr (SAGE) {
         const float4 b = *reinterpret_cast<const float4*>(g + H + c0 + j);
         gn[j] = b.x; gn[j + 1] = b.y; gn[j + 2] = b.z; gn[j + 3] = b.w;
       }
-      // a row is the root's self row and/or one of its sampled neighbours (both
-      // with a self-loop); the neighbour rows are exactly layers[L-1] (in_layer)
-      const bool self = u == srow, nbr = in_layer[u] != 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        x[j] = (self ? (deg > 0 ? x[j] : x[j] + gn[j]) : 0.f) + (nbr ? gn[j] / (float)deg : 0.f);
-    } else {
-      const float m = (float)((u == srow) + (in_layer[u] != 0)) / (float)(deg + 1);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) x[j] = x[j] * m;
     }
-    float v[8];
+    for (int i0 = 0; i0 < nq; i0 += 4) {
+      float hv[4][8];
+      int8_t inl[4];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      v[j] = hv[j] > 0.f ? x[j] : 0.f;
-      cs[j] += v[j];
+      for (int t = 0; t < 4; ++t) {  // issue the four rows' loads first
+        const int u = q0 + min(i0 + t, nq - 1);
+        load_vec(h + (int64_t)u * H + c0, hv[t]);
+        if constexpr (sizeof(T) == 4) load_vec(h + (int64_t)u * H + c0 + 4, hv[t] + 4);
+        inl[t] = in_layer[u];
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (i0 + t >= nq) break;
+        const int u = q0 + i0 + t;
+        // a row is the root's self row and/or one of its sampled neighbours (both
+        // with a self-loop); the neighbour rows are exactly layers[L-1] (in_layer)
+        const bool self = u == srow, nbr = inl[t] != 0;
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float x;
+          if constexpr (SAGE)
+            x = (self ? (deg > 0 ? gs[j] : gs[j] + gn[j]) : 0.f) + (nbr ? gn[j] / (float)deg : 0.f);
+          else
+            x = gs[j] * ((float)((int)self + (int)nbr) / (float)(deg + 1));
+          v[j] = hv[t][j] > 0.f ? x : 0.f;
+          cs[j] += v[j];
+        }
+        const int64_t o = (int64_t)u * H + c0;
+        if (dh_out) {
+          *reinterpret_cast<float4*>(dh_out + o) = make_float4(v[0], v[1], v[2], v[3]);
+          *reinterpret_cast<float4*>(dh_out + o + 4) = make_float4(v[4], v[5], v[6], v[7]);
+        }
+        if (lowp) store_vec(lowp + o, v);
+      }
     }
-    const int64_t o = (int64_t)u * H + c0;
-    if (dh_out) {
-      *reinterpret_cast<float4*>(dh_out + o) = make_float4(v[0], v[1], v[2], v[3]);
-      *reinterpret_cast<float4*>(dh_out + o + 4) = make_float4(v[4], v[5], v[6], v[7]);
-    }
-    if (lowp) store_vec(lowp + o, v);
   }
   if (lane_on)
 #pragma unroll
@@ -1184,7 +1185,7 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
       // top layer: per-row map, no scatter (k_scatter_top)
       const bool tc_dx = tc && d->in_dim[k - 1] % 64 == 0 && d->Wb[k - 1];
       const bool want_f32 = !tc || (k - 1 >= 2 && !tc_dx);
-      const int grid = std::max(1, std::min((d->max_rows[k - 1] + 7) / 8, num_sms() * 4));
+      const int grid = std::max(1, std::min((n_roots + 7) / 8, num_sms() * 4));
       count_launch();
       auto kern = sage ? k_scatter_top<true, T> : k_scatter_top<false, T>;
       launch_pdl(kern, dim3(grid), dim3(256), 0, s, (const float*)d->dagg, d->in_dim[k],

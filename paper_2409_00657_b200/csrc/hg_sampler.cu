@@ -259,6 +259,22 @@ __device__ void team_select(const int32_t* __restrict__ targets, int64_t lo, int
   }
   Team::sync();
   const uint64_t T = *tsh;
+  if (Team::size() == 32) {
+    // one warp filled cand[] in ascending slot order (passes in slot order,
+    // ballot positions lane-ordered): the selected keys' output positions are
+    // a running ballot count
+    int base = 0;
+    for (int i0 = 0; i0 < m; i0 += 32) {
+      const int i = i0 + lane;
+      const uint64_t ki = i < m ? cand[i] : ~0ull;
+      const bool sel = ki <= T;
+      const unsigned b = __ballot_sync(0xffffffffu, sel);
+      if (sel) out[base + __popc(b & ((1u << lane) - 1u))] = targets[lo + (uint32_t)ki];
+      base += __popc(b);
+    }
+    Team::sync();
+    return;
+  }
   for (int i = Team::rank(); i < m; i += Team::size()) {
     const uint64_t ki = cand[i];
     if (ki <= T) {
