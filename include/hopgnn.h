@@ -372,6 +372,9 @@ int hg_set_fused_head(int32_t on);
 int hg_alloc(size_t bytes, void** out);
 int hg_free(void* p);
 int hg_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
+/* *flag = HG_EINVARIANT if a[0..n) and b[0..n) differ bitwise (replica check of
+ * the model hop without a host sync, model.py:311-314) */
+int hg_flag_if_differ(const float* a, const float* b, int64_t n, int* flag, void* stream);
 int hg_ipc_handle(void* p, void* handle_out);
 int hg_ipc_open(const void* handle, void** out);
 int hg_ipc_close(void* p);

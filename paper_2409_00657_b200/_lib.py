@@ -133,6 +133,7 @@ SIGNATURES = {
     "hg_gemm_bf16": [V, I64, C.c_int, V, I64, C.c_int, V, I64, I32, I32, I32, I32, V, I32, V],
     "hg_alloc": [C.c_size_t, C.POINTER(C.c_void_p)],
     "hg_memcpy_d2d": [V, V, C.c_size_t, V],
+    "hg_flag_if_differ": [V, V, I64, V, V],
     "hg_free": [V],
     "hg_ipc_handle": [V, V],
     "hg_ipc_open": [V, C.POINTER(C.c_void_p)],

@@ -10,6 +10,8 @@
 // iteration's remote vertices, first-setters count per home.
 #include <cstring>
 
+#include <algorithm>
+
 #include "hg_common.cuh"
 
 namespace hg {
@@ -425,6 +427,27 @@ extern "C" int hg_alloc(size_t bytes, void** out) {
   const size_t b = bytes < 256 ? 256 : bytes;
   HG_CUDA_TRY(cudaMalloc(out, b));
   HG_CUDA_TRY(cudaMemset(*out, 0, b));  // mailboxes rely on zeroed counters
+  return HG_OK;
+}
+
+__global__ void k_flag_if_differ(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                                 int64_t n, int* flag, int code) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (a[i] != b[i]) { raise_flag(flag, code); return; }
+}
+
+// Device-side replica check of the model hop (model.py:311-314 "replicas
+// diverged"): bitwise compare of two f32 buffers, raising HG_EINVARIANT in
+// *flag on any difference -- no host synchronisation inside the step.
+extern "C" int hg_flag_if_differ(const float* a, const float* b, int64_t n, int* flag,
+                                 void* stream) {
+  if (n <= 0) return HG_OK;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 4);
+  k_flag_if_differ<<<grid, 256, 0, (cudaStream_t)stream>>>((const uint32_t*)a,
+                                                            (const uint32_t*)b, n, flag,
+                                                            HG_EINVARIANT);
+  HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;
 }
 

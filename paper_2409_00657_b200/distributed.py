@@ -766,6 +766,7 @@ class MicrographTrainer:
         self._loss_pending = []
         self._recv_p = torch.empty_like(model.flat) if mode == "faithful" else None
         self._recv_g = torch.empty_like(model.grad) if mode == "faithful" else None
+        self._hop_err = torch.zeros(1, dtype=torch.int32, device=self.device)
         # our own NCCL communicator for the in-C all-reduce+SGD (and hops)
         self._comm = None
         self._comm_ok = True
@@ -1345,16 +1346,29 @@ class MicrographTrainer:
         every trace-table column is a uniform shift, so each hop is a ring
         permutation over NVSwitch."""
         S, rank = self.S, self.rank
+        m = self.model
+        if self._comm is not None:
+            # one grouped NCCL send/recv (hg_shift) and a device-side replica check:
+            # no host synchronisation per hop; the flag is read by check()
+            s = torch.cuda.current_stream(self.device).cuda_stream
+            _lib.call("hg_shift", self._comm, rank, S, int(delta), m.flat.data_ptr(),
+                      m.grad.data_ptr(), self._recv_p.data_ptr(), self._recv_g.data_ptr(),
+                      m.flat.numel(), s)
+            _lib.call("hg_flag_if_differ", self._recv_p.data_ptr(), m.flat.data_ptr(),
+                      m.flat.numel(), self._hop_err.data_ptr(), s)
+            m.grad.copy_(self._recv_g)
+            self.traffic.hop_bytes += 2 * self.flat_bytes
+            return
         nxt, prv = (rank + delta) % S, (rank - delta) % S
-        ops = [dist.P2POp(dist.isend, self.model.flat, nxt, self.group),
-               dist.P2POp(dist.isend, self.model.grad, nxt, self.group),
+        ops = [dist.P2POp(dist.isend, m.flat, nxt, self.group),
+               dist.P2POp(dist.isend, m.grad, nxt, self.group),
                dist.P2POp(dist.irecv, self._recv_p, prv, self.group),
                dist.P2POp(dist.irecv, self._recv_g, prv, self.group)]
         for w in dist.batch_isend_irecv(ops):
             w.wait()
-        if not torch.equal(self._recv_p, self.model.flat):
+        if not torch.equal(self._recv_p, m.flat):
             raise InvariantViolation("replicas diverged during migration")
-        self.model.grad.copy_(self._recv_g)
+        m.grad.copy_(self._recv_g)
         self.traffic.hop_bytes += 2 * self.flat_bytes
 
     def _account_hops_and_sync(self, mult: int = 1):
@@ -1383,6 +1397,10 @@ class MicrographTrainer:
             self._dgl.check()
         if hasattr(self.feats, "check"):
             self.feats.check()
+        code = int(self._hop_err.item())
+        if code:
+            self._hop_err.zero_()
+            _lib.flag_status(code, "model hop (replicas diverged during migration)")
 
     def close(self) -> None:
         """Release peer mappings (CUDA IPC) held by this trainer."""
