@@ -109,7 +109,10 @@ static int isqrt_ceil(int x) {
   return r;
 }
 
-int select_mean(int fanout) { return fanout + 4 * isqrt_ceil(fanout) + 8; }
+// expected survivors of the threshold pass: fanout + 2 sqrt(fanout) + 4 (a ~2-sigma margin;
+// an under- or overflow re-runs the pass with a bisected threshold, so the draw stays
+// exact -- the margin only trades retries against the O(m) candidate rank)
+int select_mean(int fanout) { return fanout + 2 * isqrt_ceil(fanout) + 4; }
 
 int make_carve(int L, const int32_t* fanout, MgCarve* c) {
   if (L < 1 || L > HG_MAX_LAYERS) return hg_fail(HG_ECONFIG, "n_layers must be 1..%d", HG_MAX_LAYERS);
