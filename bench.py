@@ -568,7 +568,7 @@ def run_distributed(args, cfg):
     if G <= 0:
         G = next((g_ for g_ in range(12, 3, -1) if args.steps % g_ == 0), 8)
     tr = MicrographTrainer(g, part, model, cfg["fanout"], B, cfg["seed"], mode=mode,
-                           pregather=args.pregather, graph_group=G)
+                           pregather=args.pregather, graph_group=G, allreduce=args.allreduce)
     iters = tr.begin_epoch(0)
     torch.cuda.synchronize()
     setup_s = time.time() - t0
@@ -732,7 +732,8 @@ def run_distributed(args, cfg):
                        "fanout": list(cfg["fanout"]), "hidden": cfg["hidden"],
                        "run_ahead_group": G,
                        "parallelism": f"micrograph x{S} ({mode}; features sharded by planted "
-                                      f"block, CSR {args.csr}; remote rows "
+                                      f"block, CSR {args.csr}; {args.allreduce} gradient "
+                                      "all-reduce; remote rows "
                                       + ("pre-gathered by NCCL all-to-all)" if args.pregather
                                          else "read over NVLink by the gather kernel)"),
                        "l2": "inputs larger than L2"},
@@ -805,6 +806,9 @@ def main():
     ap.add_argument("--pregather", action="store_true",
                     help="multi-GPU: stage remote rows with NCCL all-to-all instead of NVLink "
                          "peer reads")
+    ap.add_argument("--allreduce", default="p2p", choices=["p2p", "nccl"],
+                    help="multi-GPU gradient all-reduce: NVLink peer-memory push (hg_p2p_allreduce) "
+                         "or NCCL")
     ap.add_argument("--csr", default="sharded", choices=["sharded", "replicated"],
                     help="multi-GPU topology: CSR rows partitioned by home (remote rows read "
                          "over NVLink in the builds) or a full copy per GPU")

@@ -372,6 +372,19 @@ int hg_set_fused_head(int32_t on);
 int hg_alloc(size_t bytes, void** out);
 int hg_free(void* p);
 int hg_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
+/* Gradient all-reduce over NVLink peer memory (model.py:299-324 across the
+ * one-process-per-GPU ranks): each rank owns an IPC-shared exchange region of
+ * hg_p2p_region_bytes(n_ranks, n) bytes (zeroed: hg_alloc); regions holds the
+ * n_ranks region pointers as mapped on this GPU (own + peers').  grads[n] is
+ * replaced by the sum over ranks.  seq (int64), counter (uint32) and err
+ * (int32) are zero-initialised device words owned by this rank; a peer that
+ * never publishes raises HG_EINVARIANT in *err instead of hanging.  Three
+ * kernels: push this rank's accumulator into every peer's region + signal,
+ * wait for every peer's signal, add the peers' slots. */
+int hg_p2p_region_bytes(int32_t n_ranks, int64_t n, int64_t* bytes);
+int hg_p2p_allreduce(float* grads, int64_t n, const uint64_t* regions, int32_t rank,
+                     int32_t n_ranks, int64_t* seq, unsigned int* counter, int* err, void* stream);
+
 /* *flag = HG_EINVARIANT if a[0..n) and b[0..n) differ bitwise (replica check of
  * the model hop without a host sync, model.py:311-314) */
 int hg_flag_if_differ(const float* a, const float* b, int64_t n, int* flag, void* stream);

@@ -523,3 +523,122 @@ extern "C" int hg_resolve_rows(const int32_t* ids, const int32_t* n_dev, const i
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;
 }
+
+// ---------------------------------------------------------------- P2P all-reduce
+namespace hg {
+//
+// Gradient all-reduce over NVLink peer memory (the synchronous update of
+// model.py:299-324 across one-process-per-GPU ranks), replacing the NCCL
+// all-reduce on the training stream:
+//   push   every rank writes its accumulator into slot [rank] of buffer
+//          (seq & 1) in EVERY peer's exchange region (fire-and-forget NVLink
+//          stores), the last CTA bumps the device sequence number and sets
+//          flag[rank] = seq in every peer's region (system-scope fences);
+//   wait   one CTA polls this rank's flags until every peer published seq
+//          (bounded: an error flag instead of a hang);
+//   reduce g += sum of the peers' slots (local HBM reads), after which the
+//          regular fused SGD + bf16 refresh runs (hg_sgd_refresh).
+// Double buffering by seq parity is safe: a rank reuses buffer (s & 1) for
+// s + 2 only after every peer published s + 1, which each peer does after its
+// reduce of s (stream order).  Region layout: [S int64 flags | pad to 256 |
+// 2 x S x n floats].
+struct ArRegion {
+  int64_t o_flags, o_buf;
+};
+
+__device__ __forceinline__ float* ar_slot(uint8_t* region, ArRegion r, int parity, int S, int p,
+                                          int64_t n) {
+  return reinterpret_cast<float*>(region + r.o_buf) + ((int64_t)parity * S + p) * n;
+}
+
+__global__ void __launch_bounds__(256)
+k_ar_push(const float* __restrict__ g, int64_t n, const uint64_t* __restrict__ regions, int rank,
+          int S, ArRegion r, int64_t* seq, unsigned int* counter) {
+  const int64_t s = *seq + 1;
+  const int par = (int)(s & 1);
+  for (int p = 0; p < S; ++p) {
+    if (p == rank) continue;
+    float* dst = ar_slot(reinterpret_cast<uint8_t*>(regions[p]), r, par, S, rank, n);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+      dst[i] = g[i];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int t = atomicAdd(counter, 1u);
+    if (t == gridDim.x - 1) {  // every CTA's stores are fenced: publish s
+      *counter = 0u;
+      *seq = s;
+      __threadfence_system();
+      for (int p = 0; p < S; ++p) {
+        if (p == rank) continue;
+        volatile int64_t* f =
+            reinterpret_cast<volatile int64_t*>(reinterpret_cast<uint8_t*>(regions[p]) + r.o_flags);
+        f[rank] = s;
+      }
+      __threadfence_system();
+    }
+  }
+}
+
+__global__ void k_ar_wait(const uint64_t* __restrict__ regions, int rank, int S, ArRegion r,
+                          const int64_t* seq, int* err) {
+  if (threadIdx.x != 0) return;
+  const int64_t s = *seq;
+  volatile int64_t* mine =
+      reinterpret_cast<volatile int64_t*>(reinterpret_cast<uint8_t*>(regions[rank]) + r.o_flags);
+  for (long long it = 0; it < (1ll << 26); ++it) {
+    bool all = true;
+    for (int p = 0; p < S; ++p)
+      if (p != rank && mine[p] < s) all = false;
+    if (all) { __threadfence_system(); return; }
+    __nanosleep(64);
+  }
+  raise_flag(err, HG_EINVARIANT);
+}
+
+__global__ void __launch_bounds__(256)
+k_ar_reduce(float* __restrict__ g, int64_t n, const uint64_t* __restrict__ regions, int rank,
+            int S, ArRegion r, const int64_t* seq) {
+  const int par = (int)(*seq & 1);
+  uint8_t* mine = reinterpret_cast<uint8_t*>(regions[rank]);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v = g[i];
+    for (int p = 0; p < S; ++p)
+      if (p != rank) v += ar_slot(mine, r, par, S, p, n)[i];
+    g[i] = v;
+  }
+}
+
+}  // namespace hg
+
+using namespace hg;
+
+extern "C" int hg_p2p_region_bytes(int32_t n_ranks, int64_t n, int64_t* bytes) {
+  const int64_t flags = ((int64_t)n_ranks * 8 + 255) / 256 * 256;
+  *bytes = flags + 2ll * n_ranks * n * 4;
+  return HG_OK;
+}
+
+extern "C" int hg_p2p_allreduce(float* grads, int64_t n, const uint64_t* regions, int32_t rank,
+                                int32_t n_ranks, int64_t* seq, unsigned int* counter, int* err,
+                                void* stream) {
+  if (n_ranks < 1 || rank < 0 || rank >= n_ranks) return hg_fail(HG_ERANGE, "bad rank");
+  if (n_ranks == 1 || n <= 0) return HG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  ArRegion r{0, ((int64_t)n_ranks * 8 + 255) / 256 * 256};
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)nsm);
+  count_launch(3);
+  k_ar_push<<<grid, 256, 0, s>>>(grads, n, regions, rank, n_ranks, r, seq, counter);
+  HG_CUDA_TRY(cudaGetLastError());
+  k_ar_wait<<<1, 32, 0, s>>>(regions, rank, n_ranks, r, seq, err);
+  HG_CUDA_TRY(cudaGetLastError());
+  k_ar_reduce<<<grid, 256, 0, s>>>(grads, n, regions, rank, n_ranks, r, seq);
+  HG_CUDA_TRY(cudaGetLastError());
+  return HG_OK;
+}

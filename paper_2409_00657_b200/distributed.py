@@ -493,12 +493,9 @@ class DistGraphLoop:
                 run.desc.lowp_fresh = 0
                 self.pin_loss[x].copy_(run.loss[:self.cap].sum().reshape(1), non_blocking=True)
                 if run.tc:  # SGD refreshes the bf16 operands: steps skip their transposes
-                    _lib.call("hg_allreduce_sgd_refresh", tr._comm, C.byref(run.desc),
-                              m.flat.data_ptr(), m.grad.data_ptr(), m.flat.numel(),
-                              float(tr.lr), 1.0 / total, cs)
+                    tr._sync_update(run, cs, refresh=True)
                 else:
-                    _lib.call("hg_allreduce_sgd", tr._comm, m.flat.data_ptr(), m.grad.data_ptr(),
-                              m.flat.numel(), float(tr.lr), 1.0 / total, cs)
+                    tr._sync_update(None, cs, refresh=False)
                 cap_s.wait_stream(self.side_build)
                 cap_s.wait_stream(self.side_gather)
             cur.wait_stream(cap_s)
@@ -585,13 +582,9 @@ class DistGroupLoop:
                     _lib.call("hg_train_step", C.byref(r.desc), self.cap, cs)
                     r.desc.lowp_fresh = 0
                     if r.tc:
-                        _lib.call("hg_allreduce_sgd_refresh", tr._comm, C.byref(r.desc),
-                                  m.flat.data_ptr(), m.grad.data_ptr(), m.flat.numel(),
-                                  float(tr.lr), 1.0 / total, cs)
+                        tr._sync_update(r, cs, refresh=True)
                     else:
-                        _lib.call("hg_allreduce_sgd", tr._comm, m.flat.data_ptr(),
-                                  m.grad.data_ptr(), m.flat.numel(), float(tr.lr), 1.0 / total,
-                                  cs)
+                        tr._sync_update(None, cs, refresh=False)
                 self.pin_loss[x].copy_(torch.stack([r.loss[:self.cap].sum() for r in run])
                                        .sum().reshape(1), non_blocking=True)
                 cap_s.wait_stream(self.side_build)
@@ -665,13 +658,10 @@ class DistGroupLoop:
                 r.desc.lowp_fresh = 1
                 _lib.call("hg_train_step", C.byref(r.desc), self.cap, s)
                 r.desc.lowp_fresh = 0
-                _lib.call("hg_allreduce_sgd_refresh", tr._comm, C.byref(r.desc),
-                          m.flat.data_ptr(), m.grad.data_ptr(), m.flat.numel(), float(tr.lr),
-                          1.0 / total, s)
+                tr._sync_update(r, s, refresh=True)
             else:
                 _lib.call("hg_train_step", C.byref(r.desc), self.cap, s)
-                _lib.call("hg_allreduce_sgd", tr._comm, m.flat.data_ptr(), m.grad.data_ptr(),
-                          m.flat.numel(), float(tr.lr), 1.0 / total, s)
+                tr._sync_update(None, s, refresh=False)
         tr._gnext = None
         tr._gdone = None
 
@@ -688,7 +678,8 @@ class MicrographTrainer:
     def __init__(self, graph: Graph, part: PartitionMap, model: ModelState, fanout, batch: int,
                  seed: int, lr: float = 0.1, dtype=torch.bfloat16, mode: str = "fused",
                  iterations: int = 0, group=None, use_tc: bool = True, pregather: bool = True,
-                 strategy: str = "micrograph", graphs: bool = True, graph_group: int = 1):
+                 strategy: str = "micrograph", graphs: bool = True, graph_group: int = 1,
+                 allreduce: str = "p2p"):
         """strategy="micrograph": HopGNN feature-centric training (engine.py:562-623);
         "model-centric": the baseline it is measured against (engine.py:482-507) --
         GPU d trains all of batch d, fetching every remote row its micrographs
@@ -700,6 +691,8 @@ class MicrographTrainer:
             raise ValueError("mode must be 'fused' or 'faithful'")
         if strategy not in ("micrograph", "model-centric"):
             raise ValueError("strategy must be 'micrograph' or 'model-centric'")
+        if allreduce not in ("p2p", "nccl"):
+            raise ValueError("allreduce must be 'p2p' or 'nccl'")
         if strategy == "model-centric":
             mode = "fused"  # one cell per GPU, nothing to hop
         self.strategy = strategy
@@ -783,6 +776,10 @@ class MicrographTrainer:
                 self._comm = comm.value
             except RuntimeError:
                 self._comm_ok = False  # fall back to torch.distributed collectives
+        # gradient all-reduce of the fast paths: NVLink peer memory (default) or NCCL
+        self._ar = None
+        if self.S > 1 and allreduce == "p2p" and self._comm_ok and self._comm is not None:
+            self._setup_p2p_allreduce()
 
     # ------------------------------------------------------------ epoch
     def begin_epoch(self, epoch: int) -> int:
@@ -1113,10 +1110,7 @@ class MicrographTrainer:
                     prev = self._drain_loss()
                 self._loss_pending.append((ev, self._loss_pin[self._loss_slot]))
         self._fast_iters = getattr(self, "_fast_iters", 0) + 1
-        total = S * self.B
-        m = self.model
-        _lib.call("hg_allreduce_sgd", self._comm, m.flat.data_ptr(), m.grad.data_ptr(),
-                  m.flat.numel(), float(self.lr), 1.0 / total, s)
+        self._sync_update(None, s, refresh=False)
         if not self.pregather:
             self._ra.release(it)
             if it + 1 < self.iters:
@@ -1141,9 +1135,7 @@ class MicrographTrainer:
             if len(self._loss_pending) >= 2:
                 prev = self._drain_loss()
             self._loss_pending.append((ev, self._loss_pin[self._loss_slot]))
-        m = self.model
-        _lib.call("hg_allreduce_sgd", self._comm, m.flat.data_ptr(), m.grad.data_ptr(),
-                  m.flat.numel(), float(self.lr), 1.0 / (self.S * self.B), s)
+        self._sync_update(None, s, refresh=False)
         self._fast_iters = getattr(self, "_fast_iters", 0) + 1
         self.traffic.allreduce_bytes += 2.0 * (self.S - 1) / self.S * self.flat_bytes
         return prev
@@ -1388,6 +1380,61 @@ class MicrographTrainer:
             self.ledger.add(rank, (rank + 1) % S, GRADIENT, 2.0 * (S - 1) / S * pb * mult,
                             2 * (S - 1) * mult)
 
+    def _setup_p2p_allreduce(self) -> None:
+        """Exchange regions of the NVLink all-reduce (hg_p2p_allreduce):
+        collective, at trainer setup."""
+        n = self.model.flat.numel()
+        nbytes = C.c_int64(0)
+        _lib.call("hg_p2p_region_bytes", self.S, n, C.byref(nbytes))
+        ptr = C.c_void_p()
+        _lib.call("hg_alloc", nbytes.value, C.byref(ptr))
+        handle = (C.c_char * 64)()
+        _lib.call("hg_ipc_handle", ptr.value, handle)
+        handles = [None] * self.S
+        dist.all_gather_object(handles, bytes(handle), group=self.group)
+        regions = []
+        self._ar_opened = []
+        for h, hb in enumerate(handles):
+            if h == self.rank:
+                regions.append(ptr.value)
+                continue
+            q = C.c_void_p()
+            _lib.call("hg_ipc_open", (C.c_char * 64).from_buffer_copy(hb), C.byref(q))
+            self._ar_opened.append(q.value)
+            regions.append(q.value)
+        dev = self.device
+        self._ar = {"mine": ptr.value,
+                    "regions": torch.tensor(regions, dtype=torch.int64, device=dev),
+                    "seq": torch.zeros(1, dtype=torch.int64, device=dev),
+                    "ctr": torch.zeros(1, dtype=torch.int32, device=dev),
+                    "err": torch.zeros(1, dtype=torch.int32, device=dev)}
+
+    def _sync_update(self, runner, stream, refresh: bool) -> None:
+        """The synchronous update (model.py:299-324): all-reduce of the summed
+        accumulators, theta -= lr * g / (S * B), gradient reset; refresh=True also
+        rewrites the bf16 operand copies (hg_sgd_refresh).  All-reduce over NVLink
+        peer memory (hg_p2p_allreduce) by default, NCCL when allreduce="nccl"."""
+        m = self.model
+        n = m.flat.numel()
+        inv = 1.0 / (self.S * self.B)
+        if self._ar is None:
+            if refresh:
+                _lib.call("hg_allreduce_sgd_refresh", self._comm, C.byref(runner.desc),
+                          m.flat.data_ptr(), m.grad.data_ptr(), n, float(self.lr), inv, stream)
+            else:
+                _lib.call("hg_allreduce_sgd", self._comm, m.flat.data_ptr(), m.grad.data_ptr(),
+                          n, float(self.lr), inv, stream)
+            return
+        a = self._ar
+        _lib.call("hg_p2p_allreduce", m.grad.data_ptr(), n, a["regions"].data_ptr(), self.rank,
+                  self.S, a["seq"].data_ptr(), a["ctr"].data_ptr(), a["err"].data_ptr(), stream)
+        if refresh:
+            _lib.call("hg_sgd_refresh", C.byref(runner.desc), m.flat.data_ptr(),
+                      m.grad.data_ptr(), n, float(self.lr), inv, 1, stream)
+        else:
+            _lib.call("hg_sgd_update", m.flat.data_ptr(), m.grad.data_ptr(), None, n,
+                      float(self.lr), inv, stream)
+
     def check(self) -> None:
         """Synchronise and raise on any device error flag: build errors (root
         out of range), push pre-gather timeouts / staging overflow."""
@@ -1401,11 +1448,19 @@ class MicrographTrainer:
         if code:
             self._hop_err.zero_()
             _lib.flag_status(code, "model hop (replicas diverged during migration)")
+        if self._ar is not None:
+            code = int(self._ar["err"].item())
+            if code:
+                self._ar["err"].zero_()
+                _lib.flag_status(code, "hg_p2p_allreduce (a peer never published its gradients)")
 
     def close(self) -> None:
         """Release peer mappings (CUDA IPC) held by this trainer."""
         if hasattr(self.feats, "close"):
             self.feats.close()
+        for p in getattr(self, "_ar_opened", []):
+            _lib.call("hg_ipc_close", p)
+        self._ar_opened = []
 
     def global_ledger(self) -> CommLedger:
         """Merge every rank's ledger (collective)."""

@@ -60,7 +60,8 @@ def pregather_worker(rank, world, init_file, result_file):
 
 
 def micrograph_worker(rank, world, init_file, result_file, mode, dtype_name, feat_mode="pg",
-                      strategy="micrograph", iters=3, graph_group=1, csr="replicated"):
+                      strategy="micrograph", iters=3, graph_group=1, csr="replicated",
+                      allreduce="p2p"):
     """Full multi-GPU micrograph (or model-centric) iterations vs the oracle
     engine (ledger exact, parameters within tolerance)."""
     import json
@@ -88,7 +89,7 @@ def micrograph_worker(rank, world, init_file, result_file, mode, dtype_name, fea
     model = init_model(arch, D, H, len(fo), C, chain(seed, 0x07), f"cuda:{rank}")
     tr = MicrographTrainer(G, part, model, fo, B, seed, lr=0.1, dtype=dtype, mode=mode,
                            iterations=iters, pregather=(feat_mode == "pg"), strategy=strategy,
-                           graph_group=graph_group)
+                           graph_group=graph_group, allreduce=allreduce)
     tr.begin_epoch(0)
     losses = [tr.step(it) for it in range(tr.iters)]
     torch.cuda.synchronize()

@@ -115,3 +115,20 @@ def test_sharded_csr_matches_oracle(strategy, csr):
     res = json.load(open(os.path.join(d, "res.0")))
     assert res["ok"], res["msg"]
     assert res["graph_used"], "group loop never engaged"
+
+
+@pytest.mark.parametrize("allreduce", ["p2p", "nccl"])
+def test_allreduce_paths_match_oracle(allreduce):
+    """Gradient all-reduce over NVLink peer memory (hg_p2p_allreduce: push,
+    signal, wait, reduce; the default) and over NCCL, both inside the grouped
+    graph loop: parameters and ledger equal the oracle's."""
+    import dist_helpers
+    world = _world()
+    d = tempfile.mkdtemp()
+    mp.spawn(dist_helpers.micrograph_worker,
+             args=(world, os.path.join(d, "init"), os.path.join(d, "res"), "fused", "f32", "peer",
+                   "micrograph", 9, 2, "sharded-blocks", allreduce),
+             nprocs=world, join=True)
+    res = json.load(open(os.path.join(d, "res.0")))
+    assert res["ok"], res["msg"]
+    assert res["graph_used"], "group loop never engaged"
