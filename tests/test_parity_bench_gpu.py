@@ -201,10 +201,16 @@ def test_cfg5_deep_sampling_bit_exact():
 
 # bf16 tolerances of the cfg4 loop (tcgen05 GEMMs, bf16 storage points; the
 # oracle emulates the storage points, arithmetic stays f64): per-iteration
-# summed loss, and the parameter CHANGE of 22 SGD steps per tensor
-LOOP_LOSS_TOL = 2e-3
-LOOP_DELTA_TOL = 2e-2       # norm-relative
-LOOP_DELTA_MAX = 2 * 2e-2   # max-abs / max|ref| (2x the norm bound)
+# summed loss (measured 2.4e-6), and the parameter CHANGE of 22 SGD steps per
+# tensor.  The change is free-running: each step's ReLU-mask flips (a
+# pre-activation within one bf16 ulp of 0 taking the other side, see
+# test_step_gpu.py) move a few gradient columns, and 22 steps add them up
+# (measured: W1 3.0 %, W2 2.1 %, biases <= 1.8 %, W_c 0.17 % norm-relative);
+# the mask-forced single-step comparison in test_step_gpu.py pins the
+# kernels themselves to ~1e-3.
+LOOP_LOSS_TOL = 1e-4
+LOOP_DELTA_TOL = 4e-2       # norm-relative
+LOOP_DELTA_MAX = 2 * 4e-2   # max-abs / max|ref| (2x the norm bound)
 
 
 def test_cfg4_group_loop_matches_oracle():
