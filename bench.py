@@ -806,6 +806,9 @@ def main():
     ap.add_argument("--pregather", action="store_true",
                     help="multi-GPU: stage remote rows with NCCL all-to-all instead of NVLink "
                          "peer reads")
+    ap.add_argument("--build-ctas", type=int, default=0,
+                    help="resident build CTAs per SM on the graph loop's build branch "
+                         "(0 = engine.BUILD_CTAS_PER_SM)")
     ap.add_argument("--allreduce", default="p2p", choices=["p2p", "nccl"],
                     help="multi-GPU gradient all-reduce: NVLink peer-memory push (hg_p2p_allreduce) "
                          "or NCCL")
@@ -816,6 +819,9 @@ def main():
                     help="multi-GPU model-hop payload (see distributed.py)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.build_ctas > 0:
+        from paper_2409_00657_b200 import engine
+        engine.BUILD_CTAS_PER_SM = args.build_ctas
     if args.impl == "reference":
         return run_reference(args, cfg)
     return run_ours(args, cfg)

@@ -463,6 +463,17 @@ int hg_pregather_push_multi(const int32_t* const* ids, const int32_t* const* n_d
                             int* err, void* stream);
 /* hg_remote_account charged to row (*it_dev + ahead) of an [iters x row_stride]
  * table (the reference's per-iteration pre-gather ledger, featstore.py:226-279). */
+/* Group variants (one launch per kind for a whole run-ahead group of n_seg
+ * iterations): ledger rows *it_dev + 1 + j with a per-iteration bitmap j
+ * (bitmaps: n_seg x words, zero on entry and exit), and the row handles of
+ * every iteration's need[0] entries (see hg_resolve_rows). */
+int hg_remote_account_group(const int32_t* const* ids, const int32_t* const* n_dev,
+                            int32_t n_seg, const int32_t* home, int32_t rank, uint32_t* bitmaps,
+                            int64_t words, unsigned long long* uniq_table, const int64_t* it_dev,
+                            int32_t row_stride, unsigned long long* total_remote, void* stream);
+int hg_resolve_rows_group(const int32_t* const* ids, const int32_t* const* n_dev, int32_t n_seg,
+                          const int32_t* home, int32_t rank, const int32_t* local_row,
+                          const int32_t* stage_row, int32_t* const* out, void* stream);
 int hg_remote_account_at(const int32_t* ids, const int32_t* n_dev, const int32_t* home,
                          int32_t rank, uint32_t* bitmap, unsigned long long* uniq_table,
                          const int64_t* it_dev, int32_t ahead, int32_t row_stride,

@@ -134,6 +134,8 @@ SIGNATURES = {
     "hg_alloc": [C.c_size_t, C.POINTER(C.c_void_p)],
     "hg_memcpy_d2d": [V, V, C.c_size_t, V],
     "hg_flag_if_differ": [V, V, I64, V, V],
+    "hg_remote_account_group": [V, V, I32, V, I32, V, I64, V, V, I32, V, V],
+    "hg_resolve_rows_group": [V, V, I32, V, I32, V, V, V, V],
     "hg_p2p_region_bytes": [I32, I64, PI64],
     "hg_p2p_allreduce": [V, I64, V, I32, I32, V, V, V, V],
     "hg_free": [V],

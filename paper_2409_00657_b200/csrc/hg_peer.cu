@@ -185,6 +185,53 @@ __global__ void k_stage_mark_stamp(const int32_t* __restrict__ ids, const int32_
   if (total_remote && lane == 0 && mine) atomicAdd(total_remote, mine);
 }
 
+// k_stage_mark_stamp over a whole run-ahead group in ONE launch: blockIdx.y
+// selects the segment (iteration); one stamp tag for the call, so a vertex
+// several segments want is listed once.
+struct StageSegs {
+  const int32_t* ids[HG_MAX_GROUP];
+  const int32_t* n_dev[HG_MAX_GROUP];
+};
+
+__global__ void k_stage_mark_stamp_multi(StageSegs segs, const int32_t* __restrict__ home,
+                                         int rank, int32_t* __restrict__ stamp,
+                                         const int64_t* __restrict__ seq,
+                                         int32_t* __restrict__ stage_list,
+                                         int32_t* __restrict__ stage_row,
+                                         int32_t* __restrict__ stage_count, int stage_cap,
+                                         int* err) {
+  const int32_t* ids = segs.ids[blockIdx.y];
+  const int n = *segs.n_dev[blockIdx.y];
+  int32_t tag = (int32_t)((*seq + 1) & 0x7fffffff);
+  if (tag == 0) tag = 1;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    int v = 0, h = rank;
+    if (i < n) {
+      v = ids[i];
+      h = home[v];
+    }
+    const bool fresh = h != rank && atomicExch(stamp + v, tag) != tag;
+    const unsigned m = __ballot_sync(0xffffffffu, fresh);
+    if (!m) continue;
+    int slot0 = 0;
+    if (lane == 0) slot0 = atomicAdd(stage_count, __popc(m));
+    slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+    if (fresh) {
+      const int slot = slot0 + __popc(m & lt);
+      if (slot < stage_cap) {
+        stage_list[slot] = v;
+        stage_row[v] = slot;
+      } else {
+        raise_flag(err, HG_EINVARIANT);
+      }
+    }
+  }
+}
+
 // 16 lanes x 16 B per row (256-byte bf16 rows); 8 rows in flight per warp.
 __global__ void __launch_bounds__(256)
 k_stage_copy(const int32_t* __restrict__ stage_list, const int32_t* __restrict__ stage_count,
@@ -351,14 +398,19 @@ extern "C" int hg_pregather_push_multi(const int32_t* const* ids, const int32_t*
   uint8_t* own = (uint8_t*)own_box;
   int32_t* count = (int32_t*)(own + o_count);
   HG_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t), s));
-  count_launch(5 + n_seg);
+  count_launch(6);
   prof_begin(PROF_PG_MARK, s);
   // one stamp tag for the whole call: a vertex wanted by several segments is
   // requested once
-  for (int g = 0; g < n_seg; ++g)
-    k_stage_mark_stamp<<<148 * 2, 256, 0, s>>>(ids[g], n_dev[g], home, rank, n_ranks, stamp, seq,
-                                               (int32_t*)(own + o_list), stage_row, count,
-                                               stage_cap, nullptr, nullptr, err, nullptr, 0);
+  if (n_seg > HG_MAX_GROUP) return hg_fail(HG_ERANGE, "at most %d segments", HG_MAX_GROUP);
+  StageSegs sg{};
+  for (int g = 0; g < n_seg; ++g) {
+    sg.ids[g] = ids[g];
+    sg.n_dev[g] = n_dev[g];
+  }
+  k_stage_mark_stamp_multi<<<dim3(148, n_seg), 256, 0, s>>>(sg, home, rank, stamp, seq,
+                                                           (int32_t*)(own + o_list), stage_row,
+                                                           count, stage_cap, err);
   prof_end(PROF_PG_MARK, s);
   prof_begin(PROF_PG_COPY, s);
   k_pg_signal<<<1, 32, 0, s>>>(bx, rank, n_ranks, m, seq, o_flags);
@@ -489,6 +541,97 @@ extern "C" int hg_remote_account(const int32_t* ids, const int32_t* n_dev, int32
   count_launch();
   k_remote_account<<<148 * 2, 256, 0, s>>>(ids, n_dev, n_host, home, rank, bitmap, uniq_per_home,
                                            total_remote);
+  HG_CUDA_TRY(cudaGetLastError());
+  return HG_OK;
+}
+
+// The reference ledger rows of a whole run-ahead group in two launches
+// (blockIdx.y = iteration j of the group, its own bitmap j): per-iteration
+// dedup exactly as hg_remote_account_at + hg_remote_clear per iteration.
+__global__ void k_remote_account_group(StageSegs segs, const int32_t* __restrict__ home, int rank,
+                                       uint32_t* __restrict__ bitmaps, int64_t words,
+                                       unsigned long long* __restrict__ table,
+                                       const int64_t* __restrict__ it_dev, int row_stride,
+                                       unsigned long long* __restrict__ total_remote) {
+  const int j = blockIdx.y;
+  const int32_t* ids = segs.ids[j];
+  const int n = *segs.n_dev[j];
+  uint32_t* bitmap = bitmaps + j * words;
+  unsigned long long* uniq_per_home = table + (*it_dev + 1 + j) * row_stride;
+  unsigned long long mine = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int v = ids[i];
+    const int h = home[v];
+    if (h == rank) continue;
+    ++mine;
+    const uint32_t bit = 1u << (v & 31);
+    const uint32_t old = atomicOr(bitmap + (v >> 5), bit);
+    if (!(old & bit)) atomicAdd(uniq_per_home + h, 1ull);
+  }
+  for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if (total_remote && (threadIdx.x & 31) == 0 && mine) atomicAdd(total_remote, mine);
+}
+
+__global__ void k_remote_clear_group(StageSegs segs, uint32_t* __restrict__ bitmaps,
+                                     int64_t words) {
+  const int j = blockIdx.y;
+  const int32_t* ids = segs.ids[j];
+  const int n = *segs.n_dev[j];
+  uint32_t* bitmap = bitmaps + j * words;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    bitmap[ids[i] >> 5] = 0u;
+}
+
+__global__ void k_resolve_rows_group(StageSegs segs, const int32_t* __restrict__ home, int rank,
+                                     const int32_t* __restrict__ local_row,
+                                     const int32_t* __restrict__ stage_row, StageSegs outs) {
+  const int j = blockIdx.y;
+  const int32_t* ids = segs.ids[j];
+  const int n = *segs.n_dev[j];
+  int32_t* out = const_cast<int32_t*>(outs.ids[j]);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int v = ids[i];
+    out[i] = home[v] == rank ? local_row[v] : -1 - stage_row[v];
+  }
+}
+
+extern "C" int hg_remote_account_group(const int32_t* const* ids, const int32_t* const* n_dev,
+                                       int32_t n_seg, const int32_t* home, int32_t rank,
+                                       uint32_t* bitmaps, int64_t words,
+                                       unsigned long long* uniq_table, const int64_t* it_dev,
+                                       int32_t row_stride, unsigned long long* total_remote,
+                                       void* stream) {
+  if (n_seg < 1 || n_seg > HG_MAX_GROUP) return hg_fail(HG_ERANGE, "bad segment count %d", n_seg);
+  StageSegs sg{};
+  for (int g = 0; g < n_seg; ++g) {
+    sg.ids[g] = ids[g];
+    sg.n_dev[g] = n_dev[g];
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  count_launch(2);
+  k_remote_account_group<<<dim3(148, n_seg), 256, 0, s>>>(sg, home, rank, bitmaps, words,
+                                                          uniq_table, it_dev, row_stride,
+                                                          total_remote);
+  HG_CUDA_TRY(cudaGetLastError());
+  k_remote_clear_group<<<dim3(148, n_seg), 256, 0, s>>>(sg, bitmaps, words);
+  HG_CUDA_TRY(cudaGetLastError());
+  return HG_OK;
+}
+
+extern "C" int hg_resolve_rows_group(const int32_t* const* ids, const int32_t* const* n_dev,
+                                     int32_t n_seg, const int32_t* home, int32_t rank,
+                                     const int32_t* local_row, const int32_t* stage_row,
+                                     int32_t* const* out, void* stream) {
+  if (n_seg < 1 || n_seg > HG_MAX_GROUP) return hg_fail(HG_ERANGE, "bad segment count %d", n_seg);
+  StageSegs sg{}, so{};
+  for (int g = 0; g < n_seg; ++g) {
+    sg.ids[g] = ids[g];
+    sg.n_dev[g] = n_dev[g];
+    so.ids[g] = out[g];
+  }
+  count_launch();
+  k_resolve_rows_group<<<dim3(148, n_seg), 256, 0, (cudaStream_t)stream>>>(
+      sg, home, rank, local_row, stage_row, so);
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;
 }

@@ -399,20 +399,20 @@ class PeerFeatures:
         o = self.mb_off
         ids = (C.c_void_p * G)(*[r.builder.tensors["need_ids"][0].data_ptr() for r in runners])
         ns = (C.c_void_p * G)(*[r.builder.tensors["totals"].data_ptr() for r in runners])
-        for j in range(G):
-            _lib.call("hg_remote_account_at", ids[j], ns[j], self.home.data_ptr(), self.rank,
-                      self.bitmap.data_ptr(), uniq_table_ptr, it_dev_ptr, 1 + j, self.S,
-                      total_ptr, stream)
-            _lib.call("hg_remote_clear", ids[j], ns[j], 0, self.bitmap.data_ptr(), stream)
+        words = self.bitmap.numel()
+        if getattr(self, "_gbitmaps", None) is None or self._gbitmaps.numel() < G * words:
+            self._gbitmaps = torch.zeros(G * words, dtype=torch.int32, device=self.device)
+        _lib.call("hg_remote_account_group", ids, ns, G, self.home.data_ptr(), self.rank,
+                  self._gbitmaps.data_ptr(), words, uniq_table_ptr, it_dev_ptr, self.S,
+                  total_ptr, stream)
         _lib.call("hg_pregather_push_multi", ids, ns, G, self.home.data_ptr(), self.rank, self.S,
                   self.local_row.data_ptr(), self.ptr, self.row_bytes, self.stamp.data_ptr(),
                   self.stage_row.data_ptr(), self.stage_cap, self.boxes.data_ptr(), self.mbox,
                   o[0], o[1], o[2], o[3], o[4], self.seq.data_ptr(), self.err.data_ptr(), stream)
-        for r, ip, np_ in zip(runners, ids, ns):
-            if r.desc.row_handle:
-                _lib.call("hg_resolve_rows", ip, np_, self.home.data_ptr(), self.rank,
-                          self.local_row.data_ptr(), self.stage_row.data_ptr(),
-                          r.desc.row_handle, stream)
+        if all(r.desc.row_handle for r in runners):
+            outs = (C.c_void_p * G)(*[r.desc.row_handle for r in runners])
+            _lib.call("hg_resolve_rows_group", ids, ns, G, self.home.data_ptr(), self.rank,
+                      self.local_row.data_ptr(), self.stage_row.data_ptr(), outs, stream)
 
     def check(self) -> None:
         """Raise if a push pre-gather gave up waiting on a peer or dropped an
