@@ -67,6 +67,18 @@ CONFIGS = {
 }
 
 
+def auto_group(K: int) -> int:
+    """Run-ahead group size: the largest G in 12..4 that divides K with at least
+    4 timed replays (K = 20 -> 5, K = 50 -> 10; G = 5 and G = 10 measured within
+    noise of each other at N = 1), else the largest divisor, else 8.  Configs
+    whose training chain dwarfs the build (reddit GCN-3, deep SAGE-4) set
+    group=1 (grouping measured slower there)."""
+    for g in range(12, 3, -1):
+        if K % g == 0 and K // g >= 4:
+            return g
+    return next((g for g in range(12, 3, -1) if K % g == 0), 8)
+
+
 def peaks():
     try:
         with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
@@ -331,10 +343,8 @@ def _run_ours(args, cfg, dev):
                        cfg["classes"], chain(cfg["seed"], 0x07), dev)
     B = cfg["batch"]
     G = int(args.group) or int(cfg.get("group", 0))
-    if G <= 0:  # auto: the largest group in 4..12 that divides K (no eager remainder), else 8
-        # (configs whose training chain dwarfs the build -- reddit GCN-3, deep
-        # SAGE-4 -- set group=1: grouping measured slower there, 0.60M vs 0.68M)
-        G = next((g for g in range(12, 3, -1) if args.steps % g == 0), 8)
+    if G <= 0:
+        G = auto_group(args.steps)
     tr = Trainer(g, table, model, cfg["fanout"], B, cfg["seed"], group=G)
     iters = tr.begin_epoch(0)
     torch.cuda.synchronize()
@@ -566,7 +576,7 @@ def run_distributed(args, cfg):
     # rule as N = 1 (N=2: 12.05M at G=1, 12.27M at G=5, 13.29M at G=10)
     G = int(args.group) or int(cfg.get("group", 0))
     if G <= 0:
-        G = next((g_ for g_ in range(12, 3, -1) if args.steps % g_ == 0), 8)
+        G = auto_group(args.steps)
     tr = MicrographTrainer(g, part, model, cfg["fanout"], B, cfg["seed"], mode=mode,
                            pregather=args.pregather, graph_group=G, allreduce=args.allreduce)
     iters = tr.begin_epoch(0)
