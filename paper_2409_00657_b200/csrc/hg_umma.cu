@@ -213,23 +213,9 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * BM_T, n0 = blockIdx.y * BN_T;
   pdl_trigger();
-  pdl_wait();
-  const int M = args.M_dev ? *args.M_dev : args.M;
-  const int K = args.K_dev ? *args.K_dev : args.K;
-  if (m0 >= M) {  // whole CTA exits together (before any barrier)
-    if constexpr (EPI == UEPI_SOFTMAX_CE)
-      for (int row = m0 + threadIdx.x; row < min(m0 + BM_T, args.n_cap); row += blockDim.x)
-        head_zero_row(args, row);
-    return;
-  }
-  // K range of this split, in 64-wide blocks
-  const int kblocks = (K + BK_T - 1) / BK_T;
-  const int per = (kblocks + gridDim.z - 1) / gridDim.z;
-  const int kb0 = blockIdx.z * per;
-  const int kb1 = min(kblocks, kb0 + per);
-  if (kb0 >= kb1) return;
-  const int nk = kb1 - kb0;
-
+  // prologue that reads nothing a predecessor writes -- barrier init and the
+  // tensor-map prefetch -- overlaps the previous kernel's tail (programmatic
+  // dependent launch); everything after pdl_wait() may read its outputs
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full_bar[s], 1);
@@ -238,10 +224,32 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     mbar_init(&done_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+  }
+  pdl_wait();
+  const int M = args.M_dev ? *args.M_dev : args.M;
+  const int K = args.K_dev ? *args.K_dev : args.K;
+  // K range of this split, in 64-wide blocks
+  const int kblocks = (K + BK_T - 1) / BK_T;
+  const int per = (kblocks + gridDim.z - 1) / gridDim.z;
+  const int kb0 = blockIdx.z * per;
+  const int kb1 = min(kblocks, kb0 + per);
+  if (m0 >= M || kb0 >= kb1) {  // whole CTA exits together (before any TMEM is held)
+    if constexpr (EPI == UEPI_SOFTMAX_CE)
+      if (m0 >= M)
+        for (int row = m0 + threadIdx.x; row < min(m0 + BM_T, args.n_cap); row += blockDim.x)
+          head_zero_row(args, row);
+    return;
+  }
+  const int nk = kb1 - kb0;
   if constexpr (EPI == UEPI_BIAS_RELU_BF16) {
     for (int c = threadIdx.x; c < BN_T; c += blockDim.x)
       bias_s[c] = n0 + c < args.N ? args.bias[n0 + c] : 0.f;
   }
+  // TMEM is allocated only after the predecessor completed: a CTA holding TMEM
+  // while waiting could starve a still-running predecessor CTA of its columns
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_base_sh)),
