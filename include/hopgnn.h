@@ -53,6 +53,9 @@ int hg_launch_count(long long* out, int reset);
 int hg_debug_build_phases(long long* out, int n);
 int hg_prof_enable(int on);
 int hg_prof_read(int site, double* total_ms, int* count);
+/* device timestamp (ns, %globaltimer) written to *slot in stream order
+   (capturable: times the branches of a replayed graph) */
+int hg_stamp(int64_t* slot, void* stream);
 
 /* ------------------------------------------------------------------------
  * 1. Reference kernel boundary (gnnsim.kernels, kernels.py:31-34)
@@ -363,6 +366,16 @@ typedef struct {
 /* Step variant (process-wide): 1 = softmax-CE fused into the tcgen05 head
  * GEMM's epilogue (C <= 192), 0 (default) = head GEMM + separate softmax-CE. */
 int hg_set_fused_head(int32_t on);
+
+/* Step variant (process-wide): 1 = training steps run the top of the
+ * network -- layer-L linear, classifier head, softmax-CE, dz_L with its bias
+ * gradient, dagg_L -- as one tcgen05 kernel per 128 roots (k_umma_top,
+ * tensor-core path, L >= 2, H <= 256, C <= 192); 0 (default) = the split
+ * kernels (measured faster on B200).  Results agree up to
+ * summation order. */
+int hg_set_fused_top(int32_t on);
+/* debug: phase timestamps of CTA 0 of later k_umma_top launches (NULL = off) */
+int hg_top_trace(int64_t* trace);
 
 /* Peer memory (one process per GPU): device allocations whose CUDA IPC
  * handles (64 bytes) other ranks map; and the reference pre-gather byte

@@ -96,6 +96,7 @@ SIGNATURES = {
     "hg_launch_count": [C.POINTER(C.c_longlong), C.c_int],
     "hg_prof_enable": [C.c_int],
     "hg_prof_read": [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int)],
+    "hg_stamp": [C.c_void_p, C.c_void_p],
     "hg_sample_frontier": [V, V, I64, V, I64, I32, U64, V, V, I64, PI64, V],
     "hg_feature_rows": [V, I64, I32, U64, V, V],
     "hg_feature_table": [V, I64, I64, I32, I32, U64, I32, V, V],
@@ -125,6 +126,8 @@ SIGNATURES = {
     "hg_mg_build_group_sharded": [C.POINTER(CsrShards), I64, V, I32, I32, V, V, I32,
                                   C.POINTER(MgLayout), V, C.POINTER(MgBatch), V, I32, V],
     "hg_set_fused_head": [I32],
+    "hg_set_fused_top": [I32],
+    "hg_top_trace": [C.c_void_p],
     "hg_train_step": [C.POINTER(StepDesc), I32, V],
     "hg_forward": [C.POINTER(StepDesc), I32, V],
     "hg_sgd_update": [V, V, V, I64, C.c_float, C.c_float, V],

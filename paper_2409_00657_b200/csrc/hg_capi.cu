@@ -109,6 +109,22 @@ extern "C" int hg_prof_read(int site, double* total_ms, int* count) {
   return HG_OK;
 }
 
+namespace hg {
+__global__ void k_stamp(int64_t* slot) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *slot = (int64_t)t;
+}
+}  // namespace hg
+
+// Device timestamp (ns, %globaltimer) into *slot when the stream reaches it;
+// capturable, so a graph replay's branches can be timed from inside the graph.
+extern "C" int hg_stamp(int64_t* slot, void* stream) {
+  hg::k_stamp<<<1, 1, 0, (cudaStream_t)stream>>>(slot);
+  HG_CUDA_TRY(cudaGetLastError());
+  return HG_OK;
+}
+
 extern "C" int hg_launch_count(long long* out, int reset) {
   *out = hg::g_launches.load();
   if (reset) hg::g_launches = 0;

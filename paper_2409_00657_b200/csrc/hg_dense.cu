@@ -893,6 +893,10 @@ __global__ void k_sgd(float* __restrict__ p, float* __restrict__ g, bf16* __rest
 int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb, bool b_mn,
               void* C, int64_t ldc, int M, int N, int K, const int32_t* M_dev,
               const int32_t* K_dev, int epi, const float* bias, int split, cudaStream_t s);
+int umma_top(const void* agg, const void* WlT, const void* Wb, const float* bias, const void* WcT,
+             const void* Wcp, void* h, void* dl, void* dz, float* dagg, int cap, int H, int C,
+             int inL, const int32_t* M_dev, const int64_t* roots, uint64_t label_state,
+             const int32_t* labels, float* loss, float* gb, cudaStream_t s);
 int umma_head_ce(const void* A, int64_t lda, const void* B, int64_t ldb, float* logits, int C,
                  int n_cap, int K, const int32_t* M_dev, const int64_t* roots, uint64_t label_state,
                  float* loss, __nv_bfloat16* dl_lowp, int ldp, cudaStream_t s);
@@ -1001,6 +1005,15 @@ static void scatter_root_attrs() {
 // GEMM has only n_roots / 128 CTAs, the separate kernel a warp per root).
 static int g_fused_head = 0;
 static bool fused_head_on() { return g_fused_head != 0; }
+// Opt-in (hg_set_fused_top): training steps run the top of the network
+// (layer-L GEMM through the dX GEMM of layer L) as one kernel per 128 roots
+// (k_umma_top).  Measured on B200 at the papers shape (phase timestamps,
+// scripts/bench_train.py HG_TOP_TRACE=1): 27 us per launch against ~19.5 us
+// for the six split kernels in the replayed graph -- each CTA streams all
+// four weight operands (~870 KB) through one SM and runs 128 rows of
+// epilogue work (softmax, masks, column sums) on that SM, where the split
+// kernels spread both over 24-128 CTAs.  The parity tests run both paths.
+static int g_fused_top = 0;
 
 // bf16 dz operand of layer k (per-layer region when lowp_layered)
 static inline bf16* dz_lowp(const hg_step_desc* d, int k) {
@@ -1060,6 +1073,12 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     cudaStreamWaitEvent(s, side->ev[n_fork], 0);
     n_fork = 0;
   };
+  const int Cp = (C + 63) / 64 * 64;
+  const bool tc_head = tc && C <= 256 && d->WcT && d->Wcp && d->dl_lowp;
+  // fused top (k_umma_top): layer-L linear, head, softmax-CE, dz_L, dagg_L
+  const bool top_fused = backward && tc_head && g_fused_top && L >= 2 &&
+                         (d->in_dim[L] == H || d->in_dim[L] == 2 * H) && d->Wb[L] &&
+                         C <= 192;
   // ---- forward
   prof_begin(PROF_STEP, s);
   if (tc && !d->lowp_fresh) {
@@ -1072,6 +1091,24 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
   }
   for (int k = 1; k <= L; ++k) {
     if (k > 1 || !d->agg1_ready) launch_aggregate<T>(d, k, s, tc && backward);
+    if (k == L && top_fused) {
+      if (!d->lowp_fresh) {
+        dim3 g((C + 31) / 32, (H + 31) / 32), b(32, 8);
+        count_launch(2);
+        k_transpose_bf16<<<g, b, 0, s>>>(d->Wc, H, C, (bf16*)d->WcT, nullptr);
+        k_pad_bf16<<<64, 256, 0, s>>>(d->Wc, H, C, (bf16*)d->Wcp, Cp);
+      }
+      int st = umma_top(d->agg[L], d->Wlp[L], d->Wb[L], d->b[L], d->WcT, d->Wcp, d->h[L],
+                        d->dl_lowp, dz_lowp(d, L), d->dagg, d->max_rows[L], H, C, d->in_dim[L],
+                        tot + L, d->roots, d->label_state, d->labels, d->loss, d->gb[L], s);
+      if (st) { join(); return st; }
+      // gW_c += h_Lᵀ dlogits, beside the rest of the backward
+      const int split = std::max(1, std::min(16, n_roots / 256));
+      st = umma_gemm(d->h[L], H, true, d->dl_lowp, Cp, true, d->gWc, C, H, C, n_roots, nullptr,
+                     tot + L, 2, nullptr, split, fork());
+      if (st) { join(); return st; }
+      break;
+    }
     if (k == 1) prof_begin(PROF_GEMM1, s);
     if (tc) {
       int st = umma_gemm(d->agg[k], d->in_dim[k], false, d->Wlp[k], d->in_dim[k], false, d->h[k], H,
@@ -1085,9 +1122,9 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     if (k == 1) prof_end(PROF_GEMM1, s);
   }
   // classifier head (model.py:246, 253-265)
-  const bool tc_head = tc && C <= 256 && d->WcT && d->Wcp && d->dl_lowp;
-  const int Cp = (C + 63) / 64 * 64;
-  if (tc_head) {
+  if (top_fused) {
+    // done by k_umma_top
+  } else if (tc_head) {
     // logits = h_L @ W_c on tcgen05 (B = W_cᵀ bf16, K-major); softmax-CE writes
     // dlogits (f32 in place + bf16 padded copy for the backward GEMMs)
     if (!d->lowp_fresh) {
@@ -1171,7 +1208,9 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
     }
     if (k == 1) { prof_end(PROF_DW1, s); break; }  // layer-1 dX is unused (features are not trainable)
     // dagg_k = dz_k W_k^T
-    if (tc && d->in_dim[k] % 64 == 0 && d->Wb[k]) {
+    if (k == L && top_fused) {
+      // written by k_umma_top
+    } else if (tc && d->in_dim[k] % 64 == 0 && d->Wb[k]) {
       int st = umma_gemm(dz_lowp(d, k), H, false, d->Wb[k], H, false, d->dagg, d->in_dim[k],
                          d->max_rows[k], d->in_dim[k], H, tot + k, nullptr, 0, nullptr, 1, s);
       if (st) { join(); return st; }
@@ -1250,6 +1289,11 @@ static int validate(const hg_step_desc* d, int n_roots) {
 }  // namespace hg
 
 using namespace hg;
+
+extern "C" int hg_set_fused_top(int32_t on) {
+  hg::g_fused_top = on != 0;
+  return HG_OK;
+}
 
 extern "C" int hg_set_fused_head(int32_t on) {
   g_fused_head = on ? 1 : 0;

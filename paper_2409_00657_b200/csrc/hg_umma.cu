@@ -199,8 +199,9 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
             const __grid_constant__ CUtensorMap map_c, UmmaArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-aligned stage ring
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~(uintptr_t)1023);
+  // 1024-byte aligned by pointer arithmetic on the shared array (an integer
+  // round trip would turn every access into a generic one)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int A_BYTES = BM_T * BK_T * 2;
   constexpr int B_BYTES = BN_T * BK_T * 2;
   constexpr int STAGE = A_BYTES + B_BYTES;
@@ -619,7 +620,547 @@ int umma_head_ce(const void* A, int64_t lda, const void* B, int64_t ldb, float* 
   return launch_t<false, false, 192, UEPI_SOFTMAX_CE>(ma, mb, mc, a, 1, s);
 }
 
+
+// ------------------------------------------------------------ fused top step
+// The top of the step for one 128-root tile in ONE kernel (model.py:236-285
+// for k = L plus the head): five dependent GEMM/epilogue stages that used to
+// be six launches (layer-L GEMM, head GEMM, softmax-CE, dz GEMM, mask +
+// column sums, dX GEMM), each a latency-bound grid of <= 32 CTAs.
+//   1. acc[0,H)      = agg_L  @ W_L            -> h_L = bf16(relu(. + b_L))
+//   2. acc[H,H+Cn)   = h_L    @ W_c            -> softmax-CE: loss, dlogits (bf16)
+//   3. acc[0,H)      = dl     @ W_cᵀ           -> dz_L = . * (h_L > 0), gb_L += colsum
+//   4. acc[0,inL)    = dz_L   @ W_Lᵀ           -> dagg_L (f32, for k_scatter_top)
+// h_L, dl and dz_L live in shared memory in the UMMA K-major 128B-swizzled
+// layout (each is the next stage's A operand) and leave through TMA stores
+// (h_L, dl and dz_L for the weight-gradient GEMMs, dagg_L for the scatter).
+// Warp roles: warp 0 lane 0 streams every stage's weight tiles through a
+// 2-deep ring (it runs ahead into the next stage while an epilogue runs),
+// warp 1 lane 0 issues the MMAs, warps 2-17 are the epilogue (TMEM lane
+// quadrant = warp % 4, one root row per lane, four warps per quadrant splitting
+// the columns; a thread-per-row epilogue on four warps spent ~30 us of
+// dependent per-thread work on the softmax and masks).  Numerics are the split
+// kernels' (same operands, same rounding points); only the order of the
+// softmax and column sums differs.
+struct TopArgs {
+  int n_cap;               // root capacity (rows of every operand)
+  const int32_t* M_dev;    // device root count N_L
+  int H, C, Cn, Cp, inL;   // hidden, classes, classes rounded to 16 / to 64, layer-L input width
+  const float* bias;       // b_L [H]
+  const int64_t* roots;
+  uint64_t label_state;
+  const int32_t* labels;   // explicit labels or null (hashed)
+  float* loss;             // [n_cap]
+  float* gb;               // gb_L [H] (accumulated)
+  int64_t* trace;          // optional phase timestamps of CTA 0 (hg_top_trace)
+};
+static int64_t* g_top_trace = nullptr;
+
+__device__ __forceinline__ void top_stamp(const TopArgs& a, int i) {
+  if (a.trace && blockIdx.x == 0) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[i] = (int64_t)t;
+  }
+}
+
+constexpr int kTopSlices = 4;                      // epilogue warps per TMEM lane quadrant
+constexpr int kTopEpiWarps = 4 * kTopSlices;
+constexpr int kTopThreads = 64 + 32 * kTopEpiWarps;  // producer + MMA warps + epilogue
+constexpr int kTopA = BM_T * BK_T * 2;         // 16 KB
+constexpr int kTopStage = kTopA + 256 * BK_T * 2;  // + 32 KB B tile
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void epi_sync() {  // the epilogue warps only
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * kTopEpiWarps) : "memory");
+}
+// byte offset of the 16-byte unit u (8 bf16 / 4 f32) of row r in a
+// 128-row x 128-byte K-major SW128 chunk (the TMA / UMMA layout)
+__device__ __forceinline__ int sw128(int r, int u) { return r * 128 + ((u ^ (r & 7)) << 4); }
+
+__device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
+  const __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&t);
+}
+
+// Column sums of a 32-row x 16-column register block (lane = row): after the
+// butterfly, lane l holds the sum of column ((l>>4)&1)*8 + ((l>>3)&1)*4 +
+// ((l>>2)&1)*2 + ((l>>1)&1) (both lanes of each pair).
+__device__ __forceinline__ float colsum16(float (&v)[16], int lane) {
+#pragma unroll
+  for (int o = 16, n = 8; o >= 2; o >>= 1, n >>= 1) {
+    const bool hi = lane & o;
+#pragma unroll
+    for (int j = 0; j < n; ++j) {
+      const float keep = hi ? v[j + n] : v[j];
+      const float send = hi ? v[j] : v[j + n];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+__global__ void __launch_bounds__(kTopThreads, 1)
+k_umma_top(const __grid_constant__ CUtensorMap map_agg, const __grid_constant__ CUtensorMap map_w,
+           const __grid_constant__ CUtensorMap map_wct, const __grid_constant__ CUtensorMap map_wcp,
+           const __grid_constant__ CUtensorMap map_wb, const __grid_constant__ CUtensorMap map_h,
+           const __grid_constant__ CUtensorMap map_dl, const __grid_constant__ CUtensorMap map_dz,
+           const __grid_constant__ CUtensorMap map_dagg, TopArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte aligned by pointer arithmetic on the shared array (an integer
+  // round trip would turn every access into a generic one)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  // Layout: slots 0-1 [0, 96K) always; dl at 96K; h_L / dz_L at
+  // max(96K + |dl|, 144K).  The load ring has four 48 KB slots while the first
+  // GEMM runs (slots 2-3 overlay dl and h_L, both idle then), three during the
+  // head and dX GEMMs (slot 2 overlays dl) and two during the dz GEMM (dl is
+  // its A operand): phase p's loads cycle over top_slot(p, i).
+  uint8_t* dls = smem + 2 * kTopStage;
+  uint8_t* hs = smem + max(2 * kTopStage + (a.Cp / 64) * 16384, 3 * kTopStage);
+  __shared__ __align__(8) uint64_t full_bar[4], empty_bar[4];
+  __shared__ __align__(8) uint64_t acc_bar[4], opnd_bar[3];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ float bias_s[256];
+  __shared__ float red[4][256];
+  __shared__ float part[2][kTopSlices][BM_T];  // per-slice softmax max / sum-exp
+  __shared__ float xl_s[BM_T];                 // label logit per row
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM_T;
+  const int H = a.H, C = a.C, Cn = a.Cn, Cp = a.Cp, inL = a.inL;
+  pdl_trigger();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 4; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int p = 0; p < 4; ++p) mbar_init(&acc_bar[p], 1);
+    for (int p = 0; p < 3; ++p) mbar_init(&opnd_bar[p], 32 * kTopEpiWarps);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    const CUtensorMap* maps[5] = {&map_agg, &map_w, &map_wct, &map_wcp, &map_wb};
+    for (auto m : maps)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+  }
+  pdl_wait();
+  const int M = *a.M_dev;
+  if (m0 >= M) {  // no roots in this tile: zero its loss rows, no TMEM taken
+    for (int r = m0 + threadIdx.x; r < min(m0 + BM_T, a.n_cap); r += blockDim.x) a.loss[r] = 0.f;
+    return;
+  }
+  for (int c = threadIdx.x; c < H; c += blockDim.x) bias_s[c] = a.bias[c];
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_sh)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base_sh;
+  const int kb_in = inL / 64, kb_h = H / 64, kb_c = Cp / 64, n_half = (inL + 255) / 256;
+  // slot of the i-th load of phase p (see the layout above)
+  auto top_slot = [](int p, int i) { return p == 0 ? i & 3 : p == 2 ? i & 1 : (i + 2) % 3; };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer: every stage's tiles, in MMA order
+      int uses[4] = {0, 0, 0, 0}, n = 0;
+      top_stamp(a, 0);
+      auto acquire = [&](int p, int i, uint32_t bytes) -> uint8_t* {
+        const int s = top_slot(p, i);
+        if (uses[s] > 0) mbar_wait(&empty_bar[s], (uses[s] - 1) & 1);
+        ++uses[s];
+        if (n < 31) top_stamp(a, 1 + n);
+        ++n;
+        mbar_expect_tx(&full_bar[s], bytes);
+        return smem + s * kTopStage;
+      };
+      for (int kb = 0; kb < kb_in; ++kb) {
+        uint8_t* st = acquire(0, kb, kTopA + H * 128);
+        tma_load_2d(st, &map_agg, &full_bar[top_slot(0, kb)], kb * 64, m0);
+        tma_load_2d(st + kTopA, &map_w, &full_bar[top_slot(0, kb)], kb * 64, 0);
+      }
+      for (int kb = 0; kb < kb_h; ++kb) {
+        uint8_t* st = acquire(1, kb, Cn * 128);
+        tma_load_2d(st + kTopA, &map_wct, &full_bar[top_slot(1, kb)], kb * 64, 0);
+      }
+      for (int kb = 0; kb < kb_c; ++kb) {
+        uint8_t* st = acquire(2, kb, H * 128);
+        tma_load_2d(st + kTopA, &map_wcp, &full_bar[top_slot(2, kb)], kb * 64, 0);
+      }
+      mbar_wait(&acc_bar[2], 0);  // slot 2 overlays dl, the dz GEMM's A operand
+      for (int hf = 0, i = 0; hf < n_half; ++hf) {
+        const int nb = min(256, inL - hf * 256);
+        for (int kb = 0; kb < kb_h; ++kb, ++i) {
+          uint8_t* st = acquire(3, i, nb * 128);
+          tma_load_2d(st + kTopA, &map_wb, &full_bar[top_slot(3, i)], kb * 64, hf * 256);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      int uses[4] = {0, 0, 0, 0}, n = 0;
+      auto consume = [&](int p, int i) -> uint32_t {
+        const int s = top_slot(p, i);
+        mbar_wait(&full_bar[s], uses[s] & 1);
+        ++uses[s];
+        if (n < 32) top_stamp(a, 32 + n);
+        ++n;
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        return smem_u32(smem + s * kTopStage);
+      };
+      auto mma_k64 = [&](uint32_t d, uint32_t sa, uint32_t sb, uint32_t idesc, bool first) {
+#pragma unroll
+        for (int kk = 0; kk < BK_T / 16; ++kk)
+          umma_bf16(d, make_desc(sa + kk * 32, 16, 1024), make_desc(sb + kk * 32, 16, 1024), idesc,
+                    (!first || kk > 0) ? 1u : 0u);
+      };
+      // 1. agg_L @ W_L  -> TMEM [0, H)
+      for (int kb = 0; kb < kb_in; ++kb) {
+        const uint32_t st = consume(0, kb);
+        mma_k64(tmem, st, st + kTopA, make_idesc(H, false, false), kb == 0);
+        umma_commit(&empty_bar[top_slot(0, kb)]);
+      }
+      umma_commit(&acc_bar[0]);
+      // 2. h_L @ W_c  -> TMEM [H, H + Cn)
+      mbar_wait(&opnd_bar[0], 0);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      for (int kb = 0; kb < kb_h; ++kb) {
+        const uint32_t st = consume(1, kb);
+        mma_k64(tmem + H, smem_u32(hs + kb * 16384), st + kTopA, make_idesc(Cn, false, false), kb == 0);
+        umma_commit(&empty_bar[top_slot(1, kb)]);
+      }
+      umma_commit(&acc_bar[1]);
+      // 3. dl @ W_cᵀ  -> TMEM [0, H)
+      mbar_wait(&opnd_bar[1], 0);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      for (int kb = 0; kb < kb_c; ++kb) {
+        const uint32_t st = consume(2, kb);
+        mma_k64(tmem, smem_u32(dls + kb * 16384), st + kTopA, make_idesc(H, false, false), kb == 0);
+        umma_commit(&empty_bar[top_slot(2, kb)]);
+      }
+      umma_commit(&acc_bar[2]);
+      // 4. dz_L @ W_Lᵀ  -> TMEM [0, inL), 256 columns per MMA
+      mbar_wait(&opnd_bar[2], 0);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      for (int hf = 0, i = 0; hf < n_half; ++hf) {
+        const int nb = min(256, inL - hf * 256);
+        for (int kb = 0; kb < kb_h; ++kb, ++i) {
+          const uint32_t st = consume(3, i);
+          mma_k64(tmem + hf * 256, smem_u32(hs + kb * 16384), st + kTopA, make_idesc(nb, false, false),
+                  kb == 0);
+          umma_commit(&empty_bar[top_slot(3, i)]);
+        }
+      }
+      umma_commit(&acc_bar[3]);
+    }
+  } else {
+    // ---------------- epilogue warps 2..17: four per TMEM lane quadrant q (one
+    // root row per lane), the columns dealt out over the four (slice j)
+    const int q = warp & 3, j = (warp - 2) >> 2;
+    const int et = (warp - 2) * 32 + lane;  // 0..511
+    const int rl = q * 32 + lane;           // row in the tile
+    const int row = m0 + rl;
+    const bool valid = row < M;
+    const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
+    const bool leader = warp == 2 && lane == 0;
+    if (leader) top_stamp(a, 72);
+    // 1. h_L = bf16(relu(acc + b)) -> hs (A operand of 2, TMA store to h_L)
+    mbar_wait(&acc_bar[0], 0);
+    if (leader) top_stamp(a, 64);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    for (int c32 = j; c32 < H / 32; c32 += kTopSlices) {
+      uint32_t r[32];
+      tmem_ld16_issue(tl + c32 * 32, r);
+      tmem_ld16_issue(tl + c32 * 32 + 16, r + 16);
+      tmem_wait16(r);
+      tmem_wait16(r + 16);
+      uint8_t* base = hs + (c32 >> 1) * 16384;
+#pragma unroll
+      for (int uu = 0; uu < 4; ++uu) {
+        const int u = (c32 & 1) * 4 + uu;
+        uint32_t pk[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int c = c32 * 32 + uu * 8 + 2 * t;
+          const float x0 = valid ? fmaxf(__uint_as_float(r[uu * 8 + 2 * t]) + bias_s[c], 0.f) : 0.f;
+          const float x1 = valid ? fmaxf(__uint_as_float(r[uu * 8 + 2 * t + 1]) + bias_s[c + 1], 0.f) : 0.f;
+          pk[t] = pack_bf2(x0, x1);
+        }
+        *reinterpret_cast<uint4*>(base + sw128(rl, u)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    mbar_arrive(&opnd_bar[0]);
+    if (leader) top_stamp(a, 65);
+    epi_sync();
+    if (leader) {
+      for (int c64 = 0; c64 < kb_h; ++c64) tma_store_2d<false>(&map_h, hs + c64 * 16384, c64 * 64, m0);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    // 2. softmax-CE over the C logits of this row (model.py:253-259); each
+    //    slice takes 16-column groups g = j, j + 4, ...; max and sum-exp are
+    //    combined across the four slices in shared memory
+    mbar_wait(&acc_bar[1], 0);
+    if (leader) top_stamp(a, 66);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tcl = tl + H;
+    // this slice's 16-column groups g = j + 4t held in registers across the
+    // three passes (one TMEM sweep, one exponential per logit)
+    constexpr int kG = 192 / 16 / kTopSlices;
+    float xv[kG][16];
+    float mx = -INFINITY;
+    // (C is uniform: only the last group needs per-column guards)
+#pragma unroll
+    for (int t = 0; t < kG; ++t) {
+      const int c16 = (j + kTopSlices * t) * 16;
+      if (c16 < Cn) {
+        uint32_t r[16];
+        tmem_ld16(tcl + c16, r);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) xv[t][e] = __uint_as_float(r[e]);
+        if (c16 + 16 <= C) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) mx = fmaxf(mx, xv[t][e]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (c16 + e < C) mx = fmaxf(mx, xv[t][e]);
+        }
+      }
+    }
+    if (leader) top_stamp(a, 73);
+    part[0][j][rl] = mx;
+    const int label = valid ? (a.labels ? a.labels[row]
+                                        : (int)(mix64(a.label_state ^ (uint64_t)a.roots[row]) %
+                                                (uint64_t)C))
+                            : -1;
+    if (leader) top_stamp(a, 74);
+    epi_sync();
+    if (leader) top_stamp(a, 75);
+    mx = fmaxf(fmaxf(part[0][0][rl], part[0][1][rl]), fmaxf(part[0][2][rl], part[0][3][rl]));
+    float sum = 0.f;
+#pragma unroll
+    for (int t = 0; t < kG; ++t) {
+      const int c16 = (j + kTopSlices * t) * 16;
+      if (c16 < Cn) {
+        const unsigned lo = (unsigned)(label - c16);
+        if (lo < 16u) {  // this row's label logit (one group per row)
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            if (e == (int)lo) xl_s[rl] = xv[t][e];
+        }
+        if (c16 + 16 <= C) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            xv[t][e] = __expf(xv[t][e] - mx);
+            sum += xv[t][e];
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            xv[t][e] = c16 + e < C ? __expf(xv[t][e] - mx) : 0.f;
+            sum += xv[t][e];
+          }
+        }
+      }
+    }
+    part[1][j][rl] = sum;
+    if (leader) top_stamp(a, 76);
+    epi_sync();
+    if (leader) top_stamp(a, 77);
+    sum = (part[1][0][rl] + part[1][1][rl]) + (part[1][2][rl] + part[1][3][rl]);
+    const float inv = valid ? 1.0f / sum : 0.f;  // capacity rows: dlogits 0
+    // dlogits = softmax - onehot(label), bf16 into dl (the onehot term is
+    // applied to the one label column afterwards)
+#pragma unroll
+    for (int t = 0; t < kG; ++t) {
+      const int c16 = (j + kTopSlices * t) * 16;
+      if (c16 >= Cp) continue;
+      uint32_t pk[8];
+      if (c16 + 16 <= C) {
+#pragma unroll
+        for (int q2 = 0; q2 < 8; ++q2) pk[q2] = pack_bf2(xv[t][2 * q2] * inv, xv[t][2 * q2 + 1] * inv);
+      } else if (c16 < Cn) {
+#pragma unroll
+        for (int q2 = 0; q2 < 8; ++q2)
+          pk[q2] = pack_bf2(c16 + 2 * q2 < C ? xv[t][2 * q2] * inv : 0.f,
+                            c16 + 2 * q2 + 1 < C ? xv[t][2 * q2 + 1] * inv : 0.f);
+      } else {
+#pragma unroll
+        for (int q2 = 0; q2 < 8; ++q2) pk[q2] = 0u;
+      }
+      uint8_t* base = dls + (c16 / 64) * 16384;
+      const int u0 = (c16 % 64) / 8;
+      *reinterpret_cast<uint4*>(base + sw128(rl, u0)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      *reinterpret_cast<uint4*>(base + sw128(rl, u0 + 1)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      if ((unsigned)(label - c16) < 16u) {
+        const float g = __expf(xl_s[rl] - mx) * inv - 1.f;
+        *reinterpret_cast<__nv_bfloat16*>(dls + (label / 64) * 16384 + sw128(rl, (label % 64) / 8) +
+                                          (label % 8) * 2) = __float2bfloat16_rn(g);
+      }
+    }
+    if (leader) top_stamp(a, 78);
+    if (j == 0) {
+      if (valid) a.loss[row] = logf(sum) - (xl_s[rl] - mx);
+      else if (row < a.n_cap) a.loss[row] = 0.f;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    mbar_arrive(&opnd_bar[1]);
+    if (leader) top_stamp(a, 67);
+    epi_sync();
+    if (leader) {
+      for (int c64 = 0; c64 < kb_c; ++c64) tma_store_2d<false>(&map_dl, dls + c64 * 16384, c64 * 64, m0);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    // 3. dz_L = (dl @ W_cᵀ) * (h_L > 0) in place of h_L in hs; gb_L column sums
+    mbar_wait(&acc_bar[2], 0);
+    if (leader) top_stamp(a, 68);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // h_L store has read hs
+    epi_sync();
+    for (int c32 = j; c32 < H / 32; c32 += kTopSlices) {
+      uint32_t r[32];
+      tmem_ld16_issue(tl + c32 * 32, r);
+      tmem_ld16_issue(tl + c32 * 32 + 16, r + 16);
+      tmem_wait16(r);
+      tmem_wait16(r + 16);
+      uint8_t* base = hs + (c32 >> 1) * 16384;
+#pragma unroll
+      for (int g16 = 0; g16 < 2; ++g16) {
+        float v[16];
+#pragma unroll
+        for (int uu = 0; uu < 2; ++uu) {
+          const int ul = g16 * 2 + uu;          // unit within the 32 columns
+          const int u = (c32 & 1) * 4 + ul;     // unit within the 64-column chunk
+          uint4 hv = *reinterpret_cast<const uint4*>(base + sw128(rl, u));
+          const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+          uint32_t pk[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const __nv_bfloat162 hb = *reinterpret_cast<const __nv_bfloat162*>(&hw[t]);
+            const float x0 = valid && __low2float(hb) > 0.f ? __uint_as_float(r[ul * 8 + 2 * t]) : 0.f;
+            const float x1 = valid && __high2float(hb) > 0.f ? __uint_as_float(r[ul * 8 + 2 * t + 1]) : 0.f;
+            v[uu * 8 + 2 * t] = x0;
+            v[uu * 8 + 2 * t + 1] = x1;
+            pk[t] = pack_bf2(x0, x1);
+          }
+          *reinterpret_cast<uint4*>(base + sw128(rl, u)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+        const float cs = colsum16(v, lane);
+        const int col = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+        if ((lane & 1) == 0) red[q][c32 * 32 + g16 * 16 + col] = cs;
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    mbar_arrive(&opnd_bar[2]);
+    if (leader) top_stamp(a, 69);
+    epi_sync();
+    if (leader) {
+      for (int c64 = 0; c64 < kb_h; ++c64) tma_store_2d<false>(&map_dz, hs + c64 * 16384, c64 * 64, m0);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    for (int c = et; c < H; c += 32 * kTopEpiWarps)
+      atomicAdd(a.gb + c, (red[0][c] + red[1][c]) + (red[2][c] + red[3][c]));
+    // 4. dagg_L -> global f32 in 16 KB boxes (128 rows x 32 columns): the four
+    //    warps of slice j (one per lane quadrant) fill a box, one of them
+    //    hands it to TMA; two boxes per slice in flight
+    mbar_wait(&acc_bar[3], 0);
+    if (leader) top_stamp(a, 70);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (leader) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // dl / dz stores done
+    epi_sync();
+    {
+      uint8_t* stg = smem + j * 2 * 16384;  // slots 0-2 (idle now)
+      const bool issuer = q == 2 && lane == 0;  // warp 2 + 4j
+      int n = 0;
+      for (int b = j; b < inL / 32; b += kTopSlices, ++n) {
+        uint8_t* buf = stg + (n & 1) * 16384;
+        if (n >= 2) {
+          if (issuer) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          asm volatile("bar.sync %0, 128;" ::"r"(2 + j) : "memory");
+        }
+        uint32_t r[32];
+        tmem_ld16_issue(tl + b * 32, r);
+        tmem_ld16_issue(tl + b * 32 + 16, r + 16);
+        tmem_wait16(r);
+        tmem_wait16(r + 16);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          *reinterpret_cast<uint4*>(buf + sw128(rl, u)) =
+              make_uint4(r[u * 4], r[u * 4 + 1], r[u * 4 + 2], r[u * 4 + 3]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + j) : "memory");
+        if (issuer) {
+          tma_store_2d<false>(&map_dagg, buf, b * 32, m0);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+      if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    if (leader) top_stamp(a, 71);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// Host side of k_umma_top.  Shapes: agg_L [cap x inL] bf16, W_L operand WlT
+// [H x inL] (= W_Lᵀ, K-major), W_L straight copy Wb [inL x H], WcT [C x H],
+// Wcp [H x Cp] (W_c zero-padded), h_L [cap x H] bf16, dl [cap x Cp] bf16,
+// dz_L [cap x H] bf16, dagg [cap x inL] f32.
+int umma_top(const void* agg, const void* WlT, const void* Wb, const float* bias, const void* WcT,
+             const void* Wcp, void* h, void* dl, void* dz, float* dagg, int cap, int H, int C,
+             int inL, const int32_t* M_dev, const int64_t* roots, uint64_t label_state,
+             const int32_t* labels, float* loss, float* gb, cudaStream_t s) {
+  const int Cn = (C + 15) / 16 * 16, Cp = (C + 63) / 64 * 64;
+  if (H % 64 || H < 64 || H > 256) return hg_fail(HG_ECONFIG, "fused top: hidden must be 64..256, a multiple of 64");
+  if (C < 1 || Cp > 192 || H + Cn > 512) return hg_fail(HG_ECONFIG, "fused top: needs 1 <= classes <= 192");
+  if (inL % 64 || inL > 512) return hg_fail(HG_ECONFIG, "fused top: bad layer input width %d", inL);
+  if (cap < 1) return HG_OK;
+  CUtensorMap m_agg, m_w, m_wct, m_wcp, m_wb, m_h, m_dl, m_dz, m_dagg;
+  int st;
+  if ((st = make_map(&m_agg, agg, inL, cap, inL, BK_T, BM_T))) return st;
+  if ((st = make_map(&m_w, WlT, inL, H, inL, BK_T, H))) return st;
+  if ((st = make_map(&m_wct, WcT, H, C, H, BK_T, Cn))) return st;
+  if ((st = make_map(&m_wcp, Wcp, Cp, H, Cp, BK_T, H))) return st;
+  if ((st = make_map(&m_wb, Wb, H, inL, H, BK_T, std::min(256, inL)))) return st;
+  if ((st = make_map(&m_h, h, H, cap, H, BK_T, BM_T))) return st;
+  if ((st = make_map(&m_dl, dl, Cp, cap, Cp, BK_T, BM_T))) return st;
+  if ((st = make_map(&m_dz, dz, H, cap, H, BK_T, BM_T))) return st;
+  if ((st = make_map(&m_dagg, dagg, inL, cap, inL, 32, BM_T, 4))) return st;
+  TopArgs a{cap, M_dev, H, C, Cn, Cp, inL, bias, roots, label_state, labels, loss, gb, g_top_trace};
+  const int hs_off = std::max(2 * kTopStage + (Cp / 64) * 16384, 3 * kTopStage);
+  const int smem = std::max(hs_off + (H / 64) * 16384, 4 * kTopStage) + 1024;
+  static int attr = 0;
+  if (smem > attr) {
+    HG_CUDA_TRY(cudaFuncSetAttribute(k_umma_top, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = smem;
+  }
+  count_launch();
+  HG_CUDA_TRY(launch_pdl(k_umma_top, dim3((cap + BM_T - 1) / BM_T), dim3(kTopThreads), smem, s, m_agg,
+                         m_w, m_wct, m_wcp, m_wb, m_h, m_dl, m_dz, m_dagg, a));
+  return HG_OK;
+}
+
 }  // namespace hg
+
+// Debug: phase timestamps (%globaltimer ns) of CTA 0 of every later
+// k_umma_top launch into trace[0..72) (null = off).  [0] producer start,
+// [1+i] load i issued, [32+i] load i landed, [64..71] epilogue phases.
+extern "C" int hg_top_trace(int64_t* trace) {
+  hg::g_top_trace = trace;
+  return HG_OK;
+}
 
 extern "C" int hg_gemm_bf16(const void* A, int64_t lda, int a_mn_major, const void* B, int64_t ldb,
                             int b_mn_major, void* C, int64_t ldc, int32_t M, int32_t N, int32_t K,

@@ -70,3 +70,18 @@ for per in (1, 10):
     print(f"train chain, {per} step(s) per graph: {e0.elapsed_time(e1) * 1000 / (reps * per):.1f} us/step")
 tot = run.builder.tensors["totals"].cpu().numpy()
 print("batch N_k", tot[:len(cfg['fanout']) + 1].tolist(), "loss", float(run.loss[:B].sum()))
+if os.environ.get("HG_TOP_TRACE"):
+    tb = torch.zeros(96, dtype=torch.int64, device="cuda")
+    _lib.call("hg_top_trace", tb.data_ptr())
+    for _ in range(3):
+        step(s)
+    torch.cuda.synchronize()
+    _lib.call("hg_top_trace", None)
+    t = tb.cpu().numpy()
+    t0 = t[72]
+    rel = lambda i: round((t[i] - t0) / 1000.0, 2) if t[i] else None  # noqa: E731
+    print("top trace (us from epilogue start): producer start", rel(0))
+    print(" load issued", [rel(1 + i) for i in range(24)])
+    print(" load landed", [rel(32 + i) for i in range(24)])
+    print(" epilogue", [rel(64 + i) for i in range(8)])
+    print(" softmax", [rel(73 + i) for i in range(6)])

@@ -72,7 +72,7 @@ def _device_masks(run, batch, n, L):
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16], ids=["f32", "bf16"])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}-{'x'.join(map(str, c[1]))}-D{c[2]}")
-def test_step_matches_oracle(world, case, dtype, fused_head=False):
+def test_step_matches_oracle(world, case, dtype, fused_head=False, fused_top=False):
     """fp32: loss, gradients and updated parameters within 1e-3 (norm-relative
     and max-abs / max|ref|) of the float64 oracle.  bf16: the oracle rounds to
     bf16 where the device stores (features, aggregates, activations, and on the
@@ -98,11 +98,13 @@ def test_step_matches_oracle(world, case, dtype, fused_head=False):
     st = np.uint64(chain(sseed, 0, 3)).view(np.int64)
     run.stage_roots(roots, [st], len(roots))
     _lib.call("hg_set_fused_head", int(fused_head))
+    _lib.call("hg_set_fused_top", int(fused_top))
     try:
         batch = run.launch()
         torch.cuda.synchronize()
     finally:
         _lib.call("hg_set_fused_head", 0)
+        _lib.call("hg_set_fused_top", 0)
     run.check()
     bf = dtype == torch.bfloat16
     tc = bf and H % 64 == 0
@@ -138,7 +140,7 @@ def test_step_matches_oracle(world, case, dtype, fused_head=False):
             rec[f"param[{i}] mask-forced"] = dict(zip(("max_abs_rel", "norm_rel"), errors(a, b)))
     tag = "tc" if tc else str(dtype).split(".")[-1]
     _report(f"step_{arch}_{'x'.join(map(str, fo))}_D{D}_H{H}_C{C}_{tag}"
-            + ("_fusedhead" if fused_head else ""),
+            + ("_fusedhead" if fused_head else "") + ("_fusedtop" if fused_top else ""),
             {"tol": tol, "max_factor": mf, "errors": rec})
     for what, (a, b) in got.items():
         if bf and what != "loss":
@@ -161,6 +163,17 @@ def test_fused_head_matches_oracle(world, case):
     (umma_head_ce) instead of the separate k_softmax_ce; 96 roots in a
     128-root capacity also exercise the zeroed capacity rows."""
     test_step_matches_oracle(world, case, torch.bfloat16, fused_head=True)
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c[3] % 64 == 0],
+                         ids=lambda c: f"{c[0]}-{'x'.join(map(str, c[1]))}-D{c[2]}-H{c[3]}")
+def test_fused_top_matches_oracle(world, case):
+    """hg_set_fused_top(1): layer-L GEMM, head GEMM, softmax-CE, dz GEMM with
+    mask + bias-gradient column sums and the dX GEMM of layer L in one
+    tcgen05 kernel per 128 roots (k_umma_top); 96 roots in a 128-root
+    capacity also exercise the capacity rows.  Cases with more than 192
+    classes or L = 1 take the split kernels."""
+    test_step_matches_oracle(world, case, torch.bfloat16, fused_top=True)
 
 
 def test_forward_only_and_repeat_determinism(world):
