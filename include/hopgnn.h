@@ -363,6 +363,13 @@ typedef struct {
   const int32_t* labels;
 } hg_step_desc;
 
+/* Side-branch budget of the run-ahead loop (process-wide): resident CTAs per
+ * SM (1..3, default 3) of the grouped layer-1 gather (hg_step_prologue_group),
+ * which runs beside the training branch (fewer leave registers for the
+ * training kernels); agg_stream != 0 (default) reads the feature rows of
+ * every layer-1 gather with an L2 evict-first policy. */
+int hg_set_side_budget(int32_t agg_ctas_per_sm, int32_t agg_stream);
+
 /* Step variant (process-wide): 1 = softmax-CE fused into the tcgen05 head
  * GEMM's epilogue (C <= 192), 0 (default) = head GEMM + separate softmax-CE. */
 int hg_set_fused_head(int32_t on);
@@ -510,6 +517,22 @@ int hg_step_prologue_group(const hg_step_desc* const* descs, int32_t n, int32_t 
 int hg_train_step(const hg_step_desc* d, int32_t n_roots, void* stream);
 /* Forward only: fills logits (and agg/h).  Used by parity tests. */
 int hg_forward(const hg_step_desc* d, int32_t n_roots, void* stream);
+
+/* One training step followed (update != 0) by the SGD + bf16 operand refresh
+ * of hg_sgd_refresh -- the unit the training loops replay.  With the
+ * persistent step enabled (hg_set_persist) and an eligible descriptor
+ * (bf16 tensor-core path, L = 2, H a multiple of 64 up to 256, C <= 256,
+ * agg1_ready, lowp_fresh, n_roots == max_roots) the whole chain runs as ONE
+ * kernel launch (k_step_persist: grid-wide barriers between the GEMM, gather,
+ * softmax, scatter and SGD phases); otherwise hg_train_step then
+ * hg_sgd_refresh.  Same results up to the order of atomic reductions. */
+int hg_train_step_sgd(const hg_step_desc* d, int32_t n_roots, float* params, float* grads,
+                      int64_t n, float lr, float inv_batch, int32_t update, void* stream);
+
+/* Persistent-step switch (process-wide): on != 0 enables it; ctas = grid size
+ * (0 = one CTA per SM); split_w1 = split-K of the layer-1 weight gradient
+ * (0 = about one work item per CTA). */
+int hg_set_persist(int32_t on, int32_t ctas, int32_t split_w1);
 /* bf16 tcgen05 GEMM, fp32 accumulate: C[MxN] = A(m,k) B(k,n).
  * A K-major: [M x K] row-major, MN-major: [K x M];  B K-major: [N x K], MN-major: [K x N].
  * epi 0: C f32 store; 1: C bf16 = relu(acc + bias); 2: C f32 += acc (atomic, split-K).

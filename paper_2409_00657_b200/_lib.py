@@ -126,9 +126,13 @@ SIGNATURES = {
     "hg_mg_build_group_sharded": [C.POINTER(CsrShards), I64, V, I32, I32, V, V, I32,
                                   C.POINTER(MgLayout), V, C.POINTER(MgBatch), V, I32, V],
     "hg_set_fused_head": [I32],
+    "hg_set_side_budget": [I32, I32],
     "hg_set_fused_top": [I32],
     "hg_top_trace": [C.c_void_p],
     "hg_train_step": [C.POINTER(StepDesc), I32, V],
+    "hg_train_step_sgd": [C.POINTER(StepDesc), I32, V, V, I64, C.c_float, C.c_float, I32, V],
+    "hg_set_persist": [I32, I32, I32],
+    "hg_persist_trace": [C.c_void_p],
     "hg_forward": [C.POINTER(StepDesc), I32, V],
     "hg_sgd_update": [V, V, V, I64, C.c_float, C.c_float, V],
     "hg_sgd_refresh": [C.POINTER(StepDesc), V, V, I64, C.c_float, C.c_float, I32, V],

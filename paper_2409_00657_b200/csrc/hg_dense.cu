@@ -23,11 +23,10 @@
 #include <mutex>
 #include <cstdlib>
 
-#include "hg_common.cuh"
+#include "hg_step.cuh"
 
 namespace hg {
 
-using bf16 = __nv_bfloat16;
 
 template <typename T> __device__ __forceinline__ float to_f(T x);
 template <> __device__ __forceinline__ float to_f<float>(float x) { return x; }
@@ -90,6 +89,15 @@ __device__ __forceinline__ void store_vec(T* p, const float* v) {
   *reinterpret_cast<uint4*>(p) = raw;
 }
 
+// 16-byte read-only load with an L2 cache policy (createpolicy) and no L1 allocation
+__device__ __forceinline__ uint4 ld_evict_first(const void* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+
 // ------------------------------------------------------------------ aggregate
 //
 // One group of G = W/VEC lanes (<= 32) per destination row.  For layer 1 the
@@ -111,6 +119,7 @@ struct RowSrc {
   int rank;
   bool by_vid;                // index arrays hold vertex ids (layer 1 vid lists)
   const int32_t* handle;      // staged mode: need[0] row handles (hg_resolve_rows) or null
+  bool stream;                // source rows read once (feature table): L2 evict-first
   __device__ __forceinline__ const T* row(int i) const {
     if (by_vid) return vrow(i);
     if (handle) {
@@ -173,6 +182,8 @@ k_aggregate(RowSrc<T> rs_in, AggSegs<T> segs, int W, int out_ld, int pad_cap) {
   T* __restrict__ out = segs.out[blockIdx.y];
   constexpr int VEC = Vec<T>::N;
   constexpr int U = HG_AGG_U;
+  uint64_t pol = 0;
+  if (rs.stream) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   constexpr unsigned FULL = 0xffffffffu;
   if (pad_cap && blockIdx.x == gridDim.x - 1) {
     // the tensor-core dW GEMM reduces over rows up to the next multiple of 64:
@@ -232,7 +243,9 @@ k_aggregate(RowSrc<T> rs_in, AggSegs<T> segs, int W, int out_ld, int pad_cap) {
 #pragma unroll
           for (int t = 0; t < U; ++t) {
             const int v = __shfl_sync(FULL, ix, (gi * G + ((t0 + t) & (G - 1))) & 31);
-            if (act && t0 + t < cnt) x[t] = __ldg(reinterpret_cast<const uint4*>(rs.row(v) + col));
+            if (act && t0 + t < cnt)
+              x[t] = rs.stream ? ld_evict_first(rs.row(v) + col, pol)
+                               : __ldg(reinterpret_cast<const uint4*>(rs.row(v) + col));
             else x[t] = make_uint4(0, 0, 0, 0);
           }
 #pragma unroll
@@ -812,21 +825,6 @@ __global__ void k_zero_rows(float* __restrict__ x, const int32_t* __restrict__ n
 // straight bf16 copy coalesced along columns; the transposed copy staged in
 // shared memory so its writes are coalesced too), plus elementwise blocks for
 // the biases.  Replaces three transposes and a pad per step.
-struct SgdMat {
-  int64_t off;        // flat offset of the matrix [rows x cols] (row-major)
-  int rows, cols;
-  bf16* tdst;         // transposed bf16 copy [cols x rows] (ld tld) or null
-  int64_t tld;
-  bf16* sdst;         // straight bf16 copy [rows x cols] (ld sld) or null
-  int64_t sld;
-  int tiles_c, tile0; // column tiles; first tile index of this matrix
-};
-struct SgdPlan {
-  int n_mats, n_tiles;
-  SgdMat m[HG_MAX_LAYERS + 1];
-  int64_t plain_lo, plain_hi;  // elementwise range (the biases)
-};
-
 __global__ void __launch_bounds__(256)
 k_sgd_refresh(float* __restrict__ p, float* __restrict__ g, float lr, float inv_batch, int update,
               SgdPlan P) {
@@ -925,6 +923,11 @@ static void gemm(cudaStream_t s, const TA* A, int lda, const float* B, int ldb, 
 // Layer-k gather + aggregate (k == 1 reads features: local table, staged
 // remote rows or peer tables).  pad: zero the rows up to the next 64 for the
 // tensor-core weight-gradient reduction.
+// hg_set_side_budget: layer-1 feature rows are streamed with an L2
+// evict-first policy so the gather (the largest HBM stream of the loop) does
+// not evict the training chain's working set from L2
+static int g_agg_stream = 1;
+
 template <typename T>
 static RowSrc<T> row_src(const hg_step_desc* d, int k) {
   const T* src = k == 1 ? (const T*)d->features : (const T*)d->h[k - 1];
@@ -936,13 +939,18 @@ static RowSrc<T> row_src(const hg_step_desc* d, int k) {
   return RowSrc<T>{src, Wd, k == 1 ? d->mg.need_ids[0] : nullptr, k == 1 ? d->feat_row : nullptr,
                    k == 1 ? (const T* const*)d->feat_peers : nullptr, d->feat_home,
                    (const T*)d->stage_base, k == 1 ? d->stage_row : nullptr, d->rank, vid,
-                   hnd ? d->row_handle : nullptr};
+                   hnd ? d->row_handle : nullptr, k == 1 && g_agg_stream != 0};
 }
 
 // Layer-k gather + aggregate for n steps sharing one row source (k == 1
 // reads features: local table, staged remote rows or peer tables; n > 1 only
 // for layer 1 of run-ahead groups).  pad: zero the rows up to the next 64 for
 // the tensor-core weight-gradient reduction.
+// resident CTAs per SM of a grouped (run-ahead) layer-1 gather: it runs beside
+// the training branch, so it must leave registers for the training kernels
+// (hg_set_side_budget)
+static int g_agg_group_ctas = HG_AGG_MINB;
+
 template <typename T>
 static void launch_aggregate_n(const hg_step_desc* const* ds, int n, int k, cudaStream_t s,
                                bool pad) {
@@ -970,7 +978,7 @@ static void launch_aggregate_n(const hg_step_desc* const* ds, int n, int k, cuda
   // a group of segments: one resident wave split over them, warps loop over
   // their rows (the software pipeline pays off); one segment: a warp per
   // row group over the capacity (every row's chain in flight at once)
-  const int wave = n > 1 ? std::max(1, num_sms() * HG_AGG_MINB / n) : num_sms() * 32;
+  const int wave = n > 1 ? std::max(1, num_sms() * g_agg_group_ctas / n) : num_sms() * 32;
   dim3 grid(std::max(1, std::min((cap + rows_per_cta - 1) / rows_per_cta, wave)), n);
   const int pad_cap = pad && sizeof(T) == 2 ? d->max_rows[k] : 0;
   prof_begin(k == 1 ? PROF_AGG1 : PROF_AGG2, s);
@@ -1295,6 +1303,14 @@ extern "C" int hg_set_fused_top(int32_t on) {
   return HG_OK;
 }
 
+extern "C" int hg_set_side_budget(int32_t agg_ctas_per_sm, int32_t agg_stream) {
+  if (agg_ctas_per_sm < 1 || agg_ctas_per_sm > HG_AGG_MINB)
+    return hg_fail(HG_ECONFIG, "agg_ctas_per_sm must be 1..%d", HG_AGG_MINB);
+  g_agg_group_ctas = agg_ctas_per_sm;
+  g_agg_stream = agg_stream != 0;
+  return HG_OK;
+}
+
 extern "C" int hg_set_fused_head(int32_t on) {
   g_fused_head = on ? 1 : 0;
   return HG_OK;
@@ -1348,10 +1364,10 @@ extern "C" int hg_forward(const hg_step_desc* d, int32_t n_roots, void* stream) 
   return HG_OK;
 }
 
-extern "C" int hg_sgd_refresh(const hg_step_desc* d, float* params, float* grads, int64_t n,
-                              float lr, float inv_batch, int32_t update, void* stream) {
-  if (n <= 0) return HG_OK;
-  if (!d->WcT || !d->Wcp) return hg_fail(HG_ECONFIG, "hg_sgd_refresh needs the bf16 head operands");
+// The SGD + bf16-refresh plan of a step's parameters (flat buffer layout
+// W_1..W_L, b_1..b_L, W_c; model.py:299-324): one 32 x 32 tile list over the
+// weight matrices with the destinations of their bf16 operand copies.
+int hg::make_sgd_plan(const hg_step_desc* d, float* params, int64_t n, SgdPlan* out) {
   const int L = d->n_layers, H = d->hidden, C = d->n_classes, Cp = (C + 63) / 64 * 64;
   SgdPlan P{};
   int tiles = 0;
@@ -1381,7 +1397,18 @@ extern "C" int hg_sgd_refresh(const hg_step_desc* d, float* params, float* grads
   P.plain_hi = d->b[L] - params + H;
   if (P.plain_lo < 0 || P.plain_hi > n || P.plain_hi < P.plain_lo)
     return hg_fail(HG_ECONFIG, "biases outside the flat parameter buffer");
-  const int grid = tiles + 4;
+  *out = P;
+  return HG_OK;
+}
+
+extern "C" int hg_sgd_refresh(const hg_step_desc* d, float* params, float* grads, int64_t n,
+                              float lr, float inv_batch, int32_t update, void* stream) {
+  if (n <= 0) return HG_OK;
+  if (!d->WcT || !d->Wcp) return hg_fail(HG_ECONFIG, "hg_sgd_refresh needs the bf16 head operands");
+  SgdPlan P{};
+  int st = make_sgd_plan(d, params, n, &P);
+  if (st) return st;
+  const int grid = P.n_tiles + 4;
   count_launch();
   prof_begin(PROF_SGD, (cudaStream_t)stream);
   launch_pdl(k_sgd_refresh, dim3(grid), dim3(256), 0, (cudaStream_t)stream, params, grads, lr,

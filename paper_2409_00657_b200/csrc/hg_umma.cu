@@ -26,7 +26,7 @@
 #include <mutex>
 #include <unordered_map>
 
-#include "hg_common.cuh"
+#include "hg_tc.cuh"
 
 namespace hg {
 
@@ -38,133 +38,8 @@ namespace hg {
 #define HG_UMMA_STAGES_256 3
 #endif
 __host__ __device__ constexpr int stages_for(int bn) { return bn >= 256 ? HG_UMMA_STAGES_256 : 4; }
-constexpr int BM_T = 128;
-constexpr int BK_T = 64;  // one 128-byte swizzle row of bf16
 
 enum UEpi { UEPI_STORE_F32 = 0, UEPI_BIAS_RELU_BF16 = 1, UEPI_ATOMIC_F32 = 2, UEPI_SOFTMAX_CE = 3 };
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE_%=;\n"
-      "bra WAIT_%=;\n"
-      "DONE_%=:\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
-                                            int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
-
-// smem box -> global (plain store or f32 add-reduction in L2), bulk-group completion
-template <bool REDUCE>
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* smem_src, int c0,
-                                             int c1) {
-  if constexpr (REDUCE)
-    asm volatile(
-        "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];"
-        ::"l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
-        : "memory");
-  else
-    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                     reinterpret_cast<uint64_t>(map)),
-                 "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
-                 : "memory");
-}
-
-// UMMA shared-memory descriptor, 128B swizzle (sm_100 version 1).
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;  // version
-  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
-  return d;
-}
-
-// kind::f16 instruction descriptor: bf16 x bf16 -> f32, M = 128
-__host__ __device__ constexpr uint32_t make_idesc(int n, bool a_mn, bool b_mn) {
-  return (1u << 4)                       // D format f32
-         | (1u << 7)                     // A bf16
-         | (1u << 10)                    // B bf16
-         | ((a_mn ? 1u : 0u) << 15)      // A major
-         | ((b_mn ? 1u : 0u) << 16)      // B major
-         | ((uint32_t)(n >> 3) << 17)    // N >> 3
-         | ((uint32_t)(128 >> 4) << 24); // M >> 4
-}
-
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                          uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
-}
-
-// Issue a 16-column TMEM load without waiting; tmem_wait16 completes it and
-// ties the registers to the wait so no use is scheduled before it.
-__device__ __forceinline__ void tmem_ld16_issue(uint32_t taddr, uint32_t* r) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"
-      " [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_wait16(uint32_t* r) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;"
-               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]),
-                 "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]),
-                 "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
-               :
-               : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15},"
-      " [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
 
 struct UmmaArgs {
   int M, N, K;               // host-known sizes (M/K may be overridden on device)
@@ -496,8 +371,8 @@ static EncodeFn encoder() {
 }
 
 // 2D bf16 tensor map: inner dim (contiguous) x outer dim, row pitch in elements.
-static int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t pitch,
-                    uint32_t box_inner, uint32_t box_outer, int elem_bytes = 2) {
+int make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t pitch,
+                    uint32_t box_inner, uint32_t box_outer, int elem_bytes) {
   struct Key {
     const void* p; uint64_t a, b, c; uint32_t d, e; int f;
     bool operator==(const Key& o) const {
@@ -669,38 +544,9 @@ constexpr int kTopThreads = 64 + 32 * kTopEpiWarps;  // producer + MMA warps + e
 constexpr int kTopA = BM_T * BK_T * 2;         // 16 KB
 constexpr int kTopStage = kTopA + 256 * BK_T * 2;  // + 32 KB B tile
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 __device__ __forceinline__ void epi_sync() {  // the epilogue warps only
   asm volatile("bar.sync 1, %0;" ::"n"(32 * kTopEpiWarps) : "memory");
 }
-// byte offset of the 16-byte unit u (8 bf16 / 4 f32) of row r in a
-// 128-row x 128-byte K-major SW128 chunk (the TMA / UMMA layout)
-__device__ __forceinline__ int sw128(int r, int u) { return r * 128 + ((u ^ (r & 7)) << 4); }
-
-__device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
-  const __nv_bfloat162 t = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<const uint32_t*>(&t);
-}
-
-// Column sums of a 32-row x 16-column register block (lane = row): after the
-// butterfly, lane l holds the sum of column ((l>>4)&1)*8 + ((l>>3)&1)*4 +
-// ((l>>2)&1)*2 + ((l>>1)&1) (both lanes of each pair).
-__device__ __forceinline__ float colsum16(float (&v)[16], int lane) {
-#pragma unroll
-  for (int o = 16, n = 8; o >= 2; o >>= 1, n >>= 1) {
-    const bool hi = lane & o;
-#pragma unroll
-    for (int j = 0; j < n; ++j) {
-      const float keep = hi ? v[j + n] : v[j];
-      const float send = hi ? v[j] : v[j + n];
-      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-    }
-  }
-  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
-}
-
 __global__ void __launch_bounds__(kTopThreads, 1)
 k_umma_top(const __grid_constant__ CUtensorMap map_agg, const __grid_constant__ CUtensorMap map_w,
            const __grid_constant__ CUtensorMap map_wct, const __grid_constant__ CUtensorMap map_wcp,

@@ -143,8 +143,7 @@ class GraphLoop:
                 m = tr.model
                 if run.tc:  # SGD refreshes the bf16 operands: the step skips its transposes
                     run.desc.lowp_fresh = 1
-                    _lib.call("hg_train_step", C.byref(run.desc), B, cs)
-                    _lib.call("hg_sgd_refresh", C.byref(run.desc), m.flat.data_ptr(),
+                    _lib.call("hg_train_step_sgd", C.byref(run.desc), B, m.flat.data_ptr(),
                               m.grad.data_ptr(), m.flat.numel(), float(tr.lr), 1.0 / B, 1, cs)
                     run.desc.lowp_fresh = 0
                 else:
@@ -219,8 +218,7 @@ class GroupLoop:
                 for r in sets[x]:
                     if r.tc:  # SGD refreshes the bf16 operands: steps skip their transposes
                         r.desc.lowp_fresh = 1
-                        _lib.call("hg_train_step", C.byref(r.desc), B, cs)
-                        _lib.call("hg_sgd_refresh", C.byref(r.desc), m.flat.data_ptr(),
+                        _lib.call("hg_train_step_sgd", C.byref(r.desc), B, m.flat.data_ptr(),
                                   m.grad.data_ptr(), m.flat.numel(), float(tr.lr), 1.0 / B, 1, cs)
                         r.desc.lowp_fresh = 0
                     else:
@@ -286,8 +284,7 @@ class GroupLoop:
         for r in self.sets[0]:
             if r.tc:
                 r.desc.lowp_fresh = 1
-                _lib.call("hg_train_step", C.byref(r.desc), B, s)
-                _lib.call("hg_sgd_refresh", C.byref(r.desc), m.flat.data_ptr(),
+                _lib.call("hg_train_step_sgd", C.byref(r.desc), B, m.flat.data_ptr(),
                           m.grad.data_ptr(), m.flat.numel(), float(tr.lr), 1.0 / B, 1, s)
                 r.desc.lowp_fresh = 0
             else:

@@ -24,11 +24,16 @@ from paper_2409_00657_b200.rng import chain  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--build-ctas", type=int, default=engine.BUILD_CTAS_PER_SM)
+ap.add_argument("--agg-ctas", type=int, default=3, help="grouped gather CTAs/SM (hg_set_side_budget)")
 ap.add_argument("--reps", type=int, default=6)
+ap.add_argument("--stream", type=int, default=1, help="evict-first feature loads")
+ap.add_argument("--persist", type=int, default=0, help="persistent training step (hg_set_persist)")
 ap.add_argument("--no-build", action="store_true", help="training branch only")
 ap.add_argument("--no-train", action="store_true", help="side branch only")
 args = ap.parse_args()
 
+_lib.call("hg_set_side_budget", args.agg_ctas, args.stream)
+_lib.call("hg_set_persist", args.persist, 0, 0)
 cfg = CONFIGS["papers"]
 G = 10
 g = generate(GraphSpec(**{k: cfg[k] for k in ("n", "avg_deg", "beta", "p_in", "n_blocks",
@@ -72,9 +77,8 @@ for x in range(2):
         if not args.no_train:
             for i, r in enumerate(gl.sets[x]):
                 r.desc.lowp_fresh = 1
-                _lib.call("hg_train_step", C.byref(r.desc), B, cs)
-                _lib.call("hg_sgd_refresh", C.byref(r.desc), m.flat.data_ptr(), m.grad.data_ptr(),
-                          m.flat.numel(), float(tr.lr), 1.0 / B, 1, cs)
+                _lib.call("hg_train_step_sgd", C.byref(r.desc), B, m.flat.data_ptr(),
+                          m.grad.data_ptr(), m.flat.numel(), float(tr.lr), 1.0 / B, 1, cs)
                 r.desc.lowp_fresh = 0
                 stamp(x, 10 + i, cs)
         cap.wait_stream(gl.side)
@@ -100,5 +104,6 @@ for rep in range(args.reps):
         rec["train_steps_end_us"] = [us(10 + i) for i in range(G)]
     out.append(rec)
 tr.check()
-print(json.dumps({"build_ctas_per_sm": args.build_ctas, "no_build": args.no_build,
+mean = {k: round(float(np.mean([r[k] for r in out])), 1) for k in out[0] if k != "train_steps_end_us"}
+print(json.dumps({"build_ctas_per_sm": args.build_ctas, "agg_ctas": args.agg_ctas, "persist": args.persist, "stream": args.stream, "mean": mean, "no_build": args.no_build,
                   "no_train": args.no_train, "replays": out}))
