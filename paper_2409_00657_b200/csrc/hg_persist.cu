@@ -701,7 +701,8 @@ bool persist_eligible(const hg_step_desc* d, int n_roots) {
   const int Cp = (C + 63) / 64 * 64;
   return d->act_dtype == 1 && d->use_tc && d->n_layers == 2 && H % 64 == 0 && H >= 64 &&
          H <= 256 && d->in_dim[1] % 64 == 0 && d->in_dim[1] <= 1024 &&
-         d->in_dim[2] == (d->arch == 1 ? 2 * H : H) && C >= 1 && Cp <= 256 && d->WcT && d->Wcp &&
+         d->in_dim[2] == (d->arch == 1 ? 2 * H : H) && C >= 1 && C % 4 == 0 && Cp <= 256 &&
+         d->WcT && d->Wcp &&
          d->dl_lowp && d->Wb[2] && d->Wlp[1] && d->Wlp[2] && d->lowp_scratch && d->dagg &&
          d->agg1_ready && d->lowp_fresh && n_roots <= d->max_rows[2] && n_roots == d->max_roots;
 }
