@@ -244,7 +244,10 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     constexpr int CW = 128 / EB;             // columns per 128-byte row
     constexpr int NCH = (BN_T + CW - 1) / CW;
     uint8_t* stage = smem + warp * (NCH * 4096);
-    const bool warp_rows = m0 + warp * 32 < M;
+    // A warp whose 32 rows all lie past the device count still stores (zeros):
+    // the weight-gradient GEMMs reduce over rows up to the next multiple of 64
+    // and read those padding rows (a reduce-add of zeros would only cost time)
+    const bool warp_rows = EPI != UEPI_ATOMIC_F32 || m0 + warp * 32 < M;
 #pragma unroll 1
     for (int ch = 0; ch < NCH; ++ch) {
       const int c = ch * CW;

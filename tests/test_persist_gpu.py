@@ -92,18 +92,23 @@ def test_persistent_step_matches_split(world, case):
     assert torch.equal(h1a[:n1], h1b[:n1]) and torch.equal(h2a[:n2], h2b[:n2])
     assert torch.equal(dla, dlb)
     assert float(lb[n_real:].abs().max()) == 0.0
+    assert not torch.isnan(ga).any(), f"split-path gradients NaN at {torch.nonzero(torch.isnan(ga)).flatten()[:6].tolist()}"
+    assert not torch.isnan(gb).any(), f"persistent gradients NaN at {torch.nonzero(torch.isnan(gb)).flatten()[:6].tolist()} offsets {list(m.offsets)}"
     assert _rel(gb, ga) <= TOL, f"gradients {_rel(gb, ga):.3e}"
     _, _, pa, _, _, _ = step(0, 1)
     _, gz, pb, _, _, _ = step(1, 1)
-    assert _rel(pb - flat0, pa - flat0) <= TOL, "SGD updates differ"
+    # the update (lr * g / B) is ~1e-3 of the weights: its float32 difference
+    # carries the weights' rounding (one ulp of |w| ~ 1e-5 of the update)
+    assert _rel(pb - flat0, pa - flat0) <= 10 * TOL, "SGD updates differ"
+    assert _rel(pb, pa) <= 1e-6, "updated parameters differ"
     assert float(gz.abs().max()) == 0.0, "gradients not reset by the fused SGD"
     # bf16 operand copies refreshed by the fused SGD == hg_sgd_refresh of the same parameters
     lowp = [t.clone() for t in (run.wb16, run.wct, run.wcp)]
     _lib.call("hg_sgd_refresh", C.byref(run.desc), m.flat.data_ptr(), m.grad.data_ptr(),
               m.flat.numel(), 0.0, 1.0, 0, s)
     torch.cuda.synchronize()
-    for a, b in zip(lowp, (run.wb16, run.wct, run.wcp)):
-        assert torch.equal(a, b)
+    for a, b in zip(lowp, (run.wb16, run.wct, run.wcp)):  # bitwise (unused slots hold garbage)
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
 
 
 def test_persist_ineligible_falls_back_to_split(world):
