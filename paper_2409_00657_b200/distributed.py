@@ -1428,6 +1428,12 @@ class MicrographTrainer:
                           n, float(self.lr), inv, stream)
             return
         a = self._ar
+        if refresh:  # one launch: exchange + reduce + SGD + bf16 refresh (hg_p2p_allreduce_sgd)
+            _lib.call("hg_p2p_allreduce_sgd", C.byref(runner.desc), m.flat.data_ptr(),
+                      m.grad.data_ptr(), n, a["regions"].data_ptr(), self.rank, self.S,
+                      a["seq"].data_ptr(), a["ctr"].data_ptr(), a["err"].data_ptr(),
+                      float(self.lr), inv, stream)
+            return
         _lib.call("hg_p2p_allreduce", m.grad.data_ptr(), n, a["regions"].data_ptr(), self.rank,
                   self.S, a["seq"].data_ptr(), a["ctr"].data_ptr(), a["err"].data_ptr(), stream)
         if refresh:
