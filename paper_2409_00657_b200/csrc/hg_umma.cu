@@ -68,8 +68,14 @@ __device__ __forceinline__ void head_zero_row(const UmmaArgs& a, int row) {
   a.loss[row] = 0.f;
 }
 
+#ifndef HG_UMMA_THREADS
+#define HG_UMMA_THREADS 256
+#endif
+constexpr int kUmmaThreads = HG_UMMA_THREADS;  // 4 warps (roles + epilogue) or 8 (two epilogue warps per lane quadrant)
+constexpr int kEpiPerQ = kUmmaThreads / 128;
+
 template <bool A_MN, bool B_MN, int BN_T, int EPI>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(kUmmaThreads, 1)
 k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
             const __grid_constant__ CUtensorMap map_c, UmmaArgs args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -182,15 +188,16 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     }
     umma_commit(&done_bar);
   }
-  // ---------------- epilogue: all 4 warps, TMEM lane quadrant = warp
+  // ---------------- epilogue: TMEM lane quadrant wq = warp % 4; on the TMA path
+  // the kEpiPerQ warps of a quadrant take alternate column chunks, the other
+  // paths use warps 0-3
   __syncwarp();
+  const int wq = warp & 3, half = warp >> 2;
+  const bool epi_on = half == 0 || (EPI != UEPI_SOFTMAX_CE && args.tma_epi);
+  if (epi_on) {
   mbar_wait(&done_bar, 0);
   asm volatile("tcgen05.fence::after_thread_sync;");
-  const int row = m0 + warp * 32 + lane;
-#ifdef HG_UMMA_NOEPI  // timing experiment: main loop only
-  const bool valid = false;
-  if (false) {
-#else
+  const int row = m0 + wq * 32 + lane;
   const bool valid = row < M;
   if constexpr (EPI == UEPI_SOFTMAX_CE) {
     // one TMEM sweep (4 loads in flight, warp-uniform) copies each thread's
@@ -235,7 +242,6 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       }
     }
   } else if (args.tma_epi) {
-#endif
     // Coalesced epilogue: each warp stages its 32 rows x (128-byte column
     // chunk) in the now idle pipeline smem, 128B-swizzled, and one lane hands
     // the box to TMA (store, or f32 add-reduce in L2 for split-K partials).
@@ -243,22 +249,23 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     constexpr int EB = EPI == UEPI_BIAS_RELU_BF16 ? 2 : 4;
     constexpr int CW = 128 / EB;             // columns per 128-byte row
     constexpr int NCH = (BN_T + CW - 1) / CW;
-    uint8_t* stage = smem + warp * (NCH * 4096);
+    constexpr int NCW = (NCH + kEpiPerQ - 1) / kEpiPerQ;  // chunks per warp
+    uint8_t* stage = smem + warp * (NCW * 4096);
     // A warp whose 32 rows all lie past the device count still stores (zeros):
     // the weight-gradient GEMMs reduce over rows up to the next multiple of 64
     // and read those padding rows (a reduce-add of zeros would only cost time)
-    const bool warp_rows = EPI != UEPI_ATOMIC_F32 || m0 + warp * 32 < M;
+    const bool warp_rows = EPI != UEPI_ATOMIC_F32 || m0 + wq * 32 < M;
 #pragma unroll 1
-    for (int ch = 0; ch < NCH; ++ch) {
+    for (int ch = half; ch < NCH; ch += kEpiPerQ) {
       const int c = ch * CW;
       if (n0 + c >= args.N || !warp_rows) break;
       uint32_t rr[CW];
 #pragma unroll
       for (int q = 0; q < CW; q += 16)
-        tmem_ld16_issue(tmem + ((uint32_t)(warp * 32) << 16) + c + q, rr + q);
+        tmem_ld16_issue(tmem + ((uint32_t)(wq * 32) << 16) + c + q, rr + q);
 #pragma unroll
       for (int q = 0; q < CW; q += 16) tmem_wait16(rr + q);
-      uint8_t* box = stage + ch * 4096 + lane * 128;
+      uint8_t* box = stage + (ch / kEpiPerQ) * 4096 + lane * 128;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         uint4 v;
@@ -282,7 +289,7 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0)
-        tma_store_2d<EPI == UEPI_ATOMIC_F32>(&map_c, stage + ch * 4096, n0 + c, m0 + warp * 32);
+        tma_store_2d<EPI == UEPI_ATOMIC_F32>(&map_c, stage + (ch / kEpiPerQ) * 4096, n0 + c, m0 + wq * 32);
     }
     if (lane == 0) {
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -346,6 +353,7 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   }
   }
   }  // row-per-thread epilogue
+  }  // epi_on
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 2)
@@ -420,7 +428,7 @@ static int launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensor
   }
   dim3 grid((a.M + BM_T - 1) / BM_T, (a.N + BN_T - 1) / BN_T, split);
   count_launch();
-  HG_CUDA_TRY(launch_pdl(kern, grid, dim3(128), smem, s, ma, mb, mc, a));
+  HG_CUDA_TRY(launch_pdl(kern, grid, dim3(kUmmaThreads), smem, s, ma, mb, mc, a));
   return HG_OK;
 }
 
