@@ -111,14 +111,22 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
   }
   pdl_wait();
-  const int M = args.M_dev ? *args.M_dev : args.M;
+  // Forward GEMMs (device row count, host K): the row count only matters to
+  // the epilogue, so the mainloop starts without waiting for that dependent
+  // load -- every capacity tile runs (one wave), tiles past the count skip
+  // their stores.  Reductions (device K) need K before the first load.
+  constexpr bool kSoftmax = EPI == UEPI_SOFTMAX_CE;
+  const bool late_m = args.M_dev && !args.K_dev && !kSoftmax;
+  // issued now, first consumed in the epilogue when late_m
+  const int M_ld = args.M_dev ? __ldcg(args.M_dev) : args.M;
+  int M = late_m ? args.M : M_ld;
   const int K = args.K_dev ? *args.K_dev : args.K;
   // K range of this split, in 64-wide blocks
   const int kblocks = (K + BK_T - 1) / BK_T;
   const int per = (kblocks + gridDim.z - 1) / gridDim.z;
   const int kb0 = blockIdx.z * per;
   const int kb1 = min(kblocks, kb0 + per);
-  if (m0 >= M || kb0 >= kb1) {  // whole CTA exits together (before any TMEM is held)
+  if ((!late_m && m0 >= M) || kb0 >= kb1) {  // whole CTA exits together (before any TMEM is held)
     if constexpr (EPI == UEPI_SOFTMAX_CE)
       if (m0 >= M)
         for (int row = m0 + threadIdx.x; row < min(m0 + BM_T, args.n_cap); row += blockDim.x)
@@ -194,6 +202,7 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   __syncwarp();
   const int wq = warp & 3, half = warp >> 2;
   const bool epi_on = half == 0 || (EPI != UEPI_SOFTMAX_CE && args.tma_epi);
+  M = M_ld;
   if (epi_on) {
   mbar_wait(&done_bar, 0);
   asm volatile("tcgen05.fence::after_thread_sync;");
@@ -254,7 +263,7 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     // A warp whose 32 rows all lie past the device count still stores (zeros):
     // the weight-gradient GEMMs reduce over rows up to the next multiple of 64
     // and read those padding rows (a reduce-add of zeros would only cost time)
-    const bool warp_rows = EPI != UEPI_ATOMIC_F32 || m0 + wq * 32 < M;
+    const bool warp_rows = m0 < M && (EPI != UEPI_ATOMIC_F32 || m0 + wq * 32 < M);
 #pragma unroll 1
     for (int ch = half; ch < NCH; ch += kEpiPerQ) {
       const int c = ch * CW;
