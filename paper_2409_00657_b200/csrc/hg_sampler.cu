@@ -193,8 +193,10 @@ __device__ void team_select(const int32_t* __restrict__ targets, int64_t lo, int
                             int mean, uint64_t hv, int32_t* out, uint64_t* cand, int cap,
                             int* ctr, uint64_t* tsh, int* err) {
   const int lane = lane_id();
-  uint64_t gh = (uint64_t)mean >= (uint64_t)d ? (1ull << 32)
-                                              : (((uint64_t)mean << 32) / (uint64_t)d);
+  // threshold for ~mean survivors: any value keeps the draw exact (the count
+  // check below retries), so a float quotient replaces the 64-bit division
+  uint64_t gh = mean >= d ? (1ull << 32)
+                          : (uint64_t)__float2ull_rz(__fdividef((float)mean, (float)d) * 4294967296.0f);
   uint64_t lo_b = 0, hi_b = 1ull << 33;
   int m = 0;
   for (int attempt = 0;; ++attempt) {
@@ -211,15 +213,11 @@ __device__ void team_select(const int32_t* __restrict__ targets, int64_t lo, int
       unsigned mask[kU];
       int cw = 0;
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
+      for (int u = 0; u < kU; ++u) {  // branch-free: slots past d hash too, never taken
         const int j = base + u * 32 + lane;
-        take[u] = false;
-        key[u] = 0;
-        if (j < d) {
-          const uint64_t h = mix64(hv ^ (uint64_t)j);
-          take[u] = (h >> 32) < gh;
-          key[u] = (h & kHi32) | (uint64_t)j;
-        }
+        const uint64_t h = mix64(hv ^ (uint64_t)j);
+        take[u] = j < d && (h >> 32) < gh;
+        key[u] = (h & kHi32) | (uint64_t)(uint32_t)j;
         mask[u] = __ballot_sync(0xffffffffu, take[u]);
         cw += __popc(mask[u]);
       }
