@@ -54,6 +54,22 @@ __device__ __forceinline__ void load_vec(const T* p, float* v) {
   }
 }
 
+// 16 loaded bytes -> VEC floats
+template <typename T>
+__device__ __forceinline__ void unpack_vec(const uint4 raw, float* v) {
+  if constexpr (sizeof(T) == 4) {
+    v[0] = __uint_as_float(raw.x); v[1] = __uint_as_float(raw.y);
+    v[2] = __uint_as_float(raw.z); v[3] = __uint_as_float(raw.w);
+  } else {
+    const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[2 * i] = __uint_as_float(w[i] << 16);
+      v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+  }
+}
+
 // 16-byte vector from shared memory (TMA-staged rows)
 template <typename T>
 __device__ __forceinline__ void load_vec_s(const T* p, float* v) {
@@ -230,10 +246,11 @@ k_aggregate(RowSrc<T> rs_in, AggSegs<T> segs, int W, int out_ld, int pad_cap) {
       const int cv = c0 + gl;
       const bool act = row_ok && cv < nvec;
       const int col = cv * VEC;
-      float self[VEC], acc[VEC];
+      float acc[VEC];
 #pragma unroll
       for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
-      if (act) load_vec(sp + col, self);
+      // the self row stays packed (16 bytes) through the neighbour loop
+      const uint4 self_raw = act ? __ldg(reinterpret_cast<const uint4*>(sp + col)) : make_uint4(0, 0, 0, 0);
       for (int jb = 0; jb < max_deg; jb += G) {       // neighbour chunks of G indices
         const int ix = jb == 0 ? idx : (gl < deg - jb ? nbr_idx[j0 + jb + gl] : 0);
         const int cnt = min(G, deg - jb);              // this group's neighbours in the chunk
@@ -265,6 +282,8 @@ k_aggregate(RowSrc<T> rs_in, AggSegs<T> segs, int W, int out_ld, int pad_cap) {
         }
       }
       if (!act) continue;
+      float self[VEC];
+      unpack_vec<T>(self_raw, self);
       if constexpr (SAGE) {
         float nb[VEC];
         const float inv = deg > 0 ? 1.0f / (float)deg : 0.f;

@@ -33,7 +33,7 @@ namespace hg {
 #endif
 constexpr int kBuildThreads = HG_BUILD_THREADS;
 #ifndef HG_BUILD_MINB
-#define HG_BUILD_MINB 5  // resident build CTAs per SM (48 regs): leaves room for the training branch
+#define HG_BUILD_MINB 4  // resident build CTAs per SM (64 regs, no spills)
 #endif
 constexpr int kBuildWarps = kBuildThreads / 32;
 constexpr int kBigTask = 256;  // degree above which the whole CTA draws one vertex
