@@ -320,7 +320,7 @@ def sampler_roofline(runner, g, cfg, build_site, dev, group=1, sm_mhz=None):
                         "unit": "T warp-inst/s", "frac": round(ach / peak_issue, 4),
                         "warp_inst_per_batch": inst,
                         "source": "ncu smsp__inst_executed.sum of the grouped build "
-                                  "(profiles/r02_ncu_build_w2.md)"}
+                                  "(profiles/r02_ncu_build_src.md)"}
     return out
 
 

@@ -252,14 +252,34 @@ __device__ void team_select(const int32_t* __restrict__ targets, int64_t lo, int
     }
   }
   // T = fanout-th smallest candidate key
-  for (int i = Team::rank(); i < m; i += Team::size()) {
-    const uint64_t ki = cand[i];
-    int rank = 0;
-    for (int c = 0; c < m; ++c) rank += cand[c] < ki;
-    if (rank == fo - 1) *tsh = ki;
+  uint64_t T = 0;
+  bool have_t = false;
+  if (Team::size() == 32 && m <= 32) {
+    // one candidate per lane: rank on the 32-bit hash parts (one compare per
+    // candidate, shuffles instead of shared-memory loads) unless two hash
+    // parts are equal, where the slot decides (64-bit path below)
+    const uint64_t ki = lane < m ? cand[lane] : ~0ull;
+    const uint32_t hi = (uint32_t)(ki >> 32);
+    const unsigned valid = m >= 32 ? 0xffffffffu : ((1u << m) - 1u);
+    const unsigned same = __match_any_sync(0xffffffffu, hi) & valid;
+    if (!__any_sync(0xffffffffu, lane < m && __popc(same) > 1)) {
+      int rank = 0;
+      for (int c = 0; c < m; ++c) rank += __shfl_sync(0xffffffffu, hi, c) < hi;
+      const unsigned b = __ballot_sync(0xffffffffu, lane < m && rank == fo - 1);
+      T = __shfl_sync(0xffffffffu, ki, __ffs(b) - 1);
+      have_t = true;
+    }
   }
-  Team::sync();
-  const uint64_t T = *tsh;
+  if (!have_t) {
+    for (int i = Team::rank(); i < m; i += Team::size()) {
+      const uint64_t ki = cand[i];
+      int rank = 0;
+      for (int c = 0; c < m; ++c) rank += cand[c] < ki;
+      if (rank == fo - 1) *tsh = ki;
+    }
+    Team::sync();
+    T = *tsh;
+  }
   if (Team::size() == 32) {
     // one warp filled cand[] in ascending slot order (passes in slot order,
     // ballot positions lane-ordered): the selected keys' output positions are
