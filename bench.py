@@ -848,18 +848,12 @@ def main():
                          "over NVLink in the builds) or a full copy per GPU")
     ap.add_argument("--mode", default="fused", choices=["fused", "faithful"],
                     help="multi-GPU model-hop payload (see distributed.py)")
-    ap.add_argument("--update", default="fused", choices=["fused", "split"],
-                    help="multi-GPU p2p update: one launch (hg_p2p_allreduce_sgd) or "
-                         "push/wait/reduce + hg_sgd_refresh (A/B)")
     ap.add_argument("--agg-stream", type=int, default=1,
                     help="layer-1 feature rows with an L2 evict-first policy (A/B)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config], profile_key=args.config)
     from paper_2409_00657_b200 import _lib as _l
     _l.call("hg_set_side_budget", 3, int(args.agg_stream))
-    if args.update == "split":
-        from paper_2409_00657_b200 import distributed as _d
-        _d.FUSED_UPDATE = False
     if args.build_ctas > 0:
         from paper_2409_00657_b200 import engine
         engine.BUILD_CTAS_PER_SM = args.build_ctas

@@ -402,18 +402,6 @@ int hg_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
  * kernels: push this rank's accumulator into every peer's region + signal,
  * wait for every peer's signal, add the peers' slots. */
 int hg_p2p_region_bytes(int32_t n_ranks, int64_t n, int64_t* bytes);
-
-/* Fused all-reduce + synchronous update over the same exchange regions: the
- * gradients of every rank summed (hg_p2p_allreduce's order), then SGD with
- * inv_batch, gradient reset and the bf16 operand copies (hg_sgd_refresh) --
- * one launch.  Work units are hg_sgd_refresh's 32 x 32 weight tiles and
- * 256-element bias chunks; CTA b exchanges its units with CTA b of every
- * peer through per-CTA flags (no grid-wide wait).  n_ranks == 1 is
- * hg_sgd_refresh. */
-int hg_p2p_allreduce_sgd(const hg_step_desc* d, float* params, float* grads, int64_t n,
-                         const uint64_t* regions, int32_t rank, int32_t n_ranks, int64_t* seq,
-                         unsigned int* counter, int* err, float lr, float inv_batch,
-                         void* stream);
 int hg_p2p_allreduce(float* grads, int64_t n, const uint64_t* regions, int32_t rank,
                      int32_t n_ranks, int64_t* seq, unsigned int* counter, int* err, void* stream);
 

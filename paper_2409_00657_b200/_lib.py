@@ -144,8 +144,6 @@ SIGNATURES = {
     "hg_remote_account_group": [V, V, I32, V, I32, V, I64, V, V, I32, V, V],
     "hg_resolve_rows_group": [V, V, I32, V, I32, V, V, V, V],
     "hg_p2p_region_bytes": [I32, I64, PI64],
-    "hg_p2p_allreduce_sgd": [C.POINTER(StepDesc), V, V, I64, V, I32, I32, V, V, V, C.c_float,
-                             C.c_float, V],
     "hg_p2p_allreduce": [V, I64, V, I32, I32, V, V, V, V],
     "hg_free": [V],
     "hg_ipc_handle": [V, V],

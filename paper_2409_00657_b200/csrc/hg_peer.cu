@@ -13,7 +13,6 @@
 #include <algorithm>
 
 #include "hg_common.cuh"
-#include "hg_step.cuh"
 
 namespace hg {
 
@@ -685,19 +684,10 @@ namespace hg {
 // Double buffering by seq parity is safe: a rank reuses buffer (s & 1) for
 // s + 2 only after every peer published s + 1, which each peer does after its
 // reduce of s (stream order).  Region layout: [S int64 flags | pad to 256 |
-// 2 x S x n floats] -- plus, for the fused all-reduce + SGD (k_ar_sgd), S x
-// kArCtas per-CTA flags between the rank flags and the buffers.
+// 2 x S x n floats].
 struct ArRegion {
   int64_t o_flags, o_buf;
-  int64_t o_cta;  // per-CTA flags [S][kArCtas] int64
 };
-constexpr int kArCtas = 256;
-
-static ArRegion ar_layout(int S) {
-  const int64_t f = ((int64_t)S * 8 + 255) / 256 * 256;
-  const int64_t c = ((int64_t)S * kArCtas * 8 + 255) / 256 * 256;
-  return ArRegion{0, f + c, f};
-}
 
 __device__ __forceinline__ float* ar_slot(uint8_t* region, ArRegion r, int parity, int S, int p,
                                           int64_t n) {
@@ -765,145 +755,13 @@ k_ar_reduce(float* __restrict__ g, int64_t n, const uint64_t* __restrict__ regio
   }
 }
 
-// Fused all-reduce + synchronous update (one launch instead of push, wait,
-// reduce and hg_sgd_refresh): the work units are hg_sgd_refresh's 32 x 32
-// weight tiles plus 256-element bias chunks, dealt out round-robin over the
-// CTAs -- the same on every rank.  CTA b pushes its units' gradients into
-// slot [rank] of every peer, publishes per-CTA flag [rank][b] = seq in every
-// peer, waits for flag [p][b] of every peer (bounded), then reduces its units
-// (own + peers' slots, the k_ar_reduce order) and applies SGD + gradient reset
-// + bf16 operand copies (k_sgd_refresh's arithmetic).  No CTA waits on
-// another CTA of its own grid; a rank reuses a buffer parity only after every
-// peer's grid of the previous sequence number has finished (stream order), as
-// in the three-kernel protocol.
-__device__ __forceinline__ int64_t ar_unit_elem(const SgdPlan& P, int u, int j, int* mi_out) {
-  // element j (0..1023) of tile unit u: flat index or -1 (outside the matrix)
-  int mi = 0;
-  while (mi + 1 < P.n_mats && P.m[mi + 1].tile0 <= u) ++mi;
-  *mi_out = mi;
-  const SgdMat& M = P.m[mi];
-  const int lt = u - M.tile0, tr = lt / M.tiles_c, tc = lt % M.tiles_c;
-  const int r = tr * 32 + (j >> 5), c = tc * 32 + (j & 31);
-  return (r < M.rows && c < M.cols) ? M.off + (int64_t)r * M.cols + c : -1;
-}
-
-__global__ void __launch_bounds__(256)
-k_ar_sgd(float* __restrict__ p, float* __restrict__ g, int64_t n, const uint64_t* __restrict__ regions,
-         int rank, int S, ArRegion r, int64_t* seq, unsigned int* counter, int* err, float lr,
-         float inv_batch, SgdPlan P) {
-  __shared__ bf16 tile[32][34];
-  const int64_t s = *seq + 1;
-  const int par = (int)(s & 1);
-  const int n_bias_units = (int)((P.plain_hi - P.plain_lo + 255) / 256);
-  const int U = P.n_tiles + n_bias_units;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  // ---- push this CTA's units to every peer
-  for (int u = blockIdx.x; u < U; u += gridDim.x) {
-    if (u < P.n_tiles) {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        int mi;
-        const int64_t i = ar_unit_elem(P, u, (ty + 8 * k) * 32 + tx, &mi);
-        if (i < 0) continue;
-        const float v = g[i];
-        for (int q = 0; q < S; ++q)
-          if (q != rank) ar_slot(reinterpret_cast<uint8_t*>(regions[q]), r, par, S, rank, n)[i] = v;
-      }
-    } else {
-      const int64_t i = P.plain_lo + (int64_t)(u - P.n_tiles) * 256 + threadIdx.x;
-      if (i < P.plain_hi) {
-        const float v = g[i];
-        for (int q = 0; q < S; ++q)
-          if (q != rank) ar_slot(reinterpret_cast<uint8_t*>(regions[q]), r, par, S, rank, n)[i] = v;
-      }
-    }
-  }
-  __threadfence_system();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int q = 0; q < S; ++q) {
-      if (q == rank) continue;
-      volatile int64_t* f = reinterpret_cast<volatile int64_t*>(
-          reinterpret_cast<uint8_t*>(regions[q]) + r.o_cta);
-      f[rank * kArCtas + blockIdx.x] = s;
-    }
-    __threadfence_system();
-    // ---- wait for every peer's CTA blockIdx.x
-    volatile int64_t* mine = reinterpret_cast<volatile int64_t*>(
-        reinterpret_cast<uint8_t*>(regions[rank]) + r.o_cta);
-    bool ok = false;
-    for (long long it = 0; it < (1ll << 26) && !ok; ++it) {
-      ok = true;
-      for (int q = 0; q < S; ++q)
-        if (q != rank && mine[q * kArCtas + blockIdx.x] < s) ok = false;
-      if (!ok) __nanosleep(32);
-    }
-    if (!ok) raise_flag(err, HG_EINVARIANT);
-    __threadfence_system();
-  }
-  __syncthreads();
-  // ---- reduce + SGD + bf16 copies
-  uint8_t* mreg = reinterpret_cast<uint8_t*>(regions[rank]);
-  for (int u = blockIdx.x; u < U; u += gridDim.x) {
-    if (u < P.n_tiles) {
-      int mi = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int64_t i = ar_unit_elem(P, u, (ty + 8 * k) * 32 + tx, &mi);
-        if (i < 0) continue;
-        float gs = g[i];
-        for (int q = 0; q < S; ++q)
-          if (q != rank) gs += ar_slot(mreg, r, par, S, q, n)[i];
-        const float v = p[i] - lr * (gs * inv_batch);
-        p[i] = v;
-        g[i] = 0.f;
-        const SgdMat& M = P.m[mi];
-        const int lt = u - M.tile0, tr = lt / M.tiles_c, tc = lt % M.tiles_c;
-        const int rr = tr * 32 + ty + 8 * k, cc = tc * 32 + tx;
-        const bf16 b = __float2bfloat16_rn(v);
-        if (M.sdst) M.sdst[(int64_t)rr * M.sld + cc] = b;
-        tile[ty + 8 * k][tx] = b;
-      }
-      const SgdMat& M = P.m[mi];
-      __syncthreads();
-      if (M.tdst) {
-        const int lt = u - M.tile0, tr = lt / M.tiles_c, tc = lt % M.tiles_c;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int c = tc * 32 + ty + 8 * k, rr = tr * 32 + tx;
-          if (rr < M.rows && c < M.cols) M.tdst[(int64_t)c * M.tld + rr] = tile[tx][ty + 8 * k];
-        }
-      }
-      __syncthreads();
-    } else {
-      const int64_t i = P.plain_lo + (int64_t)(u - P.n_tiles) * 256 + threadIdx.x;
-      if (i < P.plain_hi) {
-        float gs = g[i];
-        for (int q = 0; q < S; ++q)
-          if (q != rank) gs += ar_slot(mreg, r, par, S, q, n)[i];
-        p[i] -= lr * (gs * inv_batch);
-        g[i] = 0.f;
-      }
-    }
-  }
-  // the last CTA out publishes the new sequence number (every CTA read s first)
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(counter, 1u) == gridDim.x - 1) {
-      *counter = 0u;
-      *seq = s;
-      __threadfence();
-    }
-  }
-}
-
 }  // namespace hg
 
 using namespace hg;
 
 extern "C" int hg_p2p_region_bytes(int32_t n_ranks, int64_t n, int64_t* bytes) {
-  *bytes = ar_layout(n_ranks).o_buf + 2ll * n_ranks * n * 4;
+  const int64_t flags = ((int64_t)n_ranks * 8 + 255) / 256 * 256;
+  *bytes = flags + 2ll * n_ranks * n * 4;
   return HG_OK;
 }
 
@@ -913,7 +771,7 @@ extern "C" int hg_p2p_allreduce(float* grads, int64_t n, const uint64_t* regions
   if (n_ranks < 1 || rank < 0 || rank >= n_ranks) return hg_fail(HG_ERANGE, "bad rank");
   if (n_ranks == 1 || n <= 0) return HG_OK;
   cudaStream_t s = (cudaStream_t)stream;
-  const ArRegion r = ar_layout(n_ranks);
+  ArRegion r{0, ((int64_t)n_ranks * 8 + 255) / 256 * 256};
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -924,31 +782,6 @@ extern "C" int hg_p2p_allreduce(float* grads, int64_t n, const uint64_t* regions
   k_ar_wait<<<1, 32, 0, s>>>(regions, rank, n_ranks, r, seq, err);
   HG_CUDA_TRY(cudaGetLastError());
   k_ar_reduce<<<grid, 256, 0, s>>>(grads, n, regions, rank, n_ranks, r, seq);
-  HG_CUDA_TRY(cudaGetLastError());
-  return HG_OK;
-}
-
-extern "C" int hg_p2p_allreduce_sgd(const hg_step_desc* d, float* params, float* grads, int64_t n,
-                                    const uint64_t* regions, int32_t rank, int32_t n_ranks,
-                                    int64_t* seq, unsigned int* counter, int* err, float lr,
-                                    float inv_batch, void* stream) {
-  if (n_ranks < 1 || rank < 0 || rank >= n_ranks) return hg_fail(HG_ERANGE, "bad rank");
-  if (n <= 0) return HG_OK;
-  if (n_ranks == 1) return hg_sgd_refresh(d, params, grads, n, lr, inv_batch, 1, stream);
-  SgdPlan P{};
-  int st = make_sgd_plan(d, params, n, &P);
-  if (st) return st;
-  const int U = P.n_tiles + (int)((P.plain_hi - P.plain_lo + 255) / 256);
-  int dev = 0, nsm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = std::max(1, std::min({U, nsm, kArCtas}));
-  count_launch();
-  prof_begin(PROF_SGD, (cudaStream_t)stream);
-  k_ar_sgd<<<grid, 256, 0, (cudaStream_t)stream>>>(params, grads, n, regions, rank, n_ranks,
-                                                   ar_layout(n_ranks), seq, counter, err, lr,
-                                                   inv_batch, P);
-  prof_end(PROF_SGD, (cudaStream_t)stream);
   HG_CUDA_TRY(cudaGetLastError());
   return HG_OK;
 }

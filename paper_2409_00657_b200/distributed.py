@@ -439,9 +439,6 @@ _DIST_PRIO = os.environ.get("HG_DIST_PRIO", "1") != "0"
 _ROW_HANDLES = os.environ.get("HG_ROW_HANDLES", "1") != "0"
 # DistGroupLoop: one deduplicated push per group (per-iteration ledger rows)
 _GROUP_PUSH = os.environ.get("HG_GROUP_PUSH", "1") != "0"
-# p2p synchronous update: one launch (hg_p2p_allreduce_sgd) or push / wait /
-# reduce + hg_sgd_refresh (bench.py --update split)
-FUSED_UPDATE = True
 _GROUP_GATHER = os.environ.get("HG_GROUP_GATHER", "1") != "0"
 
 
@@ -1431,12 +1428,6 @@ class MicrographTrainer:
                           n, float(self.lr), inv, stream)
             return
         a = self._ar
-        if refresh and FUSED_UPDATE:  # one launch: exchange + reduce + SGD + bf16 refresh
-            _lib.call("hg_p2p_allreduce_sgd", C.byref(runner.desc), m.flat.data_ptr(),
-                      m.grad.data_ptr(), n, a["regions"].data_ptr(), self.rank, self.S,
-                      a["seq"].data_ptr(), a["ctr"].data_ptr(), a["err"].data_ptr(),
-                      float(self.lr), inv, stream)
-            return
         _lib.call("hg_p2p_allreduce", m.grad.data_ptr(), n, a["regions"].data_ptr(), self.rank,
                   self.S, a["seq"].data_ptr(), a["ctr"].data_ptr(), a["err"].data_ptr(), stream)
         if refresh:

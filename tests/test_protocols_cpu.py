@@ -136,64 +136,3 @@ def test_p2p_allreduce_double_buffer_world8():
     for t in ts:
         t.join()
     assert not errors, errors[0]
-
-
-def test_p2p_allreduce_sgd_per_cta_flags_world8():
-    """hg_p2p_allreduce_sgd (k_ar_sgd): CTA b of every rank exchanges only its
-    own units through per-CTA flags [sender][b]; a rank's next launch starts
-    only after all its CTAs finished (stream order).  Invariant: every unit's
-    sum is the true sum at every step, with two buffers and no grid-wide wait."""
-    steps, n_cta, units = 25, 4, 10
-    n = units * 8
-    bufs = np.zeros((S, 2, S, n))                       # receiver x parity x sender x n
-    flags = np.zeros((S, S, n_cta), dtype=np.int64)     # [receiver][sender][cta]
-    seqs = [0] * S
-    errors = []
-
-    def grad(r, s):
-        return np.random.default_rng(r * 1000 + s).standard_normal(n)
-
-    def cta(r, b, s, g, rng):
-        try:
-            par = s & 1
-            mine = [u for u in range(b, units, n_cta)]
-            for u in mine:                              # push this CTA's units
-                for p in range(S):
-                    if p != r:
-                        bufs[p, par, r, u * 8:(u + 1) * 8] = g[u * 8:(u + 1) * 8]
-                        _jitter(rng)
-            for p in range(S):                          # per-CTA flags
-                if p != r:
-                    flags[p][r][b] = s
-            _wait(lambda: all(flags[r][p][b] >= s for p in range(S) if p != r), "cta grads")
-            want = sum(grad(q, s) for q in range(S))
-            for u in mine:
-                sl = slice(u * 8, (u + 1) * 8)
-                total = g[sl] + sum(bufs[r, par, p, sl] for p in range(S) if p != r)
-                if not np.allclose(total, want[sl]):
-                    raise AssertionError(f"rank {r} cta {b} step {s}: wrong sum")
-                _jitter(rng)
-        except Exception as e:  # noqa: BLE001
-            errors.append(e)
-
-    def rank_main(r):
-        rng = random.Random(r)
-        for step in range(1, steps + 1):
-            s = seqs[r] + 1
-            g = grad(r, step)
-            ts = [threading.Thread(target=cta, args=(r, b, s, g, random.Random(rng.random())))
-                  for b in range(n_cta)]
-            for t in ts:
-                t.start()
-            for t in ts:                                # the launch completes
-                t.join()
-            seqs[r] = s
-            if errors:
-                return
-
-    ts = [threading.Thread(target=rank_main, args=(r,)) for r in range(S)]
-    for t in ts:
-        t.start()
-    for t in ts:
-        t.join()
-    assert not errors, errors[0]
