@@ -58,6 +58,7 @@ struct UmmaArgs {
   __nv_bfloat16* dl_lowp;
   int ldp;                   // dl_lowp row pitch (classes rounded up to 64)
   int n_cap;                 // capacity rows: [M_dev, n_cap) get zeros
+  int late_m;                // host: every capacity tile fits one wave, M_dev read late
 };
 
 // Rows [r0, r1) of the head outputs past the device root count: no loss, no gradient.
@@ -116,7 +117,7 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
   // load -- every capacity tile runs (one wave), tiles past the count skip
   // their stores.  Reductions (device K) need K before the first load.
   constexpr bool kSoftmax = EPI == UEPI_SOFTMAX_CE;
-  const bool late_m = args.M_dev && !args.K_dev && !kSoftmax;
+  const bool late_m = args.late_m && args.M_dev && !args.K_dev && !kSoftmax;
   // issued now, first consumed in the epilogue when late_m
   const int M_ld = args.M_dev ? __ldcg(args.M_dev) : args.M;
   int M = late_m ? args.M : M_ld;
@@ -480,6 +481,19 @@ int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
   }
   if (!tma_epi) memset(&mc, 0, sizeof(mc));
   UmmaArgs a{M, N, K, M_dev, K_dev, C, ldc, bias, tma_epi};
+  {
+    // late row count only while every capacity tile fits one wave: tiles past
+    // the count then run on otherwise idle SMs; beyond a wave they would queue
+    // (multi-GPU capacities hold several batches' rows)
+    static int sms_ = [] {
+      int dev = 0, n = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+      return n > 0 ? n : 148;
+    }();
+    const int64_t ctas = (int64_t)((M + BM_T - 1) / BM_T) * ((N + bn - 1) / bn) * std::max(split, 1);
+    a.late_m = ctas <= sms_ ? 1 : 0;
+  }
 
 #define HG_UMMA_CASE(AM, BMJ, BNV, E)                                                       \
   if (a_mn == AM && b_mn == BMJ && bn == BNV && epi == E)                                   \
