@@ -316,28 +316,51 @@ __global__ void k_pg_wait(const uint64_t* __restrict__ boxes, int rank, int S, M
   if (threadIdx.x == 0 && !spin_peers(boxes, rank, S, off, *seq)) raise_flag(err, HG_EINVARIANT);
 }
 
-// owner side: serve every peer's requests homed here.  Half-warp per row.
+// owner side: serve every peer's requests homed here.  A warp reads 32 list
+// entries of the requester's mailbox in one coalesced NVLink load (the list
+// lives in the REQUESTER's memory; one dependent remote read per entry was
+// the serve's latency chain), looks their homes up locally, then copies the
+// rows homed here two at a time (half a warp per 256-byte row) into the
+// requester's staging rows.
 __global__ void __launch_bounds__(256)
 k_pg_serve(const uint64_t* __restrict__ boxes, int rank, int S, Mailbox m, const int64_t* seq,
            const int32_t* __restrict__ home, const int32_t* __restrict__ local_row,
            const uint8_t* __restrict__ shard, int row_bytes, int stage_cap, int* err) {
   // the requests are ready: k_pg_wait (one CTA) polled the peers' signals, so
   // these CTAs never occupy SM slots while spinning
+  const unsigned full = 0xffffffffu;
   const int vec = row_bytes / 16;
-  const int hw = (blockIdx.x * blockDim.x + threadIdx.x) / 16, hl = threadIdx.x & 15;
-  const int n_hw = gridDim.x * blockDim.x / 16;
+  const int lane = threadIdx.x & 31, hl = lane & 15;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int n_w = (gridDim.x * blockDim.x) >> 5;
   for (int p = 0; p < S; ++p) {
     if (p == rank) continue;
     uint8_t* box = mb_base(boxes, p);
     const int n = min(*reinterpret_cast<volatile int32_t*>(box + m.o_count), stage_cap);
     const int32_t* list = reinterpret_cast<const int32_t*>(box + m.o_list);
     uint8_t* staging = box + m.o_staging;
-    for (int i = hw; i < n; i += n_hw) {
-      const int v = list[i];
-      if (home[v] != rank) continue;
-      const uint4* src = reinterpret_cast<const uint4*>(shard + (int64_t)local_row[v] * row_bytes);
-      uint4* dst = reinterpret_cast<uint4*>(staging + (int64_t)i * row_bytes);
-      for (int c = hl; c < vec; c += 16) dst[c] = src[c];
+    for (int base = w * 32; base < n; base += n_w * 32) {
+      const int i = base + lane;
+      const int v = i < n ? list[i] : -1;
+      const bool mine = v >= 0 && home[v] == rank;
+      const int r = mine ? local_row[v] : 0;
+      unsigned todo = __ballot_sync(full, mine);
+      while (todo) {  // warp-uniform: two rows per round, one per half-warp
+        const int j0 = __ffs(todo) - 1;
+        todo &= todo - 1;
+        int j1 = -1;
+        if (todo) {
+          j1 = __ffs(todo) - 1;
+          todo &= todo - 1;
+        }
+        const int j = lane < 16 ? j0 : j1;
+        const int rr = __shfl_sync(full, r, j < 0 ? 0 : j);
+        if (j >= 0) {
+          const uint4* src = reinterpret_cast<const uint4*>(shard + (int64_t)rr * row_bytes);
+          uint4* dst = reinterpret_cast<uint4*>(staging + (int64_t)(base + j) * row_bytes);
+          for (int c = hl; c < vec; c += 16) dst[c] = src[c];
+        }
+      }
     }
   }
   __threadfence_system();  // rows land before the "done" signal of the next kernel
