@@ -27,6 +27,8 @@ ap.add_argument("--build-ctas", type=int, default=engine.BUILD_CTAS_PER_SM)
 ap.add_argument("--agg-ctas", type=int, default=3, help="grouped gather CTAs/SM (hg_set_side_budget)")
 ap.add_argument("--reps", type=int, default=6)
 ap.add_argument("--stream", type=int, default=1, help="evict-first feature loads")
+ap.add_argument("--inline-gather", action="store_true",
+                help="layer-1 gather of each step on the training stream (not the side branch)")
 ap.add_argument("--persist", type=int, default=0, help="persistent training step (hg_set_persist)")
 ap.add_argument("--no-build", action="store_true", help="training branch only")
 ap.add_argument("--no-train", action="store_true", help="side branch only")
@@ -72,10 +74,13 @@ for x in range(2):
                 stamp(x, 1, ss)
                 nxt.build(tr.graph, stream=ss, ctas_per_sm=args.build_ctas)
                 stamp(x, 2, ss)
-                _lib.call("hg_step_prologue_group", gl.descp[1 - x], G, 1, ss)
+                if not args.inline_gather:
+                    _lib.call("hg_step_prologue_group", gl.descp[1 - x], G, 1, ss)
                 stamp(x, 3, ss)
         if not args.no_train:
             for i, r in enumerate(gl.sets[x]):
+                if args.inline_gather:  # this step's layer-1 gather on the training stream
+                    _lib.call("hg_step_prologue", C.byref(r.desc), B, 1, cs)
                 r.desc.lowp_fresh = 1
                 _lib.call("hg_train_step_sgd", C.byref(r.desc), B, m.flat.data_ptr(),
                           m.grad.data_ptr(), m.flat.numel(), float(tr.lr), 1.0 / B, 1, cs)
@@ -105,5 +110,5 @@ for rep in range(args.reps):
     out.append(rec)
 tr.check()
 mean = {k: round(float(np.mean([r[k] for r in out])), 1) for k in out[0] if k != "train_steps_end_us"}
-print(json.dumps({"build_ctas_per_sm": args.build_ctas, "agg_ctas": args.agg_ctas, "persist": args.persist, "stream": args.stream, "mean": mean, "no_build": args.no_build,
+print(json.dumps({"build_ctas_per_sm": args.build_ctas, "agg_ctas": args.agg_ctas, "persist": args.persist, "stream": args.stream, "inline_gather": args.inline_gather, "mean": mean, "no_build": args.no_build,
                   "no_train": args.no_train, "replays": out}))
