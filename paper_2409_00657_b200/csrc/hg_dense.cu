@@ -910,6 +910,9 @@ __global__ void k_sgd(float* __restrict__ p, float* __restrict__ g, bf16* __rest
 int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb, bool b_mn,
               void* C, int64_t ldc, int M, int N, int K, const int32_t* M_dev,
               const int32_t* K_dev, int epi, const float* bias, int split, cudaStream_t s);
+int umma_gemm_mask(const void* A, int64_t lda, const void* B, int64_t ldb, __nv_bfloat16* C,
+                   int64_t ldc, int M, int N, int K, const int32_t* M_dev,
+                   const __nv_bfloat16* mask, int ldm, float* colsum, cudaStream_t s);
 int umma_top(const void* agg, const void* WlT, const void* Wb, const float* bias, const void* WcT,
              const void* Wcp, void* h, void* dl, void* dz, float* dagg, int cap, int H, int C,
              int inL, const int32_t* M_dev, const int64_t* roots, uint64_t label_state,
@@ -1176,14 +1179,26 @@ static int run_step(const hg_step_desc* d, int n_roots, cudaStream_t s, bool bac
                                                    (bf16*)d->dl_lowp, Cp);
     }
     if (backward) {
-      // dz_L = (dlogits @ W_cᵀ) * (h_L > 0); gb_L; bf16 dz_L for the dW GEMM
-      st = umma_gemm(d->dl_lowp, Cp, false, d->Wcp, Cp, false, d->dh[L], H, n_roots, H, Cp,
-                     tot + L, nullptr, 0, nullptr, 1, s);
-      if (st) { join(); return st; }
-      dim3 g((H + 31) / 32, 16);
-      count_launch();
-      launch_pdl(k_mask_colsum<T>, dim3(g), dim3(256), 0, s, d->dh[L], (const T*)d->h[L], tot + L, H, d->gb[L],
-                                         dz_lowp(d, L), d->max_rows[L]);
+      // dz_L = bf16((dlogits @ W_cᵀ) * (h_L > 0)) and gb_L += its column sums, in
+      // the dz GEMM's epilogue (no f32 dh_L round trip, no k_mask_colsum); the
+      // rows past the root count come out zero for the dW GEMM's reduction
+      // (the f32 dh_L is still produced where a SIMT dX GEMM of layer L would read it)
+      if (L == 1 || (d->in_dim[L] % 64 == 0 && d->Wb[L])) {
+        // rows up to the next multiple of 64 (within the capacity): the dW GEMM's
+        // reduction reads them, so they are stored (as zeros past the root count)
+        const int mrows = std::min(d->max_rows[L], (n_roots + 63) / 64 * 64);
+        st = umma_gemm_mask(d->dl_lowp, Cp, d->Wcp, Cp, dz_lowp(d, L), H, mrows, H, Cp, tot + L,
+                            (const bf16*)d->h[L], H, d->gb[L], s);
+        if (st) { join(); return st; }
+      } else {
+        st = umma_gemm(d->dl_lowp, Cp, false, d->Wcp, Cp, false, d->dh[L], H, n_roots, H, Cp,
+                       tot + L, nullptr, 0, nullptr, 1, s);
+        if (st) { join(); return st; }
+        dim3 g((H + 31) / 32, 16);
+        count_launch();
+        launch_pdl(k_mask_colsum<T>, dim3(g), dim3(256), 0, s, d->dh[L], (const T*)d->h[L], tot + L,
+                   H, d->gb[L], dz_lowp(d, L), d->max_rows[L]);
+      }
       // gW_c += h_Lᵀ dlogits (both MN-major, reduction over the roots), forked
       const int split = std::max(1, std::min(16, n_roots / 256));
       st = umma_gemm(d->h[L], H, true, d->dl_lowp, Cp, true, d->gWc, C, H, C, n_roots,

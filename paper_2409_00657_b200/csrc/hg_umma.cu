@@ -39,7 +39,8 @@ namespace hg {
 #endif
 __host__ __device__ constexpr int stages_for(int bn) { return bn >= 256 ? HG_UMMA_STAGES_256 : 4; }
 
-enum UEpi { UEPI_STORE_F32 = 0, UEPI_BIAS_RELU_BF16 = 1, UEPI_ATOMIC_F32 = 2, UEPI_SOFTMAX_CE = 3 };
+enum UEpi { UEPI_STORE_F32 = 0, UEPI_BIAS_RELU_BF16 = 1, UEPI_ATOMIC_F32 = 2, UEPI_SOFTMAX_CE = 3,
+            UEPI_MASK_BF16 = 4 };
 
 struct UmmaArgs {
   int M, N, K;               // host-known sizes (M/K may be overridden on device)
@@ -59,6 +60,11 @@ struct UmmaArgs {
   int ldp;                   // dl_lowp row pitch (classes rounded up to 64)
   int n_cap;                 // capacity rows: [M_dev, n_cap) get zeros
   int late_m;                // host: every capacity tile fits one wave, M_dev read late
+  // UEPI_MASK_BF16 (dz of the top layer, model.py:266-272): C = bf16(acc * (h > 0)),
+  // colsum[c] += sum over the rows of the masked values (bias gradient)
+  const __nv_bfloat16* mask;  // h [rows x ldm] bf16
+  int ldm;
+  float* colsum;
 };
 
 // Rows [r0, r1) of the head outputs past the device root count: no loss, no gradient.
@@ -256,7 +262,8 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
     // chunk) in the now idle pipeline smem, 128B-swizzled, and one lane hands
     // the box to TMA (store, or f32 add-reduce in L2 for split-K partials).
     // Rows past the device count are written as zeros (inside the capacity).
-    constexpr int EB = EPI == UEPI_BIAS_RELU_BF16 ? 2 : 4;
+    constexpr bool kBf16Out = EPI == UEPI_BIAS_RELU_BF16 || EPI == UEPI_MASK_BF16;
+    constexpr int EB = kBf16Out ? 2 : 4;
     constexpr int CW = 128 / EB;             // columns per 128-byte row
     constexpr int NCH = (BN_T + CW - 1) / CW;
     constexpr int NCW = (NCH + kEpiPerQ - 1) / kEpiPerQ;  // chunks per warp
@@ -276,6 +283,40 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
 #pragma unroll
       for (int q = 0; q < CW; q += 16) tmem_wait16(rr + q);
       uint8_t* box = stage + (ch / kEpiPerQ) * 4096 + lane * 128;
+      if constexpr (EPI == UEPI_MASK_BF16) {
+        // this row's 64 h columns (loads in flight together), mask, bf16,
+        // and the column sums of the masked values (butterfly over the warp's
+        // 32 rows, one atomic per column per warp)
+        const __nv_bfloat16* hp = args.mask + (int64_t)(valid ? row : 0) * args.ldm + n0 + c;
+        uint4 hraw[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) hraw[u] = *reinterpret_cast<const uint4*>(hp + u * 8);
+#pragma unroll
+        for (int g16 = 0; g16 < 4; ++g16) {
+          float v[16];
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int u = g16 * 2 + h2;
+            const uint32_t hw[4] = {hraw[u].x, hraw[u].y, hraw[u].z, hraw[u].w};
+            uint32_t pk[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const float m0 = __uint_as_float(hw[t] << 16), m1 = __uint_as_float(hw[t] & 0xFFFF0000u);
+              const float x0 = valid && m0 > 0.f ? __uint_as_float(rr[u * 8 + 2 * t]) : 0.f;
+              const float x1 = valid && m1 > 0.f ? __uint_as_float(rr[u * 8 + 2 * t + 1]) : 0.f;
+              v[h2 * 8 + 2 * t] = x0;
+              v[h2 * 8 + 2 * t + 1] = x1;
+              pk[t] = pack_bf2(x0, x1);
+            }
+            *reinterpret_cast<uint4*>(box + ((u ^ (lane & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+          const float cs = colsum16(v, lane);
+          const int col = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
+                          ((lane >> 1) & 1);
+          if ((lane & 1) == 0 && n0 + c + g16 * 16 + col < args.N)
+            atomicAdd(args.colsum + n0 + c + g16 * 16 + col, cs);
+        }
+      } else {
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         uint4 v;
@@ -296,6 +337,7 @@ k_umma_gemm(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ C
         }
         *reinterpret_cast<uint4*>(box + ((u ^ (lane & 7)) << 4)) = v;
       }
+      }  // not UEPI_MASK_BF16
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0)
@@ -443,9 +485,11 @@ static int launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensor
 }
 
 // Generic entry: shapes are capacities (M/K) when *_dev counts are given.
-int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb, bool b_mn,
-              void* C, int64_t ldc, int M, int N, int K, const int32_t* M_dev,
-              const int32_t* K_dev, int epi, const float* bias, int split, cudaStream_t s) {
+static int umma_gemm_ex(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
+                        bool b_mn, void* C, int64_t ldc, int M, int N, int K,
+                        const int32_t* M_dev, const int32_t* K_dev, int epi, const float* bias,
+                        int split, const __nv_bfloat16* mask, int ldm, float* colsum,
+                        cudaStream_t s) {
   if (N <= 0 || (N > 256 && N % 256)) return hg_fail(HG_ECONFIG, "umma N must be <= 256 or a multiple of 256");
   // N tile (grid.y covers the rest): the widest tile that still spreads the
   // problem over about half the SMs -- small-M GEMMs (one micrograph batch of
@@ -474,13 +518,18 @@ int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
   if (st) return st;
   // TMA epilogue when C's rows are 16-byte aligned (else row-per-thread stores)
   CUtensorMap mc;
-  const int eb = epi == UEPI_BIAS_RELU_BF16 ? 2 : 4;
+  const int eb = (epi == UEPI_BIAS_RELU_BF16 || epi == UEPI_MASK_BF16) ? 2 : 4;
   int tma_epi = ((uintptr_t)C % 16 == 0 && (ldc * eb) % 16 == 0) ? 1 : 0;
   if (tma_epi && make_map(&mc, C, (uint64_t)N, (uint64_t)M, ldc, 128 / eb, 32, eb) != HG_OK) {
     tma_epi = 0;
   }
   if (!tma_epi) memset(&mc, 0, sizeof(mc));
+  if (epi == UEPI_MASK_BF16 && !tma_epi)
+    return hg_fail(HG_ECONFIG, "masked dz epilogue needs 16-byte aligned bf16 rows");
   UmmaArgs a{M, N, K, M_dev, K_dev, C, ldc, bias, tma_epi};
+  a.mask = mask;
+  a.ldm = ldm;
+  a.colsum = colsum;
   {
     // late row count only while every capacity tile fits one wave: tiles past
     // the count then run on otherwise idle SMs; beyond a wave they would queue
@@ -504,10 +553,27 @@ int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb,
   HG_UMMA_N(false, false, UEPI_STORE_F32)
   HG_UMMA_N(true, true, UEPI_ATOMIC_F32)
   HG_UMMA_N(true, true, UEPI_STORE_F32)
+  HG_UMMA_N(false, false, UEPI_MASK_BF16)
 #undef HG_UMMA_N
 #undef HG_UMMA_CASE
   return hg_fail(HG_ECONFIG, "unsupported umma variant (a_mn=%d b_mn=%d N=%d epi=%d)", (int)a_mn,
                  (int)b_mn, N, epi);
+}
+
+int umma_gemm(const void* A, int64_t lda, bool a_mn, const void* B, int64_t ldb, bool b_mn,
+              void* C, int64_t ldc, int M, int N, int K, const int32_t* M_dev,
+              const int32_t* K_dev, int epi, const float* bias, int split, cudaStream_t s) {
+  return umma_gemm_ex(A, lda, a_mn, B, ldb, b_mn, C, ldc, M, N, K, M_dev, K_dev, epi, bias, split,
+                      nullptr, 0, nullptr, s);
+}
+
+// dz = bf16((A @ B) * (mask > 0)) with colsum += the masked column sums (both
+// operands K-major): the top layer's dz GEMM with k_mask_colsum folded in.
+int umma_gemm_mask(const void* A, int64_t lda, const void* B, int64_t ldb, __nv_bfloat16* C,
+                   int64_t ldc, int M, int N, int K, const int32_t* M_dev,
+                   const __nv_bfloat16* mask, int ldm, float* colsum, cudaStream_t s) {
+  return umma_gemm_ex(A, lda, false, B, ldb, false, C, ldc, M, N, K, M_dev, nullptr,
+                      UEPI_MASK_BF16, nullptr, 1, mask, ldm, colsum, s);
 }
 
 // Classifier head with the softmax-CE fused into the epilogue: logits
