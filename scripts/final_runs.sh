@@ -2,7 +2,7 @@
 # Final round-2 measurement set on one 4-GPU box: N = 4, 2, 1 bench lines
 # (defaults: cfg4, K = 50), the N = 1 ncu launch list, and the GPU test-suite
 # (multi-GPU tests included).
-o=gpurun_out/final
+o=${1:-gpurun_out/final}
 mkdir -p $o
 timeout 1000 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29701 bench.py --gpus 4 > $o/bench_n4.json 2> $o/bench_n4.err
 CUDA_VISIBLE_DEVICES=0,1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29702 bench.py --gpus 2 > $o/bench_n2.json 2> $o/bench_n2.err
