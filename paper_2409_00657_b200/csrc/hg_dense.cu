@@ -184,12 +184,10 @@ struct AggSegs {
 // The dependent chain per row is (self_pos, nbr_off) -> (nbr_idx, self row)
 // -> neighbour rows -> store; with ~2 rows x U loads in flight per warp the
 // ~100K-row gather of a batch keeps >100 KB in flight per SM.
-// U: neighbour loads in flight per lane -- HG_AGG_U for the layer-1 gather
-// (fanout 10 in one round, register budget of HG_AGG_MINB CTAs/SM), 16 for the
-// deeper layers (a root's <= 15 hop-1 rows in one round; one CTA per SM there)
-template <typename T, bool SAGE, int U>
-__global__ void __launch_bounds__(256, U <= HG_AGG_U ? HG_AGG_MINB : 2)
+template <typename T, bool SAGE>
+__global__ void __launch_bounds__(256, HG_AGG_MINB)
 k_aggregate(RowSrc<T> rs_in, AggSegs<T> segs, int W, int out_ld, int pad_cap) {
+  constexpr int U = HG_AGG_U;
   pdl_trigger();
   pdl_wait();
   RowSrc<T> rs = rs_in;
@@ -1008,11 +1006,9 @@ static void launch_aggregate_n(const hg_step_desc* const* ds, int n, int k, cuda
   prof_begin(k == 1 ? PROF_AGG1 : PROF_AGG2, s);
   count_launch();
   if (d->arch == 1)
-    launch_pdl(k == 1 ? k_aggregate<T, true, HG_AGG_U> : k_aggregate<T, true, 16>, dim3(grid),
-               dim3(256), 0, s, row_src<T>(d, k), segs, Wd, d->in_dim[k], pad_cap);
+    launch_pdl(k_aggregate<T, true>, dim3(grid), dim3(256), 0, s, row_src<T>(d, k), segs, Wd, d->in_dim[k], pad_cap);
   else
-    launch_pdl(k == 1 ? k_aggregate<T, false, HG_AGG_U> : k_aggregate<T, false, 16>, dim3(grid),
-               dim3(256), 0, s, row_src<T>(d, k), segs, Wd, d->in_dim[k], pad_cap);
+    launch_pdl(k_aggregate<T, false>, dim3(grid), dim3(256), 0, s, row_src<T>(d, k), segs, Wd, d->in_dim[k], pad_cap);
   prof_end(k == 1 ? PROF_AGG1 : PROF_AGG2, s);
 }
 
