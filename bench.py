@@ -339,9 +339,6 @@ def run_ours(args, cfg):
         return run_distributed(args, cfg)
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
-    if os.environ.get("HG_PRIO"):
-        with torch.cuda.stream(torch.cuda.Stream(dev, priority=-int(os.environ["HG_PRIO"]))):
-            return _run_ours(args, cfg, dev)
     return _run_ours(args, cfg, dev)
 
 

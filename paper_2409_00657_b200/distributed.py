@@ -28,7 +28,6 @@ categories and messages) so byte counts compare one for one with gnnsim;
 from __future__ import annotations
 
 import ctypes as C
-import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -361,11 +360,10 @@ class PeerFeatures:
         # pre-gather (hg_resolve_rows): the layer-1 gather then does one
         # L2-resident lookup per source row instead of home + staging-row
         # lookups by vertex id
-        if _ROW_HANDLES:
-            if getattr(runner, "row_handle", None) is None:
-                cap0 = runner.builder.tensors["need_ids"][0].numel()
-                runner.row_handle = torch.zeros(cap0, dtype=torch.int32, device=self.device)
-            d.row_handle = runner.row_handle.data_ptr()
+        if getattr(runner, "row_handle", None) is None:
+            cap0 = runner.builder.tensors["need_ids"][0].numel()
+            runner.row_handle = torch.zeros(cap0, dtype=torch.int32, device=self.device)
+        d.row_handle = runner.row_handle.data_ptr()
 
     def pregather(self, runner: CellRunner, uniq_row_ptr: int, total_ptr: int, stream,
                   it_dev_ptr=None, empty: bool = False) -> None:
@@ -435,11 +433,6 @@ class PeerFeatures:
 
 # ---------------------------------------------------------------- graph loop
 
-_DIST_PRIO = os.environ.get("HG_DIST_PRIO", "1") != "0"
-_ROW_HANDLES = os.environ.get("HG_ROW_HANDLES", "1") != "0"
-# DistGroupLoop: one deduplicated push per group (per-iteration ledger rows)
-_GROUP_PUSH = os.environ.get("HG_GROUP_PUSH", "1") != "0"
-_GROUP_GATHER = os.environ.get("HG_GROUP_GATHER", "1") != "0"
 
 
 class DistGraphLoop:
@@ -468,8 +461,7 @@ class DistGraphLoop:
         # stream priority, the SM-filling build branch at low priority
         from .engine import _streams
         self._cap_s, self.side_build = _streams(dev)
-        self.side_gather = (torch.cuda.Stream(dev, priority=-1) if _DIST_PRIO
-                            else torch.cuda.Stream(dev))
+        self.side_gather = torch.cuda.Stream(dev, priority=-1)
         self.pin_loss = [torch.zeros(1, dtype=torch.float32).pin_memory() for _ in range(3)]
         self._dummy = torch.zeros(2, dtype=torch.int64, device=dev)
         m = tr.model
@@ -612,27 +604,14 @@ class DistGroupLoop:
         iteration, cursor+1 .. cursor+G), advance the gather cursor by G, and
         run each iteration's layer-1 gather from the shared staging."""
         tr = self.tr
-        if _GROUP_PUSH:
-            tr.feats.pregather_group(self.sets[k], tr._acct_rows.data_ptr(),
-                                     tr._acct_total.data_ptr(), s, tr._g_pg.data_ptr())
-            _lib.call("hg_iter_stage_ranged", tr._g_roots.data_ptr(), tr._g_ranges.data_ptr(),
-                      tr._g_states.data_ptr(), tr.iters, tr._g_pg.data_ptr(), 0, self.G, self.G,
-                      self._dummy.data_ptr(), self._dummy.data_ptr(),
-                      self._dummy.data_ptr() + 8, s)
-            if _GROUP_GATHER:  # the group's layer-1 gathers in ONE launch (per-batch handles)
-                _lib.call("hg_step_prologue_group", self.descp[k], self.G, 1, s)
-            else:
-                for r in self.sets[k]:
-                    _lib.call("hg_step_prologue", C.byref(r.desc), self.cap, 1, s)
-            return
-        for r in self.sets[k]:
-            _lib.call("hg_iter_stage_ranged", tr._g_roots.data_ptr(), tr._g_ranges.data_ptr(),
-                      tr._g_states.data_ptr(), tr.iters, tr._g_pg.data_ptr(), 0, 1, 1,
-                      self._dummy.data_ptr(), self._dummy.data_ptr(),
-                      self._dummy.data_ptr() + 8, s)
-            tr.feats.pregather(r, tr._acct_rows.data_ptr(), tr._acct_total.data_ptr(), s,
-                               it_dev_ptr=tr._g_pg.data_ptr())
-            _lib.call("hg_step_prologue", C.byref(r.desc), self.cap, 1, s)
+        tr.feats.pregather_group(self.sets[k], tr._acct_rows.data_ptr(),
+                                 tr._acct_total.data_ptr(), s, tr._g_pg.data_ptr())
+        _lib.call("hg_iter_stage_ranged", tr._g_roots.data_ptr(), tr._g_ranges.data_ptr(),
+                  tr._g_states.data_ptr(), tr.iters, tr._g_pg.data_ptr(), 0, self.G, self.G,
+                  self._dummy.data_ptr(), self._dummy.data_ptr(),
+                  self._dummy.data_ptr() + 8, s)
+        # the group's layer-1 gathers in ONE launch (per-batch row handles)
+        _lib.call("hg_step_prologue_group", self.descp[k], self.G, 1, s)
 
     def replay(self, x: int) -> None:
         self.graphs[x].replay()

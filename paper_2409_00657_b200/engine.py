@@ -15,7 +15,6 @@ with no host synchronisation.
 from __future__ import annotations
 
 import ctypes as C
-import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -37,7 +36,7 @@ SEED_BATCHES, SEED_SAMPLER, SEED_MODEL, SEED_MERGE = 0x05, 0x06, 0x07, 0x08
 # Stream priorities of the graph loops: the training chain (latency-bound,
 # small grids) at high priority, the build / gather branch (throughput-bound,
 # fills every SM) at low priority, so freed SM slots go to training first.
-_TRAIN_PRIO = int(os.environ.get("HG_TRAIN_PRIO", "1"))
+_TRAIN_PRIO = 1
 # Resident build CTAs per SM on the graph loop's build branch (GroupLoop):
 # 3 x 256 threads x 48 registers leaves a GEMM / gather CTA room on every SM,
 # so the training branch is not starved while a group is being built.
