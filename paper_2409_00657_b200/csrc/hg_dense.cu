@@ -406,7 +406,21 @@ __global__ void k_softmax_ce(float* __restrict__ logits, int C, const int64_t* _
   if (r >= n_roots) return;
   const int lane = lane_id();
   float* x = logits + (int64_t)r * C;
-  if (n_dev && r >= *n_dev) {  // capacity rows past the device root count: no loss, no gradient
+  // the independent loads first -- the device root count, the label source
+  // and the row's logits (<= 8 per lane) -- so they share one round trip
+  // (capacity rows hold stale logits; they are only read, then zeroed)
+  constexpr int kPer = 8;
+  const int n = n_dev ? *n_dev : n_roots;
+  const int64_t root = labels ? 0 : roots[r];
+  const int lab_in = labels ? labels[r] : 0;
+  float xv[kPer];
+  const bool regs = C <= 32 * kPer;
+#pragma unroll
+  for (int t = 0; t < kPer; ++t) {
+    const int c = lane + 32 * t;
+    xv[t] = regs && c < C ? x[c] : -INFINITY;
+  }
+  if (r >= n) {  // capacity rows past the device root count: no loss, no gradient
     for (int c = lane; c < C; c += 32) x[c] = 0.f;
     if (dl_lowp)
       for (int c = lane; c < ldp; c += 32) dl_lowp[(int64_t)r * ldp + c] = __float2bfloat16_rn(0.f);
@@ -414,21 +428,43 @@ __global__ void k_softmax_ce(float* __restrict__ logits, int C, const int64_t* _
     return;
   }
   float mx = -INFINITY;
-  for (int c = lane; c < C; c += 32) mx = fmaxf(mx, x[c]);
+  if (regs) {
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) mx = fmaxf(mx, xv[t]);
+  } else {
+    for (int c = lane; c < C; c += 32) mx = fmaxf(mx, x[c]);
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   float s = 0.f;
-  for (int c = lane; c < C; c += 32) s += expf(x[c] - mx);
+  if (regs) {
+#pragma unroll
+    for (int t = 0; t < kPer; ++t)
+      if (lane + 32 * t < C) s += expf(xv[t] - mx);
+  } else {
+    for (int c = lane; c < C; c += 32) s += expf(x[c] - mx);
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  const int label = labels ? labels[r] : (int)(mix64(label_state ^ (uint64_t)roots[r]) % (uint64_t)C);
+  const int label = labels ? lab_in : (int)(mix64(label_state ^ (uint64_t)root) % (uint64_t)C);
   const float xl = x[label];
   __syncwarp();
   const float inv = 1.0f / s;
-  for (int c = lane; c < C; c += 32) {
-    const float g = expf(x[c] - mx) * inv - (c == label ? 1.f : 0.f);
-    x[c] = g;
-    if (dl_lowp) dl_lowp[(int64_t)r * ldp + c] = __float2bfloat16_rn(g);
+  if (regs) {
+#pragma unroll
+    for (int t = 0; t < kPer; ++t) {
+      const int c = lane + 32 * t;
+      if (c >= C) break;
+      const float g = expf(xv[t] - mx) * inv - (c == label ? 1.f : 0.f);
+      x[c] = g;
+      if (dl_lowp) dl_lowp[(int64_t)r * ldp + c] = __float2bfloat16_rn(g);
+    }
+  } else {
+    for (int c = lane; c < C; c += 32) {
+      const float g = expf(x[c] - mx) * inv - (c == label ? 1.f : 0.f);
+      x[c] = g;
+      if (dl_lowp) dl_lowp[(int64_t)r * ldp + c] = __float2bfloat16_rn(g);
+    }
   }
   if (dl_lowp)
     for (int c = C + lane; c < ldp; c += 32) dl_lowp[(int64_t)r * ldp + c] = __float2bfloat16_rn(0.f);
