@@ -700,6 +700,23 @@ k_scatter_top(const float* __restrict__ dagg, int ld, const int32_t* __restrict_
     const int q0 = need_off_p[r], nq = need_off_p[r + 1] - q0;
     const int rowL = need_off_c[r];
     if (!lane_on || nq == 0 || need_off_c[r + 1] - rowL != 1) continue;  // empty micrograph
+    // software pipeline: the h rows of the next four need[L-1] rows (and their
+    // in-layer flags) are in flight while this batch is computed; the first
+    // batch's loads share a round trip with the self / degree / dagg loads
+    constexpr int NV = sizeof(T) == 4 ? 2 : 1;  // 16-byte vectors per lane row
+    uint4 raw[4][NV];
+    int8_t inl[4];
+    auto fetch = [&](int i0) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int u = q0 + min(i0 + t, nq - 1);
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+          raw[t][v] = __ldg(reinterpret_cast<const uint4*>(h + (int64_t)u * H + c0) + v);
+        inl[t] = in_layer[u];
+      }
+    };
+    fetch(0);
     const int srow = self_pos[rowL];
     const int deg = nbr_off[rowL + 1] - nbr_off[rowL];
     const float* g = dagg + (int64_t)rowL * ld;
@@ -715,21 +732,21 @@ k_scatter_top(const float* __restrict__ dagg, int ld, const int32_t* __restrict_
     }
     for (int i0 = 0; i0 < nq; i0 += 4) {
       float hv[4][8];
-      int8_t inl[4];
+      int8_t il[4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {  // issue the four rows' loads first
-        const int u = q0 + min(i0 + t, nq - 1);
-        load_vec(h + (int64_t)u * H + c0, hv[t]);
-        if constexpr (sizeof(T) == 4) load_vec(h + (int64_t)u * H + c0 + 4, hv[t] + 4);
-        inl[t] = in_layer[u];
+      for (int t = 0; t < 4; ++t) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) unpack_vec<T>(raw[t][v], hv[t] + v * (8 / NV));
+        il[t] = inl[t];
       }
+      if (i0 + 4 < nq) fetch(i0 + 4);
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         if (i0 + t >= nq) break;
         const int u = q0 + i0 + t;
         // a row is the root's self row and/or one of its sampled neighbours (both
         // with a self-loop); the neighbour rows are exactly layers[L-1] (in_layer)
-        const bool self = u == srow, nbr = inl[t] != 0;
+        const bool self = u == srow, nbr = il[t] != 0;
         float v[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
