@@ -165,6 +165,7 @@ struct AggSegs {
   const int32_t* nbr_off[HG_MAX_GROUP];
   const int32_t* nbr_idx[HG_MAX_GROUP];
   const int32_t* n_rows[HG_MAX_GROUP];
+  int cap[HG_MAX_GROUP];                // row capacity (nbr_off holds cap + 1 entries)
   T* out[HG_MAX_GROUP];
   const int32_t* handle[HG_MAX_GROUP];  // staged mode: per-batch need[0] row handles
 };
@@ -221,17 +222,26 @@ k_aggregate(RowSrc<T> rs_in, AggSegs<T> segs, int W, int out_ld, int pad_cap) {
   // flight while row i's source rows load, so the dependent index chain
   // (offsets -> indices -> rows) costs one DRAM round trip per row, not three.
   int a = (blockIdx.x * warps + (threadIdx.x >> 5)) * P + gi;
+  // row metadata is loaded for any row inside the capacity (in bounds) and
+  // discarded past the device row count, so the first loads do not wait for
+  // that count
+  const int cap_rows = segs.cap[blockIdx.y];
   auto meta = [&](int r, int& j0, int& deg, int& sidx) {
     j0 = 0; deg = 0; sidx = 0;
-    if (r < n_rows) {
+    if (r < cap_rows) {
       j0 = nbr_off[r];
       deg = nbr_off[r + 1] - j0;
       sidx = self_pos[r];
     }
   };
+  auto valid_meta = [&](int r, int& j0, int& deg, int& sidx) {
+    if (r >= n_rows) { j0 = 0; deg = 0; sidx = 0; }
+  };
   int j0, deg, sidx, j0n, degn, sidxn;
   meta(a, j0, deg, sidx);
   meta(a + stride, j0n, degn, sidxn);
+  valid_meta(a, j0, deg, sidx);
+  valid_meta(a + stride, j0n, degn, sidxn);
   int idx = gl < min(G, deg) ? nbr_idx[j0 + gl] : 0;
   while (__any_sync(FULL, a < n_rows)) {
     const bool row_ok = a < n_rows;
@@ -239,6 +249,7 @@ k_aggregate(RowSrc<T> rs_in, AggSegs<T> segs, int W, int out_ld, int pad_cap) {
     const int idxn = gl < min(G, degn) ? nbr_idx[j0n + gl] : 0;
     int j0nn, degnn, sidxnn;
     meta(a + 2 * stride, j0nn, degnn, sidxnn);
+    valid_meta(a + 2 * stride, j0nn, degnn, sidxnn);
     const T* sp = rs.row(row_ok ? sidx : 0);
     const int max_deg = __reduce_max_sync(FULL, deg);
     T* o = out + (int64_t)a * out_ld;
@@ -1043,6 +1054,7 @@ static void launch_aggregate_n(const hg_step_desc* const* ds, int n, int k, cuda
     segs.nbr_off[b] = e->mg.nbr_off[k];
     segs.nbr_idx[b] = vid ? e->mg.nbr_vid1 : e->mg.nbr_idx[k];
     segs.n_rows[b] = e->mg.totals + k;
+    segs.cap[b] = e->max_rows[k];
     segs.out[b] = (T*)e->agg[k];
     cap = std::max(cap, e->max_rows[k]);
   }
